@@ -1,0 +1,255 @@
+"""CPU oracle for RaFI forwarding -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its
+``cpu_baseline`` leg and ``--impl reference`` arm) may import this package.
+The product (``paper_2605_30294_b200``) never imports it, and the two share no
+code: see ``oracle/rafi_oracle.c`` for the implementation and its citations.
+
+This module is a ctypes wrapper (argument marshalling only) around
+``oracle/liborafi.so``, which it compiles with gcc on first use if missing or
+stale.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "rafi_oracle.c")
+_LIB = os.path.join(_HERE, "liborafi.so")
+
+OK = 0
+ERR_ARG = -1
+ERR_NOMEM = -2
+ERR_RECV_OVERFLOW = -3
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (plain gcc, -O2, no fast-math, single-threaded)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + ".tmp.%d" % os.getpid()
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-fPIC", "-shared", "-o", tmp, _SRC])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = C.CDLL(build())
+        P, u64, i64, i32, vp = C.c_void_p, C.c_uint64, C.c_int64, C.c_int, C.c_void_p
+        sig = {
+            "orc_create": (P, [i32, u64, u64]),
+            "orc_destroy": (None, [P]),
+            "orc_num_incoming": (u64, [P, i32]),
+            "orc_get_incoming": (i32, [P, i32, u64, vp]),
+            "orc_emit": (i32, [P, i32, vp, i64]),
+            "orc_load_snapshot": (i32, [P, i32, vp, vp, u64, u64]),
+            "orc_set_incoming": (i32, [P, i32, vp, u64]),
+            "orc_forward_plain": (i64, [P]),
+            "orc_forward_literal": (i64, [P]),
+            "orc_pack_keys": (None, [vp, u64, vp]),
+            "orc_radix_sort_keys": (i32, [vp, u64]),
+            "orc_gather": (None, [vp, vp, u64, u64, vp, vp]),
+            "orc_compute_segments": (None, [vp, u64, i32, vp, vp]),
+            "orc_alltoall_u64": (None, [i32, vp, vp]),
+            "orc_alltoallv_bytes": (None, [i32, vp, vp, vp, vp, vp]),
+            "orc_R": (i32, [P]),
+            "orc_cap": (u64, [P]),
+            "orc_B": (u64, [P]),
+            "orc_out_ptr": (P, [P, i32]),
+            "orc_dest_ptr": (P, [P, i32]),
+            "orc_in_ptr": (P, [P, i32]),
+            "orc_binned_ptr": (P, [P, i32]),
+            "orc_emitted": (u64, [P, i32]),
+            "orc_invalid": (u64, [P, i32]),
+            "orc_dropped_last": (u64, [P, i32]),
+            "orc_invalid_last": (u64, [P, i32]),
+            "orc_C_ptr": (P, [P]),
+            "orc_send_off_ptr": (P, [P]),
+            "orc_recv_off_ptr": (P, [P]),
+            "orc_G": (u64, [P]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _view(ptr, n, dtype):
+    n = int(n)
+    dtype = np.dtype(dtype)
+    if n == 0:
+        return np.zeros(0, dtype)
+    buf = (C.c_uint8 * (n * dtype.itemsize)).from_address(ptr)
+    return np.frombuffer(buf, dtype=dtype, count=n)
+
+
+class World:
+    """R simulated ranks, each with a RaFI context of ``cap`` items of ``B`` bytes."""
+
+    def __init__(self, R: int, cap: int, B: int):
+        self.R, self.cap, self.B = int(R), int(cap), int(B)
+        self._w = lib().orc_create(self.R, self.cap, self.B)
+        if not self._w:
+            raise MemoryError("orc_create failed")
+
+    def close(self):
+        if self._w:
+            lib().orc_destroy(self._w)
+            self._w = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- device interface ------------------------------------------------
+    def emit(self, r: int, item: bytes, d: int) -> bool:
+        assert len(item) == self.B
+        buf = np.frombuffer(bytes(item), np.uint8)
+        return bool(lib().orc_emit(self._w, r, _ptr(buf), int(d)))
+
+    def emit_many(self, r: int, items: np.ndarray, dests) -> int:
+        """Sequential emits in array order; returns the number accepted."""
+        items = np.ascontiguousarray(items, dtype=np.uint8).reshape(-1, self.B)
+        acc = 0
+        for i in range(items.shape[0]):
+            acc += lib().orc_emit(self._w, r, _ptr(items[i]), int(dests[i]))
+        return acc
+
+    def load_snapshot(self, r: int, items: np.ndarray, dests: np.ndarray, ctr: int, invalid: int = 0):
+        items = np.ascontiguousarray(items, dtype=np.uint8)
+        dests = np.ascontiguousarray(dests, dtype=np.int32)
+        rc = lib().orc_load_snapshot(self._w, r, _ptr(items), _ptr(dests), int(ctr), int(invalid))
+        if rc != OK:
+            raise ValueError("orc_load_snapshot rc=%d" % rc)
+
+    def set_incoming(self, r: int, items: np.ndarray):
+        items = np.ascontiguousarray(items, dtype=np.uint8).reshape(-1)
+        n = items.size // self.B
+        rc = lib().orc_set_incoming(self._w, r, _ptr(items), n)
+        if rc != OK:
+            raise ValueError("orc_set_incoming rc=%d" % rc)
+
+    def num_incoming(self, r: int) -> int:
+        return int(lib().orc_num_incoming(self._w, r))
+
+    def incoming(self, r: int) -> np.ndarray:
+        n = self.num_incoming(r)
+        return _view(lib().orc_in_ptr(self._w, r), n * self.B, np.uint8).reshape(n, self.B).copy()
+
+    # -- forward ------------------------------------------------------------
+    def forward(self, literal: bool = False) -> int:
+        f = lib().orc_forward_literal if literal else lib().orc_forward_plain
+        return int(f(self._w))
+
+    # -- state / results of the last forward ---------------------------------
+    def emitted(self, r):
+        return int(lib().orc_emitted(self._w, r))
+
+    def invalid(self, r):
+        return int(lib().orc_invalid(self._w, r))
+
+    def dropped_last(self, r):
+        return int(lib().orc_dropped_last(self._w, r))
+
+    def invalid_last(self, r):
+        return int(lib().orc_invalid_last(self._w, r))
+
+    def out_items(self, r, n=None) -> np.ndarray:
+        if n is None:
+            n = min(self.emitted(r), self.cap)
+        return _view(lib().orc_out_ptr(self._w, r), n * self.B, np.uint8).reshape(n, self.B).copy()
+
+    def out_dests(self, r, n=None) -> np.ndarray:
+        if n is None:
+            n = min(self.emitted(r), self.cap)
+        return _view(lib().orc_dest_ptr(self._w, r), n, np.int32).copy()
+
+    def binned(self, r, n) -> np.ndarray:
+        return _view(lib().orc_binned_ptr(self._w, r), n * self.B, np.uint8).reshape(n, self.B).copy()
+
+    def C(self) -> np.ndarray:
+        return _view(lib().orc_C_ptr(self._w), self.R * self.R, np.uint64).reshape(self.R, self.R).copy()
+
+    def send_off(self) -> np.ndarray:
+        return _view(lib().orc_send_off_ptr(self._w), self.R * self.R, np.uint64).reshape(self.R, self.R).copy()
+
+    def recv_off(self) -> np.ndarray:
+        return _view(lib().orc_recv_off_ptr(self._w), self.R * self.R, np.uint64).reshape(self.R, self.R).copy()
+
+    def G(self) -> int:
+        return int(lib().orc_G(self._w))
+
+
+# -- pipeline pieces of the paper-literal forward, exposed for pinning ------
+
+def pack_keys(dests) -> np.ndarray:
+    d = np.ascontiguousarray(dests, dtype=np.int32)
+    k = np.zeros(max(d.size, 1), np.uint64)
+    lib().orc_pack_keys(_ptr(d), d.size, _ptr(k))
+    return k[: d.size]
+
+
+def radix_sort_keys(keys) -> np.ndarray:
+    k = np.array(keys, dtype=np.uint64)
+    k = np.ascontiguousarray(k) if k.size else np.zeros(1, np.uint64)
+    n = len(keys)
+    rc = lib().orc_radix_sort_keys(_ptr(k), n)
+    assert rc == OK
+    return k[:n]
+
+
+def sort_and_gather(items: np.ndarray, dests, B: int):
+    """pack_keys -> radix sort -> gather: returns (sorted items, sorted dests)."""
+    items = np.ascontiguousarray(items, dtype=np.uint8).reshape(-1)
+    n = len(dests)
+    keys = radix_sort_keys(pack_keys(dests))
+    keys = np.ascontiguousarray(keys) if n else np.zeros(1, np.uint64)
+    out = np.zeros(max(n * B, 1), np.uint8)
+    sd = np.zeros(max(n, 1), np.int32)
+    src = items if items.size else np.zeros(1, np.uint8)
+    lib().orc_gather(_ptr(src), _ptr(keys), n, B, _ptr(out), _ptr(sd))
+    return out[: n * B].reshape(n, B), sd[:n]
+
+
+def compute_segments(sorted_dests, R: int):
+    d = np.ascontiguousarray(sorted_dests, dtype=np.int32)
+    d = d if d.size else np.zeros(1, np.int32)
+    cnt = np.zeros(R, np.uint64)
+    off = np.zeros(R, np.uint64)
+    lib().orc_compute_segments(_ptr(d), len(sorted_dests), R, _ptr(cnt), _ptr(off))
+    return cnt, off
+
+
+def alltoall_u64(send: np.ndarray) -> np.ndarray:
+    send = np.ascontiguousarray(send, dtype=np.uint64)
+    R = send.shape[0]
+    recv = np.zeros((R, R), np.uint64)
+    lib().orc_alltoall_u64(R, _ptr(send), _ptr(recv))
+    return recv
+
+
+def alltoallv_bytes(sendbufs, scount, sdispl, recvbufs, rdispl):
+    """Simulated MPI_Alltoallv over lists of per-rank numpy uint8 buffers."""
+    R = len(sendbufs)
+    sp = (C.c_void_p * R)(*[b.ctypes.data for b in sendbufs])
+    rp = (C.c_void_p * R)(*[b.ctypes.data for b in recvbufs])
+    sc = np.ascontiguousarray(scount, dtype=np.uint64)
+    sd = np.ascontiguousarray(sdispl, dtype=np.uint64)
+    rd = np.ascontiguousarray(rdispl, dtype=np.uint64)
+    lib().orc_alltoallv_bytes(R, C.cast(sp, C.c_void_p), _ptr(sc), _ptr(sd), C.cast(rp, C.c_void_p), _ptr(rd))
