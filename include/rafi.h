@@ -1,0 +1,228 @@
+/*
+ * rafi.h -- C ABI of the B200-native RaFI work-item forwarding library.
+ *
+ * RaFI ("Ray Forwarding Infrastructure", arXiv 2605.30294) lets GPU kernels
+ * emit trivially copyable work items ("rays") addressed to ranks, and moves
+ * them to those ranks once per round.  This header is the host side; the
+ * device side is include/rafi_device.cuh.  Citations: PAPER:<line> (section)
+ * of the paper's LaTeX source.
+ *
+ * Conventions (all functions):
+ *   - Host-callable only.  Return a rafi_status (0 = OK, < 0 = error) unless
+ *     stated otherwise.  No C++ exception crosses this boundary.  The text of
+ *     the most recent error of the calling thread is rafi_last_error().
+ *   - Pointers are plain host or device addresses; no torch types.
+ *   - Sizes and counts are 64-bit.  Item counts per rank per round must be
+ *     < 2^32 (the paper's 32-bit index in the sort key).
+ *   - A context OWNS its queues (cudaMalloc'd).  The NCCL communicator and
+ *     the CUDA stream passed at creation are BORROWED: the caller keeps them
+ *     alive until rafi_destroy and destroys them afterwards.
+ *   - All device work of a context is ordered on its stream.
+ *   - Collective calls (rafi_create* with a communicator, rafi_resize,
+ *     rafi_forward) must be made by every process of the communicator in the
+ *     same order, across all contexts on that communicator.
+ *   - After a collective error (e.g. RAFI_ERR_RECV_OVERFLOW) the context is
+ *     unusable except for the read-only getters and rafi_destroy; such an
+ *     error is returned identically on every rank.
+ */
+#ifndef RAFI_H
+#define RAFI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RAFI_ABI_VERSION 1
+
+typedef enum {
+  RAFI_OK = 0,
+  RAFI_ERR_INVALID_ARG = -1,   /* bad argument; nothing was done */
+  RAFI_ERR_CUDA = -2,          /* a CUDA runtime call failed (see rafi_last_error) */
+  RAFI_ERR_NCCL = -3,          /* an NCCL call failed */
+  RAFI_ERR_NOMEM = -4,         /* device or pinned-host allocation failed */
+  RAFI_ERR_RECV_OVERFLOW = -5, /* some rank would receive more than its capacity (collective) */
+  RAFI_ERR_STATE = -6,         /* context is unusable after an earlier collective error */
+  RAFI_ERR_UNSUPPORTED = -7    /* valid request this build/configuration does not support */
+} rafi_status;
+
+typedef struct rafi_ctx rafi_ctx; /* opaque; owns all queues */
+
+/*
+ * The device interface ("DeviceInterface<T>"): a trivially
+ * copyable view assembled on the host and passed BY VALUE as a kernel
+ * parameter.  It holds the paper's "four pointers":
+ * the input array, the output array, the destination array and the atomic
+ * emit counter.  Re-fetch it after every rafi_forward / rafi_resize (the
+ * incoming pointer and count change).
+ */
+typedef struct {
+  const void* in;                 /* incoming items, dense, num_in * item_bytes bytes */
+  uint64_t num_in;                /* numIncoming() */
+  const uint64_t* num_in_dev;     /* the same count, device-resident */
+  void* out;                      /* outgoing queue, capacity * item_bytes bytes */
+  int32_t* dest;                  /* destination rank per outgoing slot */
+  unsigned long long* ctr;        /* atomic emit counter; NOT clamped at capacity */
+  unsigned long long* invalid;    /* emits rejected for an invalid destination */
+  uint64_t capacity;              /* items (resizeRayQueues) */
+  uint32_t item_bytes;            /* sizeof(T) */
+  int32_t num_ranks;              /* R: valid destinations are [0, R) */
+  int32_t my_rank;                /* this queue's rank in [0, R) */
+  int32_t reserved;
+} rafi_device_view;
+
+typedef struct {
+  size_t item_bytes;   /* sizeof(T) >= 1; items are packed at this stride, no padding */
+  size_t capacity;     /* max items per queue, per local rank */
+  void* nccl_comm;     /* ncclComm_t spanning all processes (BORROWED), or NULL for one process */
+  void* stream;        /* cudaStream_t (BORROWED); NULL = the legacy default stream */
+  int local_ranks;     /* logical ranks this process hosts on its device (>= 1); R = procs * local_ranks */
+  int device;          /* CUDA device ordinal, or -1 for the calling thread's current device */
+} rafi_create_params;
+
+/* Per-round statistics of one local rank (last completed rafi_forward). */
+typedef struct {
+  uint64_t round;             /* rafi_forward calls completed on this context */
+  uint64_t n_out;             /* items that entered the last forward: min(ctr, capacity) */
+  uint64_t dropped;           /* emits beyond capacity in that round */
+  uint64_t invalid;           /* emits with a destination outside [0, R) */
+  uint64_t num_in;            /* items received (= numIncoming now) */
+  uint64_t bytes_sent_remote; /* payload bytes this rank sent to other ranks */
+  uint64_t bytes_recv_remote; /* payload bytes this rank received from other ranks */
+  int64_t G;                  /* the last forward's return value */
+  int32_t num_ranks;
+  int32_t my_rank;
+  /* device time of each phase of the last forward, ms (CUDA events on the
+     context stream); 0 unless RAFI_OPT_TIMING is on.  Whole-context values:
+     one launch covers all local ranks. */
+  float ms_hist, ms_scan, ms_scatter, ms_count_exchange, ms_payload_exchange, ms_wrapup, ms_total;
+  float ms_reserved;
+  uint64_t kernel_launches;   /* cumulative kernels this context has launched */
+  uint64_t forward_launches;  /* kernels launched by the last forward */
+} rafi_stats;
+
+/* ---- options (rafi_set_option / rafi_get_option) --------------------------- */
+#define RAFI_OPT_EXCHANGE 1        /* payload exchange: RAFI_EXCHANGE_* (default AUTO) */
+#define RAFI_OPT_TIMING 2          /* 1 = record per-phase CUDA events (adds one sync); default 0 */
+#define RAFI_OPT_TILE 3            /* binning tile in items (multiple of 256); 0 = auto from item size */
+#define RAFI_OPT_SELF_DIRECT 4     /* reserved (self run placement); 0 */
+
+#define RAFI_EXCHANGE_AUTO 0       /* PEER when every rank's buffers are addressable, else NCCL */
+#define RAFI_EXCHANGE_NCCL 1       /* grouped ncclSend/ncclRecv (one local rank per process) */
+#define RAFI_EXCHANGE_PEER 2       /* copy kernel over local / CUDA-IPC peer pointers (NVLink) */
+
+/* ---- lifecycle ------------------------------------------------------------ */
+
+/* HostContext<T>(gpu, comm) + resizeRayQueues(capacity).
+ * One local rank on the current device.  nccl_comm may be NULL (R = 1).
+ * COLLECTIVE when nccl_comm spans several processes. */
+int rafi_create(rafi_ctx** out, size_t item_bytes, size_t capacity, void* nccl_comm, void* stream);
+
+/* General form; see rafi_create_params.  COLLECTIVE over nccl_comm. */
+int rafi_create_ex(rafi_ctx** out, const rafi_create_params* params);
+
+/* resizeRayQueues(N): reallocates every queue of every local
+ * rank to `capacity` items.  Incoming items are kept up to the new capacity;
+ * the outgoing queue must be empty (no emits since the last forward), else
+ * RAFI_ERR_INVALID_ARG.  Not concurrent with emits or forwards.  COLLECTIVE. */
+int rafi_resize(rafi_ctx* ctx, size_t capacity);
+
+/* Frees all queues.  Does NOT destroy the communicator or the stream.  Waits
+ * for the context's outstanding device work.  NULL is a no-op. */
+void rafi_destroy(rafi_ctx* ctx);
+
+/* ---- device interface ------------------------------------------------------- */
+
+/* getDeviceInterface() for local rank `local` in [0, local_ranks). */
+int rafi_get_device_view(const rafi_ctx* ctx, int local, rafi_device_view* out);
+
+/* numIncoming() on the host; 0 for a bad argument. */
+uint64_t rafi_num_incoming(const rafi_ctx* ctx, int local);
+
+/* Bulk emitOutgoing from the host (PAPER:70-71 semantics, one launch):
+ * appends items[i] (item_bytes each, packed) addressed to dests[i] to local
+ * rank `local`'s outgoing queue.  `items`/`dests` may be device pointers or
+ * host pointers (pinned or pageable; copied through a staging buffer on the
+ * context stream).  Invalid destinations are rejected and counted; emits past
+ * capacity are dropped and counted.  Within one call accepted items keep their
+ * relative order in the queue except across 2048-item blocks, whose order
+ * follows the atomic counter.  Asynchronous w.r.t. the host for device
+ * pointers. */
+int rafi_emit_bulk(rafi_ctx* ctx, int local, const void* items, const int32_t* dests, uint64_t n);
+
+/* ---- forwarding -------------------------------------------------------------- */
+
+/* forwardRays().  COLLECTIVE.  Bins every local rank's
+ * outgoing queue by destination (stable in slot order), exchanges counts and
+ * payloads so that each item lands in the incoming queue of the rank its emit
+ * named -- per destination, sources in rank order, each source's items in
+ * slot order -- resets the emit counters, and returns G >= 0, the total
+ * number of items received by all ranks (identical on every rank; 0 means
+ * distributed termination).  Returns a negative rafi_status on
+ * error; RAFI_ERR_RECV_OVERFLOW (some rank would receive > capacity) is
+ * detected before any payload moves and leaves all queues unchanged.
+ * The payload copy may still be in flight on the stream when this returns;
+ * anything ordered after it on the stream sees the new incoming queues. */
+int64_t rafi_forward(rafi_ctx* ctx);
+
+/* ---- introspection (host copies; ordered on the context stream, blocking) --- */
+
+int rafi_num_ranks(const rafi_ctx* ctx);                 /* R, or < 0 on error */
+int rafi_local_ranks(const rafi_ctx* ctx);               /* local ranks, or < 0 */
+int rafi_rank_of(const rafi_ctx* ctx, int local);        /* global rank of local rank, or < 0 */
+uint64_t rafi_capacity(const rafi_ctx* ctx);
+uint64_t rafi_item_bytes(const rafi_ctx* ctx);
+
+/* Copies incoming items [first, first+count) of local rank `local` to dst
+ * (host or device pointer). */
+int rafi_read_incoming(const rafi_ctx* ctx, int local, void* dst, uint64_t first, uint64_t count);
+
+/* Snapshot of the outgoing queue before forwarding: *ctr and *invalid receive
+ * the raw counters; items_dst / dests_dst (may be NULL) receive
+ * min(ctr, capacity) items / dests. */
+int rafi_read_outgoing(const rafi_ctx* ctx, int local, void* items_dst, int32_t* dests_dst,
+                       uint64_t* ctr, uint64_t* invalid);
+
+/* The destination-sorted send batch of the last forward (n_out items). */
+int rafi_read_binned(const rafi_ctx* ctx, int local, void* dst, uint64_t count);
+
+/* The last forward's R x R count matrix, row = source rank, column = destination. */
+int rafi_get_matrix(const rafi_ctx* ctx, uint64_t* C);
+
+int rafi_get_stats(const rafi_ctx* ctx, int local, rafi_stats* out);
+
+int rafi_set_option(rafi_ctx* ctx, int key, long long value);
+int rafi_get_option(const rafi_ctx* ctx, int key, long long* value);
+
+const char* rafi_status_str(int status);
+const char* rafi_last_error(void);
+int rafi_abi_version(void);
+
+/* ---- NCCL communicator helpers (the library's own NCCL, linked once) -------- */
+
+/* ncclGetUniqueId into id[128]. */
+int rafi_nccl_unique_id(void* id128);
+/* ncclCommInitRank on `device` (-1 = current); *comm receives an ncclComm_t. */
+int rafi_nccl_comm_init(void** comm, int nranks, int rank, const void* id128, int device);
+int rafi_nccl_comm_destroy(void* comm);
+
+/* ---- host-side planning (pure host code; no GPU needed) --------------------- */
+
+/* From the R x R count matrix C (row-major, C[s*R+d] = items s sends to d)
+ * computes what destination rank `d` receives: recv_count[s] = C[s][d],
+ * recv_off[s] = sum_{s'<s} C[s'][d] (prefix sums), and for each
+ * source the offset of its block for d inside its sorted batch,
+ * src_off[s] = sum_{d'<d} C[s][d'].  *total = sum_s C[s][d];
+ * *G = sum of all entries; *overflow = 1 if ANY column sum
+ * exceeds capacity (so every rank decides alike), else 0.
+ * Any output pointer may be NULL. */
+int rafi_plan(int R, const uint64_t* C, uint64_t capacity, int d, uint64_t* recv_count,
+              uint64_t* recv_off, uint64_t* src_off, uint64_t* total, uint64_t* G, int* overflow);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RAFI_H */

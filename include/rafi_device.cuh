@@ -1,0 +1,94 @@
+/*
+ * rafi_device.cuh -- device interface of RaFI, header-only.
+ *
+ *   rafi::Queue<T> q(view);            // view from rafi_get_device_view()
+ *   for (i = tid; i < q.numIncoming(); i += stride) {
+ *     T ray = q.getIncoming(i);          // any thread, any index, any order
+ *     ...
+ *     q.emitOutgoing(ray, nextRank);     // any thread, any number of times
+ *   }
+ *
+ * T is any trivially copyable type with sizeof(T) == the context's item_bytes
+ * (PAPER:40).  emitOutgoing follows the paper's atomic append
+ * with one change for B200: the lanes of a warp that emit together are
+ * aggregated, so a warp issues ONE atomicAdd on the emit counter instead of
+ * one per lane.  Slot = counter value before the add (+ the lane's rank among
+ * the emitting lanes); the item is kept iff slot < capacity ("calls that would
+ * exceed the output queue size will simply get dropped"); the
+ * counter itself is not clamped, so the host can report drops.  A destination
+ * outside [0, R) is rejected without taking a slot and counted separately.
+ */
+#ifndef RAFI_DEVICE_CUH
+#define RAFI_DEVICE_CUH
+
+#include <type_traits>
+
+#include "rafi.h"
+
+namespace rafi {
+
+__device__ __forceinline__ unsigned lane_id() {
+  unsigned l;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));
+  return l;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <class T>
+struct Queue {
+  static_assert(std::is_trivially_copyable<T>::value,
+                "RaFI items must be trivially copyable (PAPER:40)");
+  rafi_device_view v;
+
+  __host__ __device__ explicit Queue(const rafi_device_view& view) : v(view) {}
+
+  /* numIncoming(): valid on host and device. */
+  __host__ __device__ unsigned long long numIncoming() const { return v.num_in; }
+
+  /* getIncoming(i). */
+  __device__ T getIncoming(unsigned long long i) const {
+    return reinterpret_cast<const T*>(v.in)[i];
+  }
+
+  /* emitOutgoing(item, dest); returns true iff stored. */
+  __device__ bool emitOutgoing(const T& item, int dest) const {
+    const bool valid = (unsigned)dest < (unsigned)v.num_ranks;
+    const unsigned active = __activemask();
+    const unsigned vmask = __ballot_sync(active, valid);
+    const unsigned lane = lane_id();
+    if (!valid) {
+      const unsigned imask = active & ~vmask;
+      if (lane == (unsigned)(__ffs(imask) - 1)) atomicAdd(v.invalid, (unsigned long long)__popc(imask));
+      return false;
+    }
+    const unsigned leader = __ffs(vmask) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(v.ctr, (unsigned long long)__popc(vmask));
+    base = __shfl_sync(vmask, base, leader);
+    const unsigned long long slot = base + __popc(vmask & lanemask_lt());
+    if (slot >= v.capacity) return false;
+    reinterpret_cast<T*>(v.out)[slot] = item;
+    v.dest[slot] = dest;
+    return true;
+  }
+
+  __host__ __device__ int numRanks() const { return v.num_ranks; }
+  __host__ __device__ int myRank() const { return v.my_rank; }
+};
+
+/* Host helper: wrap a view, checking sizeof(T) against the context. */
+template <class T>
+inline bool make_queue(const rafi_device_view& view, Queue<T>* out) {
+  if (view.item_bytes != sizeof(T)) return false;
+  *out = Queue<T>(view);
+  return true;
+}
+
+}  // namespace rafi
+
+#endif /* RAFI_DEVICE_CUH */

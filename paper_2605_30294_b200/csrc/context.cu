@@ -1,0 +1,677 @@
+// context.cu -- host context of librafi: lifecycle, arena, the forward()
+// state machine and the C ABI entry points.
+//
+// Per local rank the arena holds (all cudaMalloc'd, so CUDA IPC works):
+//   out[cap*B]   outgoing queue, the emit target
+//   dest[cap]    int32 destination per slot
+//   binned[2]    destination-sorted send batch; two of them when peers pull
+//                over NVLink, so round k+1's scatter never overwrites what a
+//                peer may still be reading from round k (double buffer)
+//   in[cap*B]    incoming queue
+//   H, O         per-tile per-destination counts and their scan
+// plus a 64-byte control block (counters) per local rank.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace rafi_impl {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+static constexpr size_t kPad = 256;  // slack after each item buffer (vector over-reads)
+
+static int alloc_dev(void** p, size_t bytes) {
+  *p = nullptr;
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) {
+    set_error(std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+    cudaGetLastError();
+    return e == cudaErrorMemoryAllocation ? RAFI_ERR_NOMEM : RAFI_ERR_CUDA;
+  }
+  return RAFI_OK;
+}
+
+static void free_rank(LocalRank& r) {
+  cudaFree(r.out); cudaFree(r.dest); cudaFree(r.binned[0]); cudaFree(r.binned[1]);
+  cudaFree(r.in); cudaFree(r.H); cudaFree(r.O);
+  r.out = nullptr; r.dest = nullptr; r.binned[0] = r.binned[1] = nullptr; r.in = nullptr;
+  r.H = nullptr; r.O = nullptr;
+}
+
+static void close_ipc(Ctx* c) {
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  c->ipc_opened.clear();
+  c->peer_binned.clear();
+  c->peer_ok = false;
+}
+
+static bool double_buffered(const Ctx* c) { return c->nprocs > 1; }
+
+static int alloc_rank(Ctx* c, LocalRank& r, uint64_t cap) {
+  const size_t ib = (size_t)cap * c->B + kPad;
+  RAFI_CK(alloc_dev((void**)&r.out, ib));
+  RAFI_CK(alloc_dev((void**)&r.dest, (size_t)cap * 4 + kPad));
+  RAFI_CK(alloc_dev((void**)&r.binned[0], ib));
+  if (double_buffered(c)) RAFI_CK(alloc_dev((void**)&r.binned[1], ib));
+  RAFI_CK(alloc_dev((void**)&r.in, ib));
+  const size_t hb = (size_t)std::max<uint64_t>(c->max_tiles, 1) * c->R * 4 + kPad;
+  RAFI_CK(alloc_dev((void**)&r.H, hb));
+  RAFI_CK(alloc_dev((void**)&r.O, hb));
+  return RAFI_OK;
+}
+
+static int upload_rank_table(Ctx* c) {
+  std::vector<RankDev> t(c->L);
+  for (int l = 0; l < c->L; ++l) {
+    LocalRank& r = c->lr[l];
+    t[l] = RankDev{r.out, r.dest, {r.binned[0], r.binned[1] ? r.binned[1] : r.binned[0]}, r.in, r.H, r.O};
+  }
+  RAFI_CK_CUDA(cudaMemcpyAsync(c->rank_dev, t.data(), sizeof(RankDev) * c->L, cudaMemcpyHostToDevice, c->stream));
+  RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
+  return RAFI_OK;
+}
+
+// Every rank learns every rank's binned[] pointers: local ones directly,
+// other processes' through CUDA IPC handles all-gathered over NCCL.
+// Collective.  peer_ok is decided identically on all ranks.
+static int exchange_peer_pointers(Ctx* c) {
+  close_ipc(c);
+  c->peer_binned.assign((size_t)c->R * 2, nullptr);
+  for (int l = 0; l < c->L; ++l)
+    for (int b = 0; b < 2; ++b) {
+      LocalRank& r = c->lr[l];
+      c->peer_binned[(size_t)(c->proc * c->L + l) * 2 + b] = r.binned[b] ? r.binned[b] : r.binned[0];
+    }
+  if (c->nprocs == 1) { c->peer_ok = true; return RAFI_OK; }
+  const size_t per = sizeof(cudaIpcMemHandle_t) * 2 * c->L;
+  std::vector<uint8_t> mine(per), all(per * c->nprocs);
+  int ok = 1;
+  for (int l = 0; l < c->L; ++l)
+    for (int b = 0; b < 2; ++b) {
+      cudaIpcMemHandle_t h;
+      if (cudaIpcGetMemHandle(&h, c->lr[l].binned[b]) != cudaSuccess) { ok = 0; cudaGetLastError(); }
+      std::memcpy(mine.data() + sizeof(h) * (2 * l + b), &h, sizeof(h));
+    }
+  uint8_t* dbuf = nullptr;
+  RAFI_CK(alloc_dev((void**)&dbuf, per * c->nprocs + sizeof(int)));
+  int* dflag = reinterpret_cast<int*>(dbuf + per * c->nprocs);
+  int rc = RAFI_OK;
+  do {
+    if (cudaMemcpyAsync(dbuf + per * c->proc, mine.data(), per, cudaMemcpyHostToDevice, c->stream) != cudaSuccess) { rc = RAFI_ERR_CUDA; break; }
+    ncclResult_t nr = ncclAllGather(dbuf + per * c->proc, dbuf, per, ncclUint8, c->comm, c->stream);
+    if (nr != ncclSuccess) { set_error(std::string("ncclAllGather(ipc): ") + ncclGetErrorString(nr)); rc = RAFI_ERR_NCCL; break; }
+    if (cudaMemcpyAsync(all.data(), dbuf, per * c->nprocs, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess) { rc = RAFI_ERR_CUDA; break; }
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess) { rc = RAFI_ERR_CUDA; break; }
+    for (int p = 0; p < c->nprocs && ok; ++p) {
+      if (p == c->proc) continue;
+      for (int l = 0; l < c->L && ok; ++l)
+        for (int b = 0; b < 2 && ok; ++b) {
+          cudaIpcMemHandle_t h;
+          std::memcpy(&h, all.data() + per * p + sizeof(h) * (2 * l + b), sizeof(h));
+          void* ptr = nullptr;
+          if (cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            ok = 0; cudaGetLastError(); break;
+          }
+          c->ipc_opened.push_back(ptr);
+          c->peer_binned[(size_t)(p * c->L + l) * 2 + b] = (uint8_t*)ptr;
+        }
+    }
+    // agree: peer mode only if every process mapped every peer
+    if (cudaMemcpyAsync(dflag, &ok, sizeof(int), cudaMemcpyHostToDevice, c->stream) != cudaSuccess) { rc = RAFI_ERR_CUDA; break; }
+    nr = ncclAllReduce(dflag, dflag, 1, ncclInt32, ncclMin, c->comm, c->stream);
+    if (nr != ncclSuccess) { set_error(std::string("ncclAllReduce(ipc ok): ") + ncclGetErrorString(nr)); rc = RAFI_ERR_NCCL; break; }
+    int all_ok = 0;
+    if (cudaMemcpyAsync(&all_ok, dflag, sizeof(int), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess) { rc = RAFI_ERR_CUDA; break; }
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess) { rc = RAFI_ERR_CUDA; break; }
+    c->peer_ok = all_ok != 0;
+  } while (0);
+  cudaFree(dbuf);
+  if (!c->peer_ok) close_ipc(c), c->peer_binned.assign((size_t)c->R * 2, nullptr);
+  return rc;
+}
+
+static int resolve_exchange(Ctx* c) {
+  int x = c->exchange;
+  if (x == RAFI_EXCHANGE_AUTO) x = (c->nprocs == 1 || c->peer_ok) ? RAFI_EXCHANGE_PEER : RAFI_EXCHANGE_NCCL;
+  if (x == RAFI_EXCHANGE_PEER && !(c->nprocs == 1 || c->peer_ok)) {
+    set_error("PEER exchange needs every rank's buffers mapped (CUDA IPC failed)");
+    return RAFI_ERR_UNSUPPORTED;
+  }
+  if (x == RAFI_EXCHANGE_NCCL && c->L != 1) {
+    set_error("NCCL exchange supports one local rank per process");
+    return RAFI_ERR_UNSUPPORTED;
+  }
+  c->exchange_eff = x;
+  return RAFI_OK;
+}
+
+static int alloc_all(Ctx* c) {
+  c->max_tiles = (c->cap + c->tile - 1) / c->tile;
+  c->lr.assign(c->L, LocalRank{});
+  for (int l = 0; l < c->L; ++l) RAFI_CK(alloc_rank(c, c->lr[l], c->cap));
+  RAFI_CK(upload_rank_table(c));
+  return RAFI_OK;
+}
+
+static void destroy_ctx(Ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  close_ipc(c);
+  for (auto& r : c->lr) free_rank(r);
+  cudaFree(c->rank_dev); cudaFree(c->ctrl); cudaFree(c->Cdev); cudaFree(c->runs_dev); cudaFree(c->plan_dev);
+  cudaFree(c->stage);
+  cudaFreeHost(c->Chost); cudaFreeHost(c->ctrl_host); cudaFreeHost(c->runs_host); cudaFreeHost(c->plan_host);
+  for (auto& e : c->ev) if (e) cudaEventDestroy(e);
+  cudaGetLastError();
+  delete c;
+}
+
+static int create(Ctx** out, const rafi_create_params* p) {
+  *out = nullptr;
+  if (!p || p->item_bytes < 1 || p->local_ranks < 1 || p->item_bytes > (1u << 30)) {
+    set_error("rafi_create: item_bytes >= 1 and local_ranks >= 1 required");
+    return RAFI_ERR_INVALID_ARG;
+  }
+  if (p->capacity >= (1ull << 32)) {
+    set_error("rafi_create: capacity must be < 2^32 items (32-bit index in the sort key, PAPER:109)");
+    return RAFI_ERR_INVALID_ARG;
+  }
+  Ctx* c = new (std::nothrow) Ctx();
+  if (!c) return RAFI_ERR_NOMEM;
+  int dev = p->device;
+  if (dev < 0) {
+    if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); set_error("no CUDA device"); delete c; return RAFI_ERR_CUDA; }
+  }
+  c->device = dev;
+  int rc = RAFI_OK;
+  auto fail = [&](int r) { destroy_ctx(c); return r; };
+  if (cudaSetDevice(dev) != cudaSuccess) { cudaGetLastError(); set_error("cudaSetDevice failed"); return fail(RAFI_ERR_CUDA); }
+  c->stream = (cudaStream_t)p->stream;
+  c->comm = (ncclComm_t)p->nccl_comm;
+  if (c->comm) {
+    int n = 1, r = 0;
+    if (ncclCommCount(c->comm, &n) != ncclSuccess || ncclCommUserRank(c->comm, &r) != ncclSuccess) {
+      set_error("ncclCommCount/UserRank failed");
+      return fail(RAFI_ERR_NCCL);
+    }
+    c->nprocs = n; c->proc = r;
+  }
+  c->L = p->local_ranks;
+  c->R = c->nprocs * c->L;
+  c->B = p->item_bytes;
+  c->cap = p->capacity;
+  c->tile = choose_tile(c->B);
+  if ((rc = alloc_dev((void**)&c->rank_dev, sizeof(RankDev) * c->L))) return fail(rc);
+  if ((rc = alloc_dev((void**)&c->ctrl, sizeof(CtrlDev) * c->L))) return fail(rc);
+  if ((rc = alloc_dev((void**)&c->Cdev, sizeof(uint64_t) * c->R * c->R))) return fail(rc);
+  if ((rc = alloc_dev((void**)&c->runs_dev, sizeof(CopyRun) * c->L * c->R))) return fail(rc);
+  if ((rc = alloc_dev((void**)&c->plan_dev, sizeof(uint64_t) * c->L))) return fail(rc);
+  if (cudaMallocHost((void**)&c->Chost, sizeof(uint64_t) * c->R * c->R) != cudaSuccess ||
+      cudaMallocHost((void**)&c->ctrl_host, sizeof(CtrlDev) * c->L) != cudaSuccess ||
+      cudaMallocHost((void**)&c->runs_host, sizeof(CopyRun) * c->L * c->R) != cudaSuccess ||
+      cudaMallocHost((void**)&c->plan_host, sizeof(uint64_t) * c->L) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("cudaMallocHost failed");
+    return fail(RAFI_ERR_NOMEM);
+  }
+  if (cudaMemsetAsync(c->ctrl, 0, sizeof(CtrlDev) * c->L, c->stream) != cudaSuccess ||
+      cudaMemsetAsync(c->Cdev, 0, sizeof(uint64_t) * c->R * c->R, c->stream) != cudaSuccess) {
+    cudaGetLastError(); set_error("cudaMemsetAsync failed"); return fail(RAFI_ERR_CUDA);
+  }
+  for (auto& e : c->ev)
+    if (cudaEventCreate(&e) != cudaSuccess) { cudaGetLastError(); set_error("cudaEventCreate"); return fail(RAFI_ERR_CUDA); }
+  if ((rc = alloc_all(c))) return fail(rc);
+  if ((rc = exchange_peer_pointers(c))) return fail(rc);
+  if ((rc = resolve_exchange(c))) return fail(rc);
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) { cudaGetLastError(); set_error("sync"); return fail(RAFI_ERR_CUDA); }
+  *out = c;
+  return RAFI_OK;
+}
+
+// ------------------------------------------------------------------ forward
+
+static float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) { cudaGetLastError(); return 0.f; }
+  return ms;
+}
+
+static int64_t forward(Ctx* c) {
+  if (c->broken) { set_error("context unusable after an earlier collective error"); return RAFI_ERR_STATE; }
+  RAFI_CK_CUDA(cudaSetDevice(c->device));
+  const int R = c->R, L = c->L;
+  const uint64_t B = c->B;
+  c->fwd_launches = 0;
+  const bool T = c->timing;
+  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[0], c->stream));
+  // a2-a4: bin every local rank's outgoing batch by destination
+  RAFI_CK(launch_hist(c));
+  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[1], c->stream));
+  RAFI_CK(launch_scan(c));
+  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[2], c->stream));
+  RAFI_CK(launch_scatter(c));
+  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[3], c->stream));
+  // a5: every process learns the whole R x R count matrix.  The all-gather is
+  // ordered after each process's scatter on its stream, so once it completes
+  // every rank's send batch is final (what the PEER pull relies on).
+  if (c->nprocs > 1)
+    RAFI_CK_NCCL(ncclAllGather(c->Cdev + (size_t)c->proc * L * R, c->Cdev, (size_t)L * R, ncclUint64, c->comm,
+                               c->stream));
+  RAFI_CK_CUDA(cudaMemcpyAsync(c->Chost, c->Cdev, sizeof(uint64_t) * R * R, cudaMemcpyDeviceToHost, c->stream));
+  RAFI_CK_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl, sizeof(CtrlDev) * L, cudaMemcpyDeviceToHost, c->stream));
+  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[4], c->stream));
+  RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
+  // plan and the collective overflow decision (Z3)
+  uint64_t G = 0;
+  int overflow = 0;
+  for (int e = 0; e < R; ++e) {
+    uint64_t col = 0;
+    for (int s = 0; s < R; ++s) col += c->Chost[(size_t)s * R + e];
+    if (col > c->cap) overflow = 1;
+    G += col;
+  }
+  if (overflow) {
+    c->broken = true;
+    set_error("receive overflow: some rank would receive more than its capacity");
+    return RAFI_ERR_RECV_OVERFLOW;
+  }
+  std::vector<uint64_t> recv_cnt(R), recv_off(R), src_off(R);
+  for (int l = 0; l < L; ++l) {
+    const int g = c->proc * L + l;
+    uint64_t tot = 0;
+    rafi_plan(R, c->Chost, c->cap, g, recv_cnt.data(), recv_off.data(), src_off.data(), &tot, nullptr, nullptr);
+    c->plan_host[l] = tot;
+    LocalRank& r = c->lr[l];
+    r.num_in = tot;
+    r.n_out = c->ctrl_host[l].n_out;
+    r.dropped = c->ctrl_host[l].dropped;
+    r.invalid = c->ctrl_host[l].invalid_last;
+    uint64_t sent = 0, recv = 0;
+    for (int s = 0; s < R; ++s) {
+      if (s != g) {
+        sent += c->Chost[(size_t)g * R + s] * B;
+        recv += recv_cnt[s] * B;
+      }
+      CopyRun& run = c->runs_host[(size_t)l * R + s];
+      run.src = c->peer_binned.empty() ? nullptr : c->peer_binned[(size_t)s * 2 + c->cur] + src_off[s] * B;
+      run.dst = recv_off[s];
+      run.count = recv_cnt[s];
+    }
+    r.sent_remote = sent;
+    r.recv_remote = recv;
+  }
+  RAFI_CK_CUDA(cudaMemcpyAsync(c->plan_dev, c->plan_host, sizeof(uint64_t) * L, cudaMemcpyHostToDevice, c->stream));
+  // a6: payload exchange
+  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[7], c->stream));
+  if (c->exchange_eff == RAFI_EXCHANGE_PEER) {
+    RAFI_CK_CUDA(cudaMemcpyAsync(c->runs_dev, c->runs_host, sizeof(CopyRun) * L * R, cudaMemcpyHostToDevice,
+                                 c->stream));
+    uint64_t maxb = 0;
+    for (int l = 0; l < L; ++l) maxb = std::max<uint64_t>(maxb, c->plan_host[l] * B);
+    const int chunks = (int)std::min<uint64_t>((maxb + 65535) / 65536, 1u << 30);
+    if (maxb) RAFI_CK(launch_copy(c, chunks));
+  } else {  // NCCL grouped send/recv (one local rank per process)
+    const int me = c->proc;
+    uint8_t* sb = c->lr[0].binned[c->cur];
+    uint8_t* ib = c->lr[0].in;
+    rafi_plan(R, c->Chost, c->cap, me, recv_cnt.data(), recv_off.data(), nullptr, nullptr, nullptr, nullptr);
+    uint64_t soff = 0;
+    RAFI_CK_NCCL(ncclGroupStart());
+    for (int p = 0; p < R; ++p) {
+      const uint64_t sc = c->Chost[(size_t)me * R + p];
+      if (p == me) {
+        if (sc) {
+          cudaError_t e = cudaMemcpyAsync(ib + recv_off[me] * B, sb + soff * B, sc * B, cudaMemcpyDeviceToDevice, c->stream);
+          if (e != cudaSuccess) { ncclGroupEnd(); RAFI_CK_CUDA(e); }
+        }
+      } else {
+        if (sc) RAFI_CK_NCCL(ncclSend(sb + soff * B, sc * B, ncclUint8, p, c->comm, c->stream));
+        if (recv_cnt[p]) RAFI_CK_NCCL(ncclRecv(ib + recv_off[p] * B, recv_cnt[p] * B, ncclUint8, p, c->comm, c->stream));
+      }
+      soff += sc;
+    }
+    RAFI_CK_NCCL(ncclGroupEnd());
+  }
+  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[5], c->stream));
+  // a7: wrap-up: counters to 0, numIncoming = received
+  RAFI_CK(launch_wrapup(c));
+  if (T) {
+    RAFI_CK_CUDA(cudaEventRecord(c->ev[6], c->stream));
+    RAFI_CK_CUDA(cudaEventSynchronize(c->ev[6]));
+    c->st.ms_hist = ev_ms(c->ev[0], c->ev[1]);
+    c->st.ms_scan = ev_ms(c->ev[1], c->ev[2]);
+    c->st.ms_scatter = ev_ms(c->ev[2], c->ev[3]);
+    c->st.ms_count_exchange = ev_ms(c->ev[3], c->ev[4]);
+    c->st.ms_payload_exchange = ev_ms(c->ev[7], c->ev[5]);
+    c->st.ms_wrapup = ev_ms(c->ev[5], c->ev[6]);
+    c->st.ms_total = ev_ms(c->ev[0], c->ev[6]);
+  }
+  c->last_cur = c->cur;
+  if (double_buffered(c)) c->cur ^= 1;
+  c->round += 1;
+  c->last_G = (int64_t)G;  // a8: sum of all received counts, same on every rank
+  return (int64_t)G;
+}
+
+static bool bad_local(const Ctx* c, int local) { return !c || local < 0 || local >= c->L; }
+
+static bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace rafi_impl
+
+using namespace rafi_impl;
+
+extern "C" {
+
+int rafi_abi_version(void) { return RAFI_ABI_VERSION; }
+
+const char* rafi_last_error(void) { return g_last_error.c_str(); }
+
+const char* rafi_status_str(int s) {
+  switch (s) {
+    case RAFI_OK: return "RAFI_OK";
+    case RAFI_ERR_INVALID_ARG: return "RAFI_ERR_INVALID_ARG";
+    case RAFI_ERR_CUDA: return "RAFI_ERR_CUDA";
+    case RAFI_ERR_NCCL: return "RAFI_ERR_NCCL";
+    case RAFI_ERR_NOMEM: return "RAFI_ERR_NOMEM";
+    case RAFI_ERR_RECV_OVERFLOW: return "RAFI_ERR_RECV_OVERFLOW";
+    case RAFI_ERR_STATE: return "RAFI_ERR_STATE";
+    case RAFI_ERR_UNSUPPORTED: return "RAFI_ERR_UNSUPPORTED";
+    default: return "RAFI_ERR_UNKNOWN";
+  }
+}
+
+int rafi_create_ex(rafi_ctx** out, const rafi_create_params* p) {
+  if (!out) return RAFI_ERR_INVALID_ARG;
+  Ctx* c = nullptr;
+  int rc = create(&c, p);
+  if (rc != RAFI_OK) return rc;
+  // rafi_ctx is never defined: the opaque handle is the Ctx address
+  *out = reinterpret_cast<rafi_ctx*>(c);
+  return RAFI_OK;
+}
+
+int rafi_create(rafi_ctx** out, size_t item_bytes, size_t capacity, void* nccl_comm, void* stream) {
+  rafi_create_params p;
+  p.item_bytes = item_bytes;
+  p.capacity = capacity;
+  p.nccl_comm = nccl_comm;
+  p.stream = stream;
+  p.local_ranks = 1;
+  p.device = -1;
+  return rafi_create_ex(out, &p);
+}
+
+void rafi_destroy(rafi_ctx* ctx) { destroy_ctx(reinterpret_cast<Ctx*>(ctx)); }
+
+int rafi_resize(rafi_ctx* ctx, size_t capacity) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return RAFI_ERR_INVALID_ARG;
+  if (c->broken) return RAFI_ERR_STATE;
+  if (capacity >= (1ull << 32)) { set_error("capacity must be < 2^32"); return RAFI_ERR_INVALID_ARG; }
+  RAFI_CK_CUDA(cudaSetDevice(c->device));
+  RAFI_CK_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl, sizeof(CtrlDev) * c->L, cudaMemcpyDeviceToHost, c->stream));
+  RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
+  for (int l = 0; l < c->L; ++l)
+    if (c->ctrl_host[l].ctr != 0 || c->ctrl_host[l].invalid != 0) {
+      set_error("rafi_resize: outgoing queue not empty (emits since the last forward)");
+      return RAFI_ERR_INVALID_ARG;
+    }
+  std::vector<LocalRank> old = c->lr;
+  const uint64_t keep_cap = c->cap;
+  c->cap = capacity;
+  c->max_tiles = (c->cap + c->tile - 1) / c->tile;
+  c->lr.assign(c->L, LocalRank{});
+  int rc = RAFI_OK;
+  for (int l = 0; l < c->L && rc == RAFI_OK; ++l) rc = alloc_rank(c, c->lr[l], capacity);
+  if (rc != RAFI_OK) {
+    for (auto& r : c->lr) free_rank(r);
+    c->lr = old; c->cap = keep_cap; c->max_tiles = (c->cap + c->tile - 1) / c->tile;
+    return rc;
+  }
+  for (int l = 0; l < c->L; ++l) {
+    const uint64_t keep = std::min<uint64_t>(old[l].num_in, capacity);
+    if (keep) RAFI_CK_CUDA(cudaMemcpyAsync(c->lr[l].in, old[l].in, keep * c->B, cudaMemcpyDeviceToDevice, c->stream));
+    c->lr[l].num_in = keep;
+    c->plan_host[l] = keep;
+  }
+  RAFI_CK_CUDA(cudaMemcpyAsync(c->plan_dev, c->plan_host, sizeof(uint64_t) * c->L, cudaMemcpyHostToDevice, c->stream));
+  RAFI_CK(launch_wrapup(c));
+  RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
+  close_ipc(c);
+  for (auto& r : old) free_rank(r);
+  RAFI_CK(upload_rank_table(c));
+  c->cur = 0;
+  RAFI_CK(exchange_peer_pointers(c));
+  RAFI_CK(resolve_exchange(c));
+  return RAFI_OK;
+}
+
+int rafi_get_device_view(const rafi_ctx* ctx, int local, rafi_device_view* v) {
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  if (bad_local(c, local) || !v) return RAFI_ERR_INVALID_ARG;
+  const LocalRank& r = c->lr[local];
+  std::memset(v, 0, sizeof(*v));
+  v->in = r.in;
+  v->num_in = r.num_in;
+  v->num_in_dev = reinterpret_cast<const uint64_t*>(&c->ctrl[local].num_in);
+  v->out = r.out;
+  v->dest = r.dest;
+  v->ctr = &c->ctrl[local].ctr;
+  v->invalid = &c->ctrl[local].invalid;
+  v->capacity = c->cap;
+  v->item_bytes = (uint32_t)c->B;
+  v->num_ranks = c->R;
+  v->my_rank = c->proc * c->L + local;
+  return RAFI_OK;
+}
+
+uint64_t rafi_num_incoming(const rafi_ctx* ctx, int local) {
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  if (bad_local(c, local)) return 0;
+  return c->lr[local].num_in;
+}
+
+int rafi_emit_bulk(rafi_ctx* ctx, int local, const void* items, const int32_t* dests, uint64_t n) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (bad_local(c, local) || (n && (!items || !dests))) return RAFI_ERR_INVALID_ARG;
+  if (c->broken) return RAFI_ERR_STATE;
+  if (n == 0) return RAFI_OK;
+  RAFI_CK_CUDA(cudaSetDevice(c->device));
+  const uint8_t* it = static_cast<const uint8_t*>(items);
+  const int32_t* ds = dests;
+  const bool dev_items = is_device_ptr(items), dev_dests = is_device_ptr(dests);
+  if (!dev_items || !dev_dests) {
+    const size_t ib = (size_t)n * c->B, need = ((ib + 255) & ~(size_t)255) + (size_t)n * 4;
+    if (need > c->stage_bytes) {
+      RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
+      cudaFree(c->stage);
+      c->stage = nullptr; c->stage_bytes = 0;
+      RAFI_CK(alloc_dev((void**)&c->stage, need));
+      c->stage_bytes = need;
+    }
+    uint8_t* si = c->stage;
+    int32_t* sd = reinterpret_cast<int32_t*>(c->stage + ((ib + 255) & ~(size_t)255));
+    if (!dev_items) { RAFI_CK_CUDA(cudaMemcpyAsync(si, items, ib, cudaMemcpyHostToDevice, c->stream)); it = si; }
+    if (!dev_dests) { RAFI_CK_CUDA(cudaMemcpyAsync(sd, dests, (size_t)n * 4, cudaMemcpyHostToDevice, c->stream)); ds = sd; }
+  }
+  return launch_emit_bulk(c, local, it, ds, n);
+}
+
+int64_t rafi_forward(rafi_ctx* ctx) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return RAFI_ERR_INVALID_ARG;
+  return forward(c);
+}
+
+int rafi_num_ranks(const rafi_ctx* ctx) { const Ctx* c = reinterpret_cast<const Ctx*>(ctx); return c ? c->R : RAFI_ERR_INVALID_ARG; }
+int rafi_local_ranks(const rafi_ctx* ctx) { const Ctx* c = reinterpret_cast<const Ctx*>(ctx); return c ? c->L : RAFI_ERR_INVALID_ARG; }
+int rafi_rank_of(const rafi_ctx* ctx, int local) {
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  if (bad_local(c, local)) return RAFI_ERR_INVALID_ARG;
+  return c->proc * c->L + local;
+}
+uint64_t rafi_capacity(const rafi_ctx* ctx) { const Ctx* c = reinterpret_cast<const Ctx*>(ctx); return c ? c->cap : 0; }
+uint64_t rafi_item_bytes(const rafi_ctx* ctx) { const Ctx* c = reinterpret_cast<const Ctx*>(ctx); return c ? c->B : 0; }
+
+int rafi_read_incoming(const rafi_ctx* ctx, int local, void* dst, uint64_t first, uint64_t count) {
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  if (bad_local(c, local) || (count && !dst)) return RAFI_ERR_INVALID_ARG;
+  const LocalRank& r = c->lr[local];
+  if (first > r.num_in || count > r.num_in - first) return RAFI_ERR_INVALID_ARG;
+  if (!count) return RAFI_OK;
+  RAFI_CK_CUDA(cudaSetDevice(c->device));
+  RAFI_CK_CUDA(cudaMemcpyAsync(dst, r.in + first * c->B, count * c->B, cudaMemcpyDefault, c->stream));
+  RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
+  return RAFI_OK;
+}
+
+int rafi_read_outgoing(const rafi_ctx* ctx, int local, void* items_dst, int32_t* dests_dst, uint64_t* ctr,
+                       uint64_t* invalid) {
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  if (bad_local(c, local)) return RAFI_ERR_INVALID_ARG;
+  RAFI_CK_CUDA(cudaSetDevice(c->device));
+  CtrlDev h;
+  RAFI_CK_CUDA(cudaMemcpyAsync(&h, &c->ctrl[local], sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
+  const uint64_t n = std::min<uint64_t>(h.ctr, c->cap);
+  if (ctr) *ctr = h.ctr;
+  if (invalid) *invalid = h.invalid;
+  if (n && items_dst)
+    RAFI_CK_CUDA(cudaMemcpyAsync(items_dst, c->lr[local].out, n * c->B, cudaMemcpyDefault, c->stream));
+  if (n && dests_dst)
+    RAFI_CK_CUDA(cudaMemcpyAsync(dests_dst, c->lr[local].dest, n * 4, cudaMemcpyDefault, c->stream));
+  RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
+  return RAFI_OK;
+}
+
+int rafi_read_binned(const rafi_ctx* ctx, int local, void* dst, uint64_t count) {
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  if (bad_local(c, local) || (count && !dst)) return RAFI_ERR_INVALID_ARG;
+  const LocalRank& r = c->lr[local];
+  if (count > r.n_out) return RAFI_ERR_INVALID_ARG;
+  if (!count) return RAFI_OK;
+  RAFI_CK_CUDA(cudaSetDevice(c->device));
+  const uint8_t* b = r.binned[c->last_cur] ? r.binned[c->last_cur] : r.binned[0];
+  RAFI_CK_CUDA(cudaMemcpyAsync(dst, b, count * c->B, cudaMemcpyDefault, c->stream));
+  RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
+  return RAFI_OK;
+}
+
+int rafi_get_matrix(const rafi_ctx* ctx, uint64_t* Cm) {
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  if (!c || !Cm) return RAFI_ERR_INVALID_ARG;
+  std::memcpy(Cm, c->Chost, sizeof(uint64_t) * c->R * c->R);
+  return RAFI_OK;
+}
+
+int rafi_get_stats(const rafi_ctx* ctx, int local, rafi_stats* out) {
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  if (bad_local(c, local) || !out) return RAFI_ERR_INVALID_ARG;
+  *out = c->st;
+  const LocalRank& r = c->lr[local];
+  out->round = c->round;
+  out->n_out = r.n_out;
+  out->dropped = r.dropped;
+  out->invalid = r.invalid;
+  out->num_in = r.num_in;
+  out->bytes_sent_remote = r.sent_remote;
+  out->bytes_recv_remote = r.recv_remote;
+  out->G = c->last_G;
+  out->num_ranks = c->R;
+  out->my_rank = c->proc * c->L + local;
+  out->kernel_launches = c->launches;
+  out->forward_launches = c->fwd_launches;
+  return RAFI_OK;
+}
+
+int rafi_set_option(rafi_ctx* ctx, int key, long long v) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return RAFI_ERR_INVALID_ARG;
+  switch (key) {
+    case RAFI_OPT_EXCHANGE: {
+      if (v < RAFI_EXCHANGE_AUTO || v > RAFI_EXCHANGE_PEER) return RAFI_ERR_INVALID_ARG;
+      const int old = c->exchange;
+      c->exchange = (int)v;
+      int rc = resolve_exchange(c);
+      if (rc != RAFI_OK) { c->exchange = old; resolve_exchange(c); }
+      return rc;
+    }
+    case RAFI_OPT_TIMING: c->timing = v != 0; return RAFI_OK;
+    case RAFI_OPT_TILE: {
+      // only between rounds with an empty outgoing queue; re-sizes H/O
+      if (v != 0 && (v % 256 != 0 || v > 4096 || v < 256)) return RAFI_ERR_INVALID_ARG;
+      const uint32_t t = v ? (uint32_t)v : choose_tile(c->B);
+      if ((uint64_t)(c->cap + t - 1) / t > c->max_tiles) {
+        // need larger H/O
+        for (auto& r : c->lr) {
+          cudaFree(r.H); cudaFree(r.O); r.H = r.O = nullptr;
+          const size_t hb = (size_t)((c->cap + t - 1) / t) * c->R * 4 + kPad;
+          RAFI_CK(alloc_dev((void**)&r.H, hb));
+          RAFI_CK(alloc_dev((void**)&r.O, hb));
+        }
+        c->max_tiles = (c->cap + t - 1) / t;
+        RAFI_CK(upload_rank_table(c));
+      }
+      c->tile = t;
+      return RAFI_OK;
+    }
+    case RAFI_OPT_SELF_DIRECT: return v == 0 ? RAFI_OK : RAFI_ERR_UNSUPPORTED;
+    default: return RAFI_ERR_INVALID_ARG;
+  }
+}
+
+int rafi_get_option(const rafi_ctx* ctx, int key, long long* v) {
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  if (!c || !v) return RAFI_ERR_INVALID_ARG;
+  switch (key) {
+    case RAFI_OPT_EXCHANGE: *v = c->exchange_eff; return RAFI_OK;
+    case RAFI_OPT_TIMING: *v = c->timing; return RAFI_OK;
+    case RAFI_OPT_TILE: *v = c->tile; return RAFI_OK;
+    case RAFI_OPT_SELF_DIRECT: *v = 0; return RAFI_OK;
+    default: return RAFI_ERR_INVALID_ARG;
+  }
+}
+
+int rafi_nccl_unique_id(void* id128) {
+  if (!id128) return RAFI_ERR_INVALID_ARG;
+  ncclUniqueId id;
+  RAFI_CK_NCCL(ncclGetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  std::memcpy(id128, &id, sizeof(id));
+  return RAFI_OK;
+}
+
+int rafi_nccl_comm_init(void** comm, int nranks, int rank, const void* id128, int device) {
+  if (!comm || !id128 || nranks < 1 || rank < 0 || rank >= nranks) return RAFI_ERR_INVALID_ARG;
+  if (device >= 0) RAFI_CK_CUDA(cudaSetDevice(device));
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof(id));
+  ncclComm_t c = nullptr;
+  RAFI_CK_NCCL(ncclCommInitRank(&c, nranks, id, rank));
+  *comm = c;
+  return RAFI_OK;
+}
+
+int rafi_nccl_comm_destroy(void* comm) {
+  if (!comm) return RAFI_OK;
+  RAFI_CK_NCCL(ncclCommDestroy((ncclComm_t)comm));
+  return RAFI_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,140 @@
+// internal.h -- private declarations of librafi (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "rafi.h"
+
+namespace rafi_impl {
+
+void set_error(const std::string& msg);
+
+#define RAFI_CK_CUDA(expr)                                                              \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      ::rafi_impl::set_error(std::string(#expr) + ": " + cudaGetErrorString(e_));       \
+      return e_ == cudaErrorMemoryAllocation ? RAFI_ERR_NOMEM : RAFI_ERR_CUDA;           \
+    }                                                                                   \
+  } while (0)
+
+#define RAFI_CK_NCCL(expr)                                                              \
+  do {                                                                                  \
+    ncclResult_t r_ = (expr);                                                           \
+    if (r_ != ncclSuccess) {                                                            \
+      ::rafi_impl::set_error(std::string(#expr) + ": " + ncclGetErrorString(r_));       \
+      return RAFI_ERR_NCCL;                                                             \
+    }                                                                                   \
+  } while (0)
+
+#define RAFI_CK(expr)          \
+  do {                         \
+    int s_ = (expr);           \
+    if (s_ != RAFI_OK) return s_; \
+  } while (0)
+
+// Device-resident per-local-rank control block.  ctr/invalid are the
+// counters emitOutgoing bumps; the rest is written by the binning kernels.
+struct alignas(64) CtrlDev {
+  unsigned long long ctr;       // emit counter (not clamped)
+  unsigned long long invalid;   // rejected emits
+  unsigned long long num_in;    // numIncoming, device copy
+  unsigned long long n_out;     // min(ctr, cap) seen by the last forward
+  unsigned long long dropped;   // ctr - n_out of the last forward
+  unsigned long long invalid_last;
+  unsigned long long pad[2];
+};
+
+// Device table of one local rank's buffers (kernel argument array).
+struct RankDev {
+  uint8_t* out;
+  int32_t* dest;
+  uint8_t* binned[2];
+  uint8_t* in;
+  uint32_t* H;
+  uint32_t* O;
+};
+
+// Per-source run of one destination's incoming queue, for the copy kernel.
+struct CopyRun {
+  const uint8_t* src;      // first byte of the run (source batch + src_off * B)
+  unsigned long long dst;  // first item in the destination incoming queue (recv_off)
+  unsigned long long count;  // items
+};
+
+struct LocalRank {
+  uint8_t* out = nullptr;     // outgoing queue (emit target)
+  int32_t* dest = nullptr;    // destination per slot
+  uint8_t* binned[2] = {nullptr, nullptr};  // send batches (double-buffered for PEER)
+  uint8_t* in = nullptr;      // incoming queue
+  uint32_t* H = nullptr;      // per-tile per-dest counts, dest-major [R][tiles]
+  uint32_t* O = nullptr;      // exclusive scan of H in dest-major order
+  uint64_t num_in = 0;        // host copy of numIncoming
+  uint64_t n_out = 0, dropped = 0, invalid = 0;  // last forward
+  uint64_t sent_remote = 0, recv_remote = 0;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;  // borrowed; null for a single process
+  int nprocs = 1, proc = 0;   // NCCL size / rank
+  int L = 1;                  // local ranks
+  int R = 1;                  // global ranks = nprocs * L
+  uint64_t B = 0;             // item bytes
+  uint64_t cap = 0;           // capacity per queue
+  uint32_t tile = 0;          // binning tile (items)
+  uint64_t max_tiles = 0;     // ceil(cap / tile)
+  int exchange = RAFI_EXCHANGE_AUTO;
+  int exchange_eff = RAFI_EXCHANGE_PEER;
+  bool timing = false;
+  bool broken = false;
+  uint64_t round = 0;
+  int cur = 0;       // which binned buffer this round writes
+  int last_cur = 0;  // which one the last forward wrote
+  int64_t last_G = 0;
+
+  std::vector<LocalRank> lr;
+  RankDev* rank_dev = nullptr;        // [L] device copy of the buffer table
+  CtrlDev* ctrl = nullptr;            // [L] device
+  uint64_t* Cdev = nullptr;           // [R*R] count matrix, device (row s = source)
+  uint64_t* Chost = nullptr;          // [R*R] pinned host mirror
+  CtrlDev* ctrl_host = nullptr;       // [L] pinned host mirror
+  CopyRun* runs_dev = nullptr;        // [L*R] copy plan, device
+  CopyRun* runs_host = nullptr;       // [L*R] pinned
+  uint64_t* plan_dev = nullptr;       // [L] per local dest: num_in (for wrap-up)
+  uint64_t* plan_host = nullptr;      // [L] pinned
+  // peer pointers to every global rank's binned buffers ([R][2]); local ones
+  // are our own allocations, remote ones are CUDA-IPC mappings
+  std::vector<uint8_t*> peer_binned;
+  std::vector<void*> ipc_opened;      // mappings to close
+  bool peer_ok = false;
+
+  // host staging for rafi_emit_bulk from host memory
+  uint8_t* stage = nullptr;
+  size_t stage_bytes = 0;
+
+  cudaEvent_t ev[8] = {};
+  rafi_stats st{};
+  uint64_t launches = 0;
+  uint64_t fwd_launches = 0;
+};
+
+inline RankDev* rank_table(Ctx* c) { return c->rank_dev; }
+
+// kernels.cu
+uint32_t choose_tile(uint64_t item_bytes);
+int launch_emit_bulk(Ctx* c, int local, const uint8_t* items, const int32_t* dests, uint64_t n);
+int launch_hist(Ctx* c);
+int launch_scan(Ctx* c);
+int launch_scatter(Ctx* c);
+int launch_copy(Ctx* c, int nruns_per_dest);
+int launch_wrapup(Ctx* c);
+size_t scatter_smem_bytes(uint32_t tile, uint64_t item_bytes, int R);
+
+}  // namespace rafi_impl

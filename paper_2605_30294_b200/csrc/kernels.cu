@@ -1,0 +1,539 @@
+// kernels.cu -- the sm_100a kernels of the forwarding hot path.
+//
+//   k_emit_bulk   a1  bulk emitOutgoing: block-aggregated atomic append
+//   k_hist        a2  per-tile per-destination counts (replaces key gen +
+//                     radix-sort counting)
+//   k_scan        a3  exclusive scan in destination-major order: tile offsets,
+//                     send counts/offsets, the count-matrix row (replaces the
+//                     boundary kernel + D2H + host gap fill)
+//   k_scatter     a4  stable scatter into one contiguous block per
+//                     destination (replaces the gather), staged
+//                     through shared memory so that both the read of the tile
+//                     and the write of every destination run are coalesced
+//   k_copy        a6  payload exchange as a copy kernel over local or CUDA-IPC
+//                     peer pointers (NVLink), the PEER transport
+//   k_wrapup      a7  reset counters, publish numIncoming
+//
+// None of this is a dense contraction: all kernels are HBM/NVLink-bound byte
+// movers (no tensor cores).  See DESIGN.md for the rooflines.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "internal.h"
+
+namespace rafi_impl {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxK = 16;          // items per thread per tile (tile <= 4096)
+constexpr int kEmitK = 8;          // emit tile = 2048 items
+constexpr int kEmitTile = kThreads * kEmitK;
+constexpr uint32_t kFull = 0xffffffffu;
+
+// x / d for x < 2^32 / d (checked by the callers' bounds), d >= 1.
+struct FastDiv {
+  uint32_t d, m;
+  __host__ explicit FastDiv(uint32_t dd) : d(dd), m(dd <= 1 ? 0u : (uint32_t)((((uint64_t)1 << 32) + dd - 1) / dd)) {}
+  __device__ __forceinline__ uint32_t div(uint32_t x) const { return d <= 1 ? x : __umulhi(x, m); }
+};
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
+
+__device__ __forceinline__ uint64_t n_items(const CtrlDev& c, uint64_t cap) {
+  return c.ctr < cap ? c.ctr : cap;
+}
+
+// Map a flat tile index over all local ranks to (local rank, tile).
+__device__ __forceinline__ bool tile_of(uint64_t g, const CtrlDev* ctrl, int L, uint64_t cap, uint32_t T,
+                                        int* l_out, uint64_t* t_out, uint64_t* n_out, uint64_t* tiles_out) {
+  uint64_t acc = 0;
+  for (int l = 0; l < L; ++l) {
+    uint64_t n = n_items(ctrl[l], cap);
+    uint64_t tl = (n + T - 1) / T;
+    if (g < acc + tl) {
+      *l_out = l; *t_out = g - acc; *n_out = n; *tiles_out = tl;
+      return true;
+    }
+    acc += tl;
+  }
+  return false;
+}
+
+// ---------------------------------------------------------------- a1 emit
+
+template <typename U>
+__global__ void __launch_bounds__(kThreads)
+k_emit_bulk(const uint8_t* __restrict__ items, const int32_t* __restrict__ dests, uint64_t n,
+            uint8_t* __restrict__ out, int32_t* __restrict__ qdest, CtrlDev* ctrl, int R, uint64_t cap,
+            uint32_t B, uint32_t UPI, FastDiv divU) {
+  __shared__ uint16_t src_of[kEmitTile];
+  __shared__ uint32_t wtot[kWarps], wbase[kWarps];
+  __shared__ unsigned long long sbase;
+  __shared__ uint32_t snvalid;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const U* itemsU = reinterpret_cast<const U*>(items);
+  U* outU = reinterpret_cast<U*>(out);
+  for (uint64_t g = blockIdx.x; g * kEmitTile < n; g += gridDim.x) {
+    const uint64_t t0 = g * kEmitTile;
+    const uint32_t nt = (uint32_t)umin64(kEmitTile, n - t0);
+    int dk[kEmitK];
+    uint32_t rk[kEmitK];
+    uint32_t run = 0;
+#pragma unroll
+    for (int k = 0; k < kEmitK; ++k) {
+      const uint32_t il = w * 32 * kEmitK + k * 32 + lane;
+      int d = il < nt ? dests[t0 + il] : -1;
+      const bool valid = il < nt && (unsigned)d < (unsigned)R;
+      const unsigned b = __ballot_sync(kFull, valid);
+      dk[k] = valid ? d : -1;
+      rk[k] = run + __popc(b & lanemask_lt());
+      run += __popc(b);
+    }
+    if (lane == 0) wtot[w] = run;
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t acc = 0;
+      for (int i = 0; i < kWarps; ++i) { wbase[i] = acc; acc += wtot[i]; }
+      snvalid = acc;
+      sbase = acc ? atomicAdd(&ctrl->ctr, (unsigned long long)acc) : 0ull;
+      if (nt > acc) atomicAdd(&ctrl->invalid, (unsigned long long)(nt - acc));
+    }
+    __syncthreads();
+    const unsigned long long base = sbase;
+    const uint32_t nvalid = snvalid;
+#pragma unroll
+    for (int k = 0; k < kEmitK; ++k) {
+      if (dk[k] >= 0) {
+        const uint32_t p = wbase[w] + rk[k];
+        src_of[p] = (uint16_t)(w * 32 * kEmitK + k * 32 + lane);
+        if (base + p < cap) qdest[base + p] = dk[k];
+      }
+    }
+    __syncthreads();
+    const uint32_t nkeep = base >= cap ? 0u : (uint32_t)umin64(nvalid, cap - base);
+    if (UPI <= 64) {
+      const uint32_t units = nkeep * UPI;
+      for (uint32_t x = tid; x < units; x += kThreads) {
+        const uint32_t p = divU.div(x), u = x - p * UPI;
+        outU[(base + p) * UPI + u] = itemsU[(t0 + src_of[p]) * UPI + u];
+      }
+    } else {
+      for (uint32_t p = w; p < nkeep; p += kWarps)
+        for (uint32_t u = lane; u < UPI; u += 32)
+          outU[(base + p) * UPI + u] = itemsU[(t0 + src_of[p]) * UPI + u];
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- a2 histogram
+
+__global__ void __launch_bounds__(kThreads)
+k_hist(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, int L, int R, uint64_t cap,
+       uint32_t T) {
+  extern __shared__ uint32_t cnt[];  // [R]
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (uint64_t g = blockIdx.x;; g += gridDim.x) {
+    int l;
+    uint64_t t, n, tiles;
+    if (!tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) break;
+    for (int d = tid; d < R; d += kThreads) cnt[d] = 0;
+    __syncthreads();
+    const uint64_t t0 = t * T;
+    const uint32_t nt = (uint32_t)umin64(T, n - t0);
+    const int32_t* dest = rk[l].dest + t0;
+    for (uint32_t i = tid; i < (T + 0u); i += kThreads) {  // T is a multiple of kThreads
+      const int d = i < nt ? dest[i] : -1;
+      const unsigned m = __match_any_sync(kFull, d);
+      if (d >= 0 && lane == __ffs(m) - 1) atomicAdd(&cnt[d], (uint32_t)__popc(m));
+    }
+    __syncthreads();
+    uint32_t* H = rk[l].H;
+    for (int d = tid; d < R; d += kThreads) H[(uint64_t)d * tiles + t] = cnt[d];
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- a3 scan
+
+// One block per local rank: O = exclusive scan of H (dest-major, dense over
+// the rank's actual tiles); the count-matrix row of this rank; counters.
+constexpr int kScanThreads = 1024;
+constexpr int kScanV = 4;
+
+__global__ void __launch_bounds__(kScanThreads)
+k_scan(const RankDev* __restrict__ rk, CtrlDev* __restrict__ ctrl, uint64_t* __restrict__ Cmat,
+       int grank0, int R, uint64_t cap, uint32_t T) {
+  __shared__ uint32_t wsum[kScanThreads / 32];
+  __shared__ uint32_t carry_s;
+  const int l = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint64_t n = n_items(ctrl[l], cap);
+  const uint64_t tiles = (n + T - 1) / T;
+  const uint64_t M = (uint64_t)R * tiles;
+  const uint32_t* H = rk[l].H;
+  uint32_t* O = rk[l].O;
+  if (tid == 0) carry_s = 0;
+  __syncthreads();
+  for (uint64_t base = 0; base < M; base += (uint64_t)kScanThreads * kScanV) {
+    uint32_t v[kScanV];
+    uint32_t s = 0;
+#pragma unroll
+    for (int j = 0; j < kScanV; ++j) {
+      const uint64_t i = base + (uint64_t)tid * kScanV + j;
+      v[j] = i < M ? H[i] : 0u;
+      s += v[j];
+    }
+    // inclusive warp scan of s
+    uint32_t x = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      uint32_t ws = wsum[lane];
+      uint32_t z = ws;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, z, o);
+        if (lane >= o) z += y;
+      }
+      wsum[lane] = z - ws;  // exclusive
+    }
+    __syncthreads();
+    const uint32_t carry = carry_s;
+    uint32_t e = carry + wsum[w] + x - s;  // exclusive prefix of this thread's first element
+#pragma unroll
+    for (int j = 0; j < kScanV; ++j) {
+      const uint64_t i = base + (uint64_t)tid * kScanV + j;
+      if (i < M) O[i] = e;
+      e += v[j];
+    }
+    __syncthreads();
+    if (tid == kScanThreads - 1) carry_s = e;
+    __syncthreads();
+  }
+  // row of the count matrix: send_count[d] = O[(d+1)*tiles] - O[d*tiles]
+  const uint32_t total = carry_s;
+  for (int d = tid; d < R; d += kScanThreads) {
+    uint64_t c = 0;
+    if (tiles) {
+      const uint32_t a = O[(uint64_t)d * tiles];
+      const uint32_t b = (d + 1 < R) ? O[(uint64_t)(d + 1) * tiles] : total;
+      c = b - a;
+    }
+    Cmat[(uint64_t)(grank0 + l) * R + d] = c;
+  }
+  if (tid == 0) {
+    CtrlDev& c = ctrl[l];
+    c.n_out = n;
+    c.dropped = c.ctr - n;
+    c.invalid_last = c.invalid;
+  }
+}
+
+// ---------------------------------------------------------------- a4 scatter
+
+template <typename U, bool kStage>
+__global__ void __launch_bounds__(kThreads, 2)
+k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, int L, int R, uint64_t cap,
+          uint32_t T, int cur, uint32_t B, uint32_t UPI, FastDiv divU, uint32_t items_smem_bytes) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  U* items_s = reinterpret_cast<U*>(smem);
+  uint16_t* src_of = reinterpret_cast<uint16_t*>(smem + items_smem_bytes);
+  uint32_t* dpos = reinterpret_cast<uint32_t*>(smem + items_smem_bytes + ((2 * T + 15) & ~15u));
+  uint32_t* wcnt = dpos + T;           // [W][R]
+  uint32_t* wbase = wcnt + kWarps * R; // [W][R]
+  uint32_t* rstart = wbase + kWarps * R;
+  uint32_t* gbase = rstart + R;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const uint32_t K = T / kThreads;
+  for (uint64_t g = blockIdx.x;; g += gridDim.x) {
+    int l;
+    uint64_t t, n, tiles;
+    if (!tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) break;
+    const uint64_t t0 = t * T;
+    const uint32_t nt = (uint32_t)umin64(T, n - t0);
+    const uint8_t* src = rk[l].out + t0 * B;
+    if (kStage) {  // whole tile -> smem, 16-byte cp.async (LDGSTS), overlaps phase 1
+      const uint32_t n16 = (nt * B + 15) / 16;
+      for (uint32_t u = tid; u < n16; u += kThreads) cp_async16(smem + 16 * u, src + 16 * (uint64_t)u);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int x = tid; x < kWarps * R; x += kThreads) wcnt[x] = 0;
+    __syncthreads();
+    // phase 1: stable rank of each item among same-dest items of its warp
+    const int32_t* dest = rk[l].dest + t0;
+    int dk[kMaxK];
+    uint32_t rk_[kMaxK];
+#pragma unroll
+    for (int k = 0; k < kMaxK; ++k) {
+      if (k < (int)K) {
+        const uint32_t il = w * 32 * K + k * 32 + lane;
+        const int d = il < nt ? dest[il] : R;
+        const unsigned m = __match_any_sync(kFull, d);
+        uint32_t c = 0;
+        if (d < R) c = wcnt[w * R + d];
+        __syncwarp();
+        if (d < R && lane == __ffs(m) - 1) wcnt[w * R + d] = c + __popc(m);
+        __syncwarp();
+        dk[k] = d;
+        rk_[k] = c + __popc(m & lanemask_lt());
+      }
+    }
+    if (kStage) cp_async_wait_all();
+    __syncthreads();
+    // phase 2: per-dest warp bases, tile run starts, global bases
+    const uint32_t* O = rk[l].O;
+    for (int d = tid; d < R; d += kThreads) {
+      uint32_t run = 0;
+      for (int i = 0; i < kWarps; ++i) { wbase[i * R + d] = run; run += wcnt[i * R + d]; }
+      rstart[d] = run;  // tile count for now
+      gbase[d] = O[(uint64_t)d * tiles + t];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t acc = 0;
+      for (int d = 0; d < R; ++d) { const uint32_t c = rstart[d]; rstart[d] = acc; acc += c; }
+    }
+    __syncthreads();
+    // phase 3: tile-local dest-major order -> source index and global slot
+#pragma unroll
+    for (int k = 0; k < kMaxK; ++k) {
+      if (k < (int)K && dk[k] < R) {
+        const int d = dk[k];
+        const uint32_t r = wbase[w * R + d] + rk_[k];
+        const uint32_t p = rstart[d] + r;
+        src_of[p] = (uint16_t)(w * 32 * K + k * 32 + lane);
+        dpos[p] = gbase[d] + r;
+      }
+    }
+    __syncthreads();
+    // phase 4: coalesced write of every destination run
+    U* dstU = reinterpret_cast<U*>(rk[l].binned[cur]);
+    const U* srcU = kStage ? items_s : reinterpret_cast<const U*>(src);
+    if (UPI <= 64) {
+      const uint32_t units = nt * UPI;
+      for (uint32_t x = tid; x < units; x += kThreads) {
+        const uint32_t p = divU.div(x), u = x - p * UPI;
+        dstU[(uint64_t)dpos[p] * UPI + u] = srcU[(uint32_t)src_of[p] * UPI + u];
+      }
+    } else {
+      for (uint32_t p = w; p < nt; p += kWarps)
+        for (uint32_t u = lane; u < UPI; u += 32)
+          dstU[(uint64_t)dpos[p] * UPI + u] = srcU[(uint64_t)src_of[p] * UPI + u];
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- a6 copy (PEER)
+
+constexpr uint32_t kCopyChunkBytes = 64 * 1024;
+
+template <typename U>
+__global__ void __launch_bounds__(kThreads)
+k_copy(const CopyRun* __restrict__ runs, const RankDev* __restrict__ rk, int R, uint32_t UPI,
+       const uint64_t* __restrict__ tot_items) {
+  const int l = blockIdx.y;
+  const uint64_t tot_units = tot_items[l] * UPI;
+  const uint64_t CH = kCopyChunkBytes / sizeof(U);
+  const uint64_t nchunks = (tot_units + CH - 1) / CH;
+  U* dst = reinterpret_cast<U*>(rk[l].in);
+  const CopyRun* rr = runs + (uint64_t)l * R;
+  for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const uint64_t u0 = c * CH, u1 = umin64(u0 + CH, tot_units);
+    for (int s = 0; s < R; ++s) {
+      const uint64_t a = rr[s].dst * UPI, b = a + rr[s].count * UPI;
+      const uint64_t lo = umax64(a, u0), hi = umin64(b, u1);
+      if (lo >= hi) continue;
+      const U* src = reinterpret_cast<const U*>(rr[s].src);
+      uint64_t u = lo + threadIdx.x;
+      for (; u + 3 * kThreads < hi; u += 4 * kThreads) {
+        const U v0 = src[u - a], v1 = src[u - a + kThreads], v2 = src[u - a + 2 * kThreads],
+                v3 = src[u - a + 3 * kThreads];
+        dst[u] = v0; dst[u + kThreads] = v1; dst[u + 2 * kThreads] = v2; dst[u + 3 * kThreads] = v3;
+      }
+      for (; u < hi; u += kThreads) dst[u] = src[u - a];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- a7 wrap-up
+
+__global__ void k_wrapup(CtrlDev* ctrl, const uint64_t* num_in, int L) {
+  const int l = threadIdx.x;
+  if (l < L) {
+    ctrl[l].ctr = 0;
+    ctrl[l].invalid = 0;
+    ctrl[l].num_in = num_in[l];
+  }
+}
+
+// ---------------------------------------------------------------- host side
+
+static int g_num_sms = 0;
+
+static int num_sms(int device) {
+  if (!g_num_sms) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0) v = 148;
+    g_num_sms = v;
+  }
+  return g_num_sms;
+}
+
+// Largest of 16/8/4/2/1 dividing the item size and every base address.
+static uint32_t unit_for(uint64_t B, uintptr_t align_bits) {
+  for (uint32_t u = 16; u > 1; u >>= 1)
+    if (B % u == 0 && (align_bits % u) == 0) return u;
+  return 1;
+}
+
+uint32_t choose_tile(uint64_t item_bytes) {
+  // smem per tile ~ T*(B + 6); keep ~100 KB so two CTAs fit on an SM.
+  uint64_t t = (96u * 1024u) / (item_bytes + 6);
+  t = (t / kThreads) * kThreads;
+  if (t < (uint64_t)kThreads) t = kThreads;
+  if (t > (uint64_t)kThreads * kMaxK) t = kThreads * kMaxK;
+  return (uint32_t)t;
+}
+
+static bool stage_tile(uint32_t T, uint64_t B) { return (uint64_t)T * B <= 128u * 1024u; }
+
+size_t scatter_smem_bytes(uint32_t T, uint64_t B, int R) {
+  const size_t items = stage_tile(T, B) ? (((size_t)T * B + 15) & ~(size_t)15) : 0;
+  return items + ((2 * (size_t)T + 15) & ~(size_t)15) + 4 * (size_t)T + 4 * (2 * (size_t)kWarps * R + 2 * (size_t)R);
+}
+
+int launch_emit_bulk(Ctx* c, int local, const uint8_t* items, const int32_t* dests, uint64_t n) {
+  if (n == 0) return RAFI_OK;
+  LocalRank& L = c->lr[local];
+  const uint32_t unit = unit_for(c->B, (uintptr_t)items | (uintptr_t)L.out);
+  const uint32_t UPI = (uint32_t)(c->B / unit);
+  const FastDiv dv(UPI);
+  const uint64_t tiles = (n + kEmitTile - 1) / kEmitTile;
+  const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)num_sms(c->device) * 8);
+  CtrlDev* ctrl = c->ctrl + local;
+#define EMIT_LAUNCH(T_)                                                                             \
+  k_emit_bulk<T_><<<grid, kThreads, 0, c->stream>>>(items, dests, n, L.out, L.dest, ctrl, c->R, c->cap, \
+                                                   (uint32_t)c->B, UPI, dv)
+  switch (unit) {
+    case 16: EMIT_LAUNCH(uint4); break;
+    case 8: EMIT_LAUNCH(uint2); break;
+    case 4: EMIT_LAUNCH(uint32_t); break;
+    case 2: EMIT_LAUNCH(uint16_t); break;
+    default: EMIT_LAUNCH(uint8_t); break;
+  }
+#undef EMIT_LAUNCH
+  RAFI_CK_CUDA(cudaGetLastError());
+  c->launches += 1;
+  return RAFI_OK;
+}
+
+static int persistent_grid(Ctx* c, int per_sm) {
+  const uint64_t max_tiles_all = c->max_tiles * (uint64_t)c->L;
+  return (int)std::max<uint64_t>(1, std::min<uint64_t>(max_tiles_all, (uint64_t)num_sms(c->device) * per_sm));
+}
+
+int launch_hist(Ctx* c) {
+  const int grid = persistent_grid(c, 8);
+  k_hist<<<grid, kThreads, sizeof(uint32_t) * c->R, c->stream>>>(rank_table(c), c->ctrl, c->L, c->R, c->cap,
+                                                                 c->tile);
+  RAFI_CK_CUDA(cudaGetLastError());
+  c->launches += 1; c->fwd_launches += 1;
+  return RAFI_OK;
+}
+
+int launch_scan(Ctx* c) {
+  k_scan<<<c->L, kScanThreads, 0, c->stream>>>(rank_table(c), c->ctrl, c->Cdev, c->proc * c->L, c->R, c->cap,
+                                               c->tile);
+  RAFI_CK_CUDA(cudaGetLastError());
+  c->launches += 1; c->fwd_launches += 1;
+  return RAFI_OK;
+}
+
+template <typename U>
+static int launch_scatter_t(Ctx* c, uint32_t UPI, int grid, size_t smem, bool stage) {
+  const FastDiv dv(UPI);
+  const uint32_t items_smem = stage ? (uint32_t)(((uint64_t)c->tile * c->B + 15) & ~(uint64_t)15) : 0u;
+  if (stage) {
+    auto k = k_scatter<U, true>;
+    RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, kThreads, smem, c->stream>>>(rank_table(c), c->ctrl, c->L, c->R, c->cap, c->tile, c->cur,
+                                          (uint32_t)c->B, UPI, dv, items_smem);
+  } else {
+    auto k = k_scatter<U, false>;
+    RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, kThreads, smem, c->stream>>>(rank_table(c), c->ctrl, c->L, c->R, c->cap, c->tile, c->cur,
+                                          (uint32_t)c->B, UPI, dv, items_smem);
+  }
+  RAFI_CK_CUDA(cudaGetLastError());
+  return RAFI_OK;
+}
+
+int launch_scatter(Ctx* c) {
+  const uint32_t unit = unit_for(c->B, 0);
+  const uint32_t UPI = (uint32_t)(c->B / unit);
+  const bool stage = stage_tile(c->tile, c->B);
+  const size_t smem = scatter_smem_bytes(c->tile, c->B, c->R);
+  const int per_sm = smem <= 110 * 1024 ? 2 : 1;
+  const int grid = persistent_grid(c, per_sm);
+  int rc;
+  switch (unit) {
+    case 16: rc = launch_scatter_t<uint4>(c, UPI, grid, smem, stage); break;
+    case 8: rc = launch_scatter_t<uint2>(c, UPI, grid, smem, stage); break;
+    case 4: rc = launch_scatter_t<uint32_t>(c, UPI, grid, smem, stage); break;
+    case 2: rc = launch_scatter_t<uint16_t>(c, UPI, grid, smem, stage); break;
+    default: rc = launch_scatter_t<uint8_t>(c, UPI, grid, smem, stage); break;
+  }
+  if (rc == RAFI_OK) { c->launches += 1; c->fwd_launches += 1; }
+  return rc;
+}
+
+int launch_copy(Ctx* c, int max_chunks) {
+  const uint32_t unit = unit_for(c->B, 0);
+  const uint32_t UPI = (uint32_t)(c->B / unit);
+  int gx = (int)std::max<int64_t>(1, std::min<int64_t>(max_chunks, (int64_t)num_sms(c->device) * 8 / c->L));
+  dim3 grid(gx, c->L);
+#define COPY_LAUNCH(T_) \
+  k_copy<T_><<<grid, kThreads, 0, c->stream>>>(c->runs_dev, rank_table(c), c->R, UPI, c->plan_dev)
+  switch (unit) {
+    case 16: COPY_LAUNCH(uint4); break;
+    case 8: COPY_LAUNCH(uint2); break;
+    case 4: COPY_LAUNCH(uint32_t); break;
+    case 2: COPY_LAUNCH(uint16_t); break;
+    default: COPY_LAUNCH(uint8_t); break;
+  }
+#undef COPY_LAUNCH
+  RAFI_CK_CUDA(cudaGetLastError());
+  c->launches += 1; c->fwd_launches += 1;
+  return RAFI_OK;
+}
+
+int launch_wrapup(Ctx* c) {
+  k_wrapup<<<1, 32 * ((c->L + 31) / 32), 0, c->stream>>>(c->ctrl, c->plan_dev, c->L);
+  RAFI_CK_CUDA(cudaGetLastError());
+  c->launches += 1; c->fwd_launches += 1;
+  return RAFI_OK;
+}
+
+}  // namespace rafi_impl

@@ -92,7 +92,7 @@ def make_dests(pattern: str, seed: int, src: int, rnd: int, n: int, R: int, seq0
         d = (seq % np.uint64(R)).astype(np.int64)
     elif pattern == "skewed":
         u = (h >> np.uint64(32)).astype(np.uint64)
-        stay = u < np.uint64(int(0.9 * 2**32))
+        stay = u < np.uint64(SKEW_STAY)
         if R == 1:
             nb = np.zeros(n, np.int64)
         else:
@@ -102,10 +102,28 @@ def make_dests(pattern: str, seed: int, src: int, rnd: int, n: int, R: int, seq0
     else:
         raise ValueError("unknown pattern %r" % pattern)
     if invalid_frac > 0.0:
-        v = (h & np.uint64(0xFFFFFFFF)).astype(np.float64) / 2.0**32
-        bad = v < invalid_frac
+        bad = (h & np.uint64(0xFFFFFFFF)) < np.uint64(invalid_threshold(invalid_frac))
         d = np.where(bad, np.where((seq & np.uint64(1)) == 0, -1, R), d)
     return d.astype(np.int32)
+
+
+def invalid_threshold(frac: float) -> int:
+    """Integer threshold on the low 32 bits of h for an invalid-dest fraction."""
+    return int(frac * 2**32)
+
+
+SKEW_STAY = int(0.9 * 2**32)  # 3865470566: P(stay on own rank) in the skewed pattern
+
+PATTERNS = {"uniform": 0, "self": 1, "ring": 2, "all_to_one": 3, "round_robin": 4, "skewed": 5}
+
+
+def walk_dests(seed: int, rnd: int, ids: np.ndarray, R: int) -> np.ndarray:
+    """Random-walk destination of each item id in round ``rnd`` (cfg1 driver):
+    multiply-shift of splitmix64(seed ^ (rnd << 40) ^ id)."""
+    ids = np.asarray(ids, dtype=np.uint64)
+    h = splitmix64(np.uint64(seed) ^ (np.uint64(rnd) << np.uint64(40)) ^ ids)
+    with np.errstate(over="ignore"):
+        return (((h >> np.uint64(32)) * np.uint64(R)) >> np.uint64(32)).astype(np.int32)
 
 
 def item_id_of(items: np.ndarray) -> np.ndarray:

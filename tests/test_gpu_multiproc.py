@@ -1,0 +1,78 @@
+"""Multi-GPU parity: one process per GPU, NCCL communicator, both payload
+transports (PEER copy kernel over CUDA-IPC NVLink pointers; NCCL grouped
+send/recv).  Every rank checks its own outputs bit-exactly against the oracle
+run on all ranks' snapshots (P1)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+    pytest.skip("needs >= 2 CUDA GPUs", allow_module_level=True)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, B, n, pattern, exchange, rounds):
+    import torch.distributed as dist
+
+    import oracle
+    import synth
+    from paper_2605_30294_b200 import rafi
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    obj = [rafi.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    comm = rafi.nccl_comm_init(world, rank, obj[0], rank)
+    cap = n * world
+    ctx = rafi.Context(B, cap, comm=comm, stream=torch.cuda.current_stream())
+    ctx.set_option(rafi.OPT_EXCHANGE, exchange)
+    assert ctx.get_option(rafi.OPT_EXCHANGE) == exchange
+    assert ctx.num_ranks == world and ctx.rank_of(0) == rank
+    for rnd in range(rounds):
+        m = n if rnd % 2 == 0 else n // 3
+        it = synth.make_items(rank, rnd, m, max(B, 16))[:, :B].copy()
+        ds = synth.make_dests(pattern, 7 + rnd, rank, rnd, m, world, invalid_frac=0.01)
+        ctx.emit_bulk(torch.from_numpy(it).cuda(), torch.from_numpy(ds).cuda(), m)
+        snap = ctx.read_outgoing(0)
+        snaps = [None] * world
+        dist.all_gather_object(snaps, snap)
+        w = oracle.World(world, cap, B)
+        for s, (items, dests, ctr, inv) in enumerate(snaps):
+            w.load_snapshot(s, items, dests, ctr, inv)
+        G_o = w.forward()
+        G = ctx.forward_rc()
+        assert G == G_o, (rank, G, G_o)
+        assert np.array_equal(ctx.matrix(), w.C())
+        st = ctx.stats()
+        assert st["num_in"] == w.num_incoming(rank)
+        assert np.array_equal(ctx.read_binned(0, st["n_out"]), w.binned(rank, st["n_out"]))
+        assert np.array_equal(ctx.read_incoming(0), w.incoming(rank))
+    # termination: nothing emitted anywhere -> 0 on every rank
+    assert ctx.forward() == 0
+    ctx.close()
+    rafi.nccl_comm_destroy(comm)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("exchange", [1, 2])  # NCCL, PEER
+@pytest.mark.parametrize("B,pattern", [(48, "uniform"), (44, "skewed"), (16, "all_to_one")])
+def test_multigpu_snapshot_parity(world, exchange, B, pattern):
+    if torch.cuda.device_count() < world:
+        pytest.skip("needs %d GPUs" % world)
+    import torch.multiprocessing as mp
+    mp.spawn(_worker, args=(world, _free_port(), B, 30011, pattern, exchange, 3), nprocs=world, join=True)

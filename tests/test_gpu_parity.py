@@ -1,0 +1,235 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Single-process cases, including R logical ranks hosted on one GPU
+(local_ranks = R), which run the same kernels and the PEER copy path with
+local pointers.  Every comparison is bit-exact (integer/byte work).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from helpers import canonical, make_inputs, oracle_sequential, p1_forward
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA GPU", allow_module_level=True)
+
+from paper_2605_30294_b200 import rafi  # noqa: E402
+
+
+def _ctx(B, cap, L=1, **kw):
+    return rafi.Context(B, cap, local_ranks=L, **kw)
+
+
+def _emit_all(ctx, inputs, device=True):
+    for l, (it, ds) in enumerate(inputs):
+        if device:
+            ctx.emit_bulk(torch.from_numpy(it).cuda(), torch.from_numpy(ds).cuda(), len(ds), local=l)
+        else:
+            ctx.emit_bulk(it, ds, len(ds), local=l)
+
+
+# ------------------------------------------------------------------ emission
+
+@pytest.mark.parametrize("B", [3, 4, 16, 44, 48, 128, 520])
+@pytest.mark.parametrize("device", [True, False])
+def test_emit_bulk_queue_contents(B, device):
+    n, L = 10007, 3
+    inputs = make_inputs(L, n, B, "uniform", 11, invalid_frac=0.03)
+    with _ctx(B, 2 * n, L) as ctx:
+        _emit_all(ctx, inputs, device)
+        for l, (it, ds) in enumerate(inputs):
+            items, dests, ctr, inv = ctx.read_outgoing(l)
+            ok = (ds >= 0) & (ds < L)
+            assert ctr == ok.sum() and inv == (~ok).sum()
+            # the queue holds exactly the accepted (item, dest) pairs (a permutation of 2048-blocks)
+            got = np.concatenate([items, dests.view(np.uint8).reshape(-1, 4)], axis=1)
+            exp = np.concatenate([it[ok], ds[ok].view(np.uint8).reshape(-1, 4)], axis=1)
+            gv = np.sort(got.view(np.dtype((np.void, got.shape[1]))).ravel())
+            ev = np.sort(exp.view(np.dtype((np.void, exp.shape[1]))).ravel())
+            assert np.array_equal(gv, ev)
+
+
+def test_emit_drop_rule():
+    """Z1: capacity 5000, 3 bulk emits of 2000 -> ctr 6000, 5000 stored, 1000 dropped."""
+    B = 16
+    with _ctx(B, 5000, 1) as ctx:
+        for k in range(3):
+            it = synth.make_items(0, 0, 2000, B, seq0=2000 * k)
+            ctx.emit_bulk(it, np.zeros(2000, np.int32))
+        items, dests, ctr, inv = ctx.read_outgoing(0)
+        assert ctr == 6000 and len(items) == 5000
+        w, G = p1_forward(ctx, 1, B)
+        assert G == 5000 and ctx.stats()["dropped"] == 1000
+
+
+# ------------------------------------------------------------------ forward, P1
+
+CASES = [
+    # (B, L, n per rank, pattern)
+    (4, 1, 5000, "uniform"), (16, 1, 0, "uniform"), (48, 1, 100000, "uniform"),
+    (8, 2, 7777, "uniform"), (12, 3, 4099, "skewed"), (16, 2, 4096, "ring"),
+    (24, 4, 20001, "uniform"), (32, 2, 4096, "uniform"), (40, 5, 3333, "round_robin"),
+    (44, 4, 50000, "uniform"), (48, 8, 30000, "uniform"), (64, 8, 12345, "skewed"),
+    (96, 3, 9000, "all_to_one"), (128, 4, 7000, "uniform"), (3, 2, 6000, "uniform"),
+    (20, 7, 5001, "uniform"), (520, 3, 2000, "uniform"), (200, 2, 3000, "self"),
+]
+
+
+@pytest.mark.parametrize("B,L,n,pattern", CASES)
+def test_forward_snapshot_parity(B, L, n, pattern):
+    inputs = make_inputs(L, n, B, pattern, 1234 + B, invalid_frac=0.01)
+    cap = max(n * L, 1)
+    with _ctx(B, cap, L) as ctx:
+        _emit_all(ctx, inputs)
+        p1_forward(ctx, L, B)
+        # a second round on the same context (counters reset, buffers reused)
+        inputs2 = make_inputs(L, n // 2, B, pattern, 99 + B, rnd=1)
+        _emit_all(ctx, inputs2)
+        p1_forward(ctx, L, B)
+
+
+@pytest.mark.parametrize("tile", [256, 512, 1024, 4096])
+def test_tile_sizes(tile):
+    B, L, n = 48, 4, 20000
+    inputs = make_inputs(L, n, B, "uniform", 5)
+    with _ctx(B, n * L, L) as ctx:
+        ctx.set_option(rafi.OPT_TILE, tile)
+        _emit_all(ctx, inputs)
+        p1_forward(ctx, L, B)
+
+
+@pytest.mark.parametrize("B,L,n,pattern", [(16, 1, 3000, "uniform"), (32, 2, 4096, "uniform"),
+                                           (48, 4, 5000, "skewed"), (44, 3, 2500, "all_to_one"),
+                                           (64, 8, 1500, "uniform")])
+def test_forward_canonical_parity(B, L, n, pattern):
+    """P2: GPU result == sequential oracle after canonical ordering by id."""
+    inputs = make_inputs(L, n, B, pattern, 77, invalid_frac=0.02)
+    cap = n * L
+    w = oracle_sequential(L, cap, B, inputs)
+    G_o = w.forward()
+    with _ctx(B, cap, L) as ctx:
+        _emit_all(ctx, inputs)
+        assert ctx.forward() == G_o
+        assert np.array_equal(ctx.matrix(), w.C())
+        for l in range(L):
+            assert np.array_equal(canonical(ctx.read_incoming(l)), canonical(w.incoming(l)))
+            assert ctx.stats(l)["invalid"] == w.invalid_last(l)
+
+
+# ------------------------------------------------------------------ edge cases
+
+def test_empty_forward_is_termination():
+    with _ctx(32, 100, 3) as ctx:
+        assert ctx.forward() == 0
+        assert all(ctx.num_incoming(l) == 0 for l in range(3))
+        assert ctx.forward() == 0
+
+
+def test_receive_overflow_collective_and_state_unchanged():
+    B, cap = 16, 100
+    with _ctx(B, cap, 2) as ctx:
+        for l in range(2):
+            ctx.emit_bulk(synth.make_items(l, 0, 60, B), np.ones(60, np.int32), local=l)
+        assert ctx.forward_rc() == rafi.ERR_RECV_OVERFLOW
+        for l in range(2):
+            _, _, ctr, _ = ctx.read_outgoing(l)
+            assert ctr == 60 and ctx.num_incoming(l) == 0
+        assert ctx.forward_rc() == rafi.ERR_STATE
+
+
+def test_exact_capacity_receive():
+    B, cap = 16, 128
+    with _ctx(B, cap, 2) as ctx:
+        for l in range(2):
+            ctx.emit_bulk(synth.make_items(l, 0, 64, B), np.ones(64, np.int32), local=l)
+        p1_forward(ctx, 2, B)
+        assert ctx.num_incoming(1) == 128
+
+
+def test_device_view_and_resize():
+    B = 32
+    with _ctx(B, 1000, 2) as ctx:
+        v = ctx.device_view(1)
+        assert v.capacity == 1000 and v.item_bytes == B and v.num_ranks == 2 and v.my_rank == 1
+        inputs = make_inputs(2, 700, B, "uniform", 3)
+        _emit_all(ctx, inputs)
+        w, _ = p1_forward(ctx, 2, B)
+        before = [ctx.read_incoming(l) for l in range(2)]
+        ctx.resize(5000)
+        assert ctx.capacity == 5000
+        for l in range(2):
+            assert np.array_equal(ctx.read_incoming(l), before[l])
+        inputs = make_inputs(2, 2400, B, "uniform", 4, rnd=1)
+        _emit_all(ctx, inputs)
+        p1_forward(ctx, 2, B)
+
+
+# ------------------------------------------------------------------ device-side emit
+
+@pytest.mark.parametrize("B", [16, 32, 44, 48, 64, 128])
+@pytest.mark.parametrize("pattern", ["uniform", "skewed", "round_robin"])
+def test_device_emit_matches_generator(B, pattern):
+    """rafi::Queue<T>::emitOutgoing (warp-aggregated) from the proxy emitter:
+    the queue holds exactly synth's items/dests (the generator's two
+    implementations agree), invalid dests rejected and counted."""
+    L, n, seed = 3, 9001, 42
+    thr = synth.invalid_threshold(0.02)
+    with _ctx(B, 2 * n, L) as ctx:
+        for l in range(L):
+            ctx.drv_emit_synthetic(synth.PATTERNS[pattern], seed, 5, n, local=l, invalid_threshold=thr)
+        for l in range(L):
+            items, dests, ctr, inv = ctx.read_outgoing(l)
+            exp_it = synth.make_items(l, 5, n, B)
+            exp_d = synth.make_dests(pattern, seed, l, 5, n, L, invalid_frac=0.02)
+            ok = (exp_d >= 0) & (exp_d < L)
+            assert ctr == ok.sum() and inv == (~ok).sum()
+            order = np.argsort(synth.item_id_of(items))
+            assert np.array_equal(items[order], exp_it[ok])
+            assert np.array_equal(dests[order], exp_d[ok])
+        p1_forward(ctx, L, B)
+
+
+def test_random_walk_cfg1_shape():
+    """cfg1 (BASELINE configs[0]): 2 ranks, 4096 x 32-B items each, uniform
+    destinations, 3 forwarding rounds, then termination; canonical parity of
+    every round against the sequential oracle."""
+    L, n, B, seed = 2, 4096, 32, synth.CONFIG_SEEDS[1]
+    w = oracle.World(L, n * L, B)
+    with _ctx(B, n * L, L) as ctx:
+        for l in range(L):
+            ctx.drv_emit_synthetic(synth.PATTERNS["uniform"], seed, 0, n, local=l)
+            w.emit_many(l, synth.make_items(l, 0, n, B), synth.make_dests("uniform", seed, l, 0, n, L))
+        Gs = []
+        for k in range(1, 5):
+            G = ctx.forward()
+            assert G == w.forward()
+            Gs.append(G)
+            for l in range(L):
+                assert np.array_equal(canonical(ctx.read_incoming(l)), canonical(w.incoming(l)))
+            # app step k: re-emit every incoming item (rounds 1..3), then stop
+            ctx.drv_random_walk(seed, k, 3)
+            if k <= 3:
+                for l in range(L):
+                    inc = w.incoming(l).copy()
+                    inc[:, 4:8] = np.frombuffer(np.uint32(k).tobytes(), np.uint8)
+                    w.emit_many(l, inc, synth.walk_dests(seed, k, synth.item_id_of(inc), L))
+        assert Gs[:3] == [2 * n] * 3
+        assert ctx.forward() == w.forward() == 0
+
+
+# ------------------------------------------------------------------ full size (bench shape)
+
+@pytest.mark.parametrize("L,n", [(1, 16 * 1024 * 1024), (8, 2 * 1024 * 1024)])
+def test_full_size_cfg2_shape(L, n):
+    """BASELINE configs[1] per-rank shape (16M x 48-B items, uniform) at R=1,
+    and 8 logical ranks x 2M on one GPU; P1 bit-exact on everything."""
+    B = 48
+    cap = n if L == 1 else n + n // 8
+    with _ctx(B, cap, L) as ctx:
+        for l in range(L):
+            ctx.drv_emit_synthetic(synth.PATTERNS["uniform"], synth.CONFIG_SEEDS[2], 0, n, local=l)
+        p1_forward(ctx, L, B)
