@@ -1,0 +1,402 @@
+"""bench.py -- forwarded work items/s of the RaFI hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl rafi|reference]
+    (N > 1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N)
+
+One STEP = one pass of the whole hot path over one batch per rank:
+  a1 emit (rafi_emit_bulk of the rank's resident batch), then rafi_forward:
+  a2 histogram, a3 scan, a4 stable scatter, a5 count exchange, a6 payload
+  exchange, a7 wrap-up, a8 termination count.
+Workload (BASELINE.json configs[1] per-rank shape, weak scaling): every rank
+holds 16,777,216 synthetic 48-byte items (the FWDRay shape)
+with uniformly random destinations over R = N ranks.  Inputs are resident in
+HBM before the timed region (768 MiB per rank > 126 MB L2, so no L2 reuse
+between steps).  value = items all ranks forwarded / max-over-ranks device
+time.  e2e = the same metric through the C ABI with HOST buffers: each step
+copies the batch in from pinned memory (inside rafi_emit_bulk) and reads the
+incoming queue back to pinned memory.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+DEF_N = 16 * 1024 * 1024
+DEF_B = 48
+METRIC = "forwarded work items/sec"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="rafi", choices=["rafi", "reference"])
+    p.add_argument("--items", type=int, default=DEF_N, help="items per rank per step")
+    p.add_argument("--item-bytes", type=int, default=DEF_B)
+    p.add_argument("--pattern", default="uniform")
+    p.add_argument("--exchange", default="auto", choices=["auto", "nccl", "peer"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle cpu_baseline sample")
+    return p.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def workload_config(args, N):
+    return {
+        "workload": "cfg2 per-rank shape: %d x %d-B items/rank, %s dest over R=%d ranks, 1 forward/step"
+                    % (args.items, args.item_bytes, args.pattern, N),
+        "items_per_rank": args.items, "item_bytes": args.item_bytes, "ranks": N, "pattern": args.pattern,
+        "l2": "inputs larger than L2 (%.0f MiB/rank resident)" % (args.items * (args.item_bytes + 4) / 2**20),
+        "step": "emit_bulk + forward (hist, scan, scatter, count exchange, payload exchange, wrap-up)",
+        "parallelism": "one rank per GPU" if N > 1 else "single GPU",
+    }
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.active", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sms)}
+
+
+# ----------------------------------------------------------------------------- oracle (CPU)
+
+def oracle_step_rate(R, n, B, pattern, seconds, max_reps=50):
+    """The oracle as it stands (single-threaded C): one step = sequential
+    emit of every rank's batch + forward, on a bounded sample of the
+    workload.  Returns (items/s, reps, sample description)."""
+    import oracle
+    import synth
+    batches = []
+    for s in range(R):
+        it = synth.make_items(s, 0, n, max(B, 16))[:, :B].copy()
+        ds = synth.make_dests(pattern, synth.CONFIG_SEEDS[2], s, 0, n, R)
+        batches.append((it, ds))
+    cap = n + n // 8 + 4096
+    w = oracle.World(R, cap, B)
+    times = []
+    t_end = time.perf_counter() + seconds
+    while len(times) < max_reps and (time.perf_counter() < t_end or len(times) < 2):
+        t0 = time.perf_counter()
+        for s, (it, ds) in enumerate(batches):
+            w.emit_many(s, it, ds)
+        G = w.forward()
+        times.append(time.perf_counter() - t0)
+        assert G == R * n, G
+    w.close()
+    med = statistics.median(times)
+    return R * n / med, len(times), "R=%d x %d items x %d B (%s), emit+forward per step, median of %d" % (
+        R, n, B, pattern, len(times))
+
+
+def cpu_sample_size(args, R):
+    # ~1-2 s per oracle step on one core: 2M items per step in total
+    return max(1024, min(args.items, (2 * 1024 * 1024) // R))
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    N = args.gpus
+    n = cpu_sample_size(args, N)
+    import oracle
+    import synth
+    batches = []
+    for s in range(N):
+        it = synth.make_items(s, 0, n, max(args.item_bytes, 16))[:, :args.item_bytes].copy()
+        ds = synth.make_dests(args.pattern, synth.CONFIG_SEEDS[2], s, 0, n, N)
+        batches.append((it, ds))
+    w = oracle.World(N, n + n // 8 + 4096, args.item_bytes)
+
+    def step():
+        for s, (it, ds) in enumerate(batches):
+            w.emit_many(s, it, ds)
+        assert w.forward() == N * n
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    v = N * n * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "items/s", "n_gpus": N, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (synth/ SplitMix64 recipe)",
+        "config": workload_config(args, N),
+        "cpu_baseline": {"value": v, "unit": "items/s", "cores": 1, "kind": "oracle",
+                         "sample": "R=%d x %d items x %d B per step (bounded sample of the workload), "
+                                   "sequential emit + plain forward, single-threaded C oracle"
+                                   % (N, n, args.item_bytes)},
+        "e2e": {"value": v, "unit": "items/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2605_30294_b200 import rafi
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    N = world
+    if world != args.gpus:
+        print("warning: --gpus %d but WORLD_SIZE %d; using %d" % (args.gpus, world, world), file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        obj = [rafi.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = rafi.nccl_comm_init(world, rank, obj[0], local)
+
+    B, n = args.item_bytes, args.items
+    stream = torch.cuda.current_stream()
+    cap = n + n // 8 + 4096
+    ctx = rafi.Context(B, cap, comm=comm, stream=stream, device=local)
+    if args.exchange != "auto":
+        ctx.set_option(rafi.OPT_EXCHANGE, {"nccl": rafi.EXCHANGE_NCCL, "peer": rafi.EXCHANGE_PEER}[args.exchange])
+    exchange = {1: "nccl", 2: "peer"}[ctx.get_option(rafi.OPT_EXCHANGE)]
+
+    # resident inputs (generated on the host by the shared generator, uploaded once)
+    items_h = synth.make_items(rank, 0, n, max(B, 16))[:, :B].copy()
+    dests_h = synth.make_dests(args.pattern, synth.CONFIG_SEEDS[2], rank, 0, n, N)
+    items_d = torch.from_numpy(items_h).to(dev)
+    dests_d = torch.from_numpy(dests_h).to(dev)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # ---- warm-up
+    for _ in range(args.warmup):
+        ctx.emit_bulk(items_d, dests_d, n)
+        G = ctx.forward()
+    assert G == N * n, (G, N * n)
+
+    # ---- timed region (device-timed, CUDA events on the context stream)
+    ctx.set_option(rafi.OPT_TIMING, 1)
+    phases = {k: 0.0 for k in ("emit", "hist", "scan", "scatter", "count_exchange", "payload_exchange", "wrapup")}
+    ev_e0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev_e1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    l0 = ctx.stats()["kernel_launches"]
+    remote = 0
+    barrier()
+    clocks.start()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for k in range(args.steps):
+        ev_e0[k].record(stream)
+        ctx.emit_bulk(items_d, dests_d, n)
+        ev_e1[k].record(stream)
+        G = ctx.forward()
+        st = ctx.stats()
+        phases["hist"] += st["ms_hist"]
+        phases["scan"] += st["ms_scan"]
+        phases["scatter"] += st["ms_scatter"]
+        phases["count_exchange"] += st["ms_count_exchange"]
+        phases["payload_exchange"] += st["ms_payload_exchange"]
+        phases["wrapup"] += st["ms_wrapup"]
+        remote += st["bytes_sent_remote"]
+    t_end.record(stream)
+    barrier()
+    clk = clocks.stop()
+    launches = ctx.stats()["kernel_launches"] - l0
+    for k in range(args.steps):
+        phases["emit"] += ev_e0[k].elapsed_time(ev_e1[k])
+    ms_total = t_start.elapsed_time(t_end)
+    ms_max = max_over_ranks(ms_total)
+    K = args.steps
+    value = N * n * K / (ms_max / 1e3)
+    ms_step = ms_max / K
+    ph = {k: v / K for k, v in phases.items()}
+
+    # ---- rooflines: algorithmic bytes per launch / average launch duration
+    hbm_peak, peak_src = load_peaks()
+    nin = ctx.num_incoming()
+    alg = {  # bytes per launch (per rank); DESIGN.md "Rooflines"
+        "emit": n * 2 * (B + 4),
+        "hist": n * 4,
+        "scatter": n * (B + 4 + B),
+        "payload_exchange": nin * 2 * B if N == 1 else None,
+    }
+    kern = {}
+    for k, byts in alg.items():
+        if byts is None or ph[k] <= 0:
+            continue
+        gbs = byts / (ph[k] / 1e3) / 1e9
+        kern[k] = {"ms": ph[k], "bytes": byts, "achieved_gbs": gbs, "frac": gbs / hbm_peak}
+    dom = max(kern, key=lambda k: kern[k]["ms"])
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        key = "%s/B%d/n%d/R%d" % (dom, B, n, N)
+        traffic = tr.get(key)
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["achieved_gbs"], "peak": hbm_peak,
+                "unit": "GB/s", "frac": kern[dom]["frac"], "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": kern[dom]["bytes"]}
+    exch = None
+    if N > 1 and ph["payload_exchange"] > 0:
+        gbs = (remote / K) / (ph["payload_exchange"] / 1e3) / 1e9
+        exch = {"gbs_per_gpu": gbs, "frac_of_900": gbs / 900.0, "transport": exchange,
+                "remote_bytes_per_step": remote / K}
+
+    # ---- end to end through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        ctx.set_option(rafi.OPT_TIMING, 0)
+        items_p = torch.from_numpy(items_h).pin_memory()
+        dests_p = torch.from_numpy(dests_h).pin_memory()
+        out_p = torch.empty((cap, B), dtype=torch.uint8).pin_memory()
+        Ke = max(3, min(K, 5))
+        for _ in range(2):
+            ctx.emit_bulk(items_p, dests_p, n)
+            ctx.forward()
+            ctx.read_incoming(out=out_p[: ctx.num_incoming()].numpy())
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        d2h = 0
+        e0.record(stream)
+        for _ in range(Ke):
+            ctx.emit_bulk(items_p, dests_p, n)             # H2D inside the call (host pointers)
+            ctx.forward()
+            m = ctx.num_incoming()
+            ctx.read_incoming(out=out_p[:m].numpy())       # D2H of the result
+            d2h += m * B
+        e1.record(stream)
+        barrier()
+        ms_e = max_over_ranks(e0.elapsed_time(e1))
+        e2e = {"value": N * n * Ke / (ms_e / 1e3), "unit": "items/s", "h2d_bytes_per_step": n * (B + 4),
+               "d2h_bytes_per_step": int(d2h / Ke), "steps": Ke}
+
+    # ---- cpu baseline: the oracle on the host, rank 0 at N=1 only
+    cpu = None
+    if N == 1 and rank == 0 and not args.no_cpu_baseline:
+        ns = cpu_sample_size(args, 1)
+        v, reps, desc = oracle_step_rate(1, ns, B, args.pattern, args.cpu_seconds)
+        cpu = {"value": v, "unit": "items/s", "cores": 1, "kind": "oracle",
+               "sample": desc + " (single-threaded C oracle on the GPU box host)"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "items/s", "n_gpus": N, "steps": K, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (synth/ SplitMix64 recipe; resident in HBM)", "config": workload_config(args, N),
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "clocks": clk, "phases_ms": ph, "kernels": kern, "exchange": exch, "exchange_transport": exchange,
+        "per_gpu_items_per_s": value / N,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if comm:
+        rafi.nccl_comm_destroy(comm)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -51,6 +51,7 @@ def lib():
             "orc_get_incoming": (i32, [P, i32, u64, vp]),
             "orc_emit": (i32, [P, i32, vp, i64]),
             "orc_load_snapshot": (i32, [P, i32, vp, vp, u64, u64]),
+            "orc_emit_many": (u64, [P, i32, vp, vp, u64]),
             "orc_set_incoming": (i32, [P, i32, vp, u64]),
             "orc_forward_plain": (i64, [P]),
             "orc_forward_literal": (i64, [P]),
@@ -124,12 +125,13 @@ class World:
         return bool(lib().orc_emit(self._w, r, _ptr(buf), int(d)))
 
     def emit_many(self, r: int, items: np.ndarray, dests) -> int:
-        """Sequential emits in array order; returns the number accepted."""
+        """Sequential emits in array order (orc_emit_many); returns the number accepted."""
         items = np.ascontiguousarray(items, dtype=np.uint8).reshape(-1, self.B)
-        acc = 0
-        for i in range(items.shape[0]):
-            acc += lib().orc_emit(self._w, r, _ptr(items[i]), int(dests[i]))
-        return acc
+        d = np.ascontiguousarray(dests, dtype=np.int32)
+        assert d.size == items.shape[0]
+        if d.size == 0:
+            return 0
+        return int(lib().orc_emit_many(self._w, r, _ptr(items), _ptr(d), d.size))
 
     def load_snapshot(self, r: int, items: np.ndarray, dests: np.ndarray, ctr: int, invalid: int = 0):
         items = np.ascontiguousarray(items, dtype=np.uint8)

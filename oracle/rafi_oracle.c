@@ -147,6 +147,15 @@ int orc_emit(orc_world *w, int r, const void *item, int64_t d) {
     return 0;                                                           /* Z1 */
 }
 
+/* n sequential emitOutgoing calls in array order (the same rule as orc_emit,
+ * one call per item).  Returns the number accepted. */
+uint64_t orc_emit_many(orc_world *w, int r, const void *items, const int32_t *dests, uint64_t n) {
+    uint64_t acc = 0;
+    const uint8_t *p = (const uint8_t *)items;
+    for (uint64_t i = 0; i < n; ++i) acc += (uint64_t)orc_emit(w, r, p + i * w->B, dests[i]);
+    return acc;
+}
+
 /* Load an observed queue state (items in slot order, their dests, the raw
  * counter values) into rank r -- used for snapshot parity, where the emit
  * slot order was decided by GPU atomics. */
