@@ -46,7 +46,7 @@ def parse():
     p.add_argument("--items", type=int, default=DEF_N, help="items per rank per step")
     p.add_argument("--item-bytes", type=int, default=DEF_B)
     p.add_argument("--pattern", default="uniform")
-    p.add_argument("--exchange", default="auto", choices=["auto", "nccl", "peer"])
+    p.add_argument("--exchange", default="auto", choices=["auto", "nccl", "peer", "fused"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle cpu_baseline sample")
@@ -237,8 +237,9 @@ def main():
     cap = n + n // 8 + 4096
     ctx = rafi.Context(B, cap, comm=comm, stream=stream, device=local)
     if args.exchange != "auto":
-        ctx.set_option(rafi.OPT_EXCHANGE, {"nccl": rafi.EXCHANGE_NCCL, "peer": rafi.EXCHANGE_PEER}[args.exchange])
-    exchange = {1: "nccl", 2: "peer"}[ctx.get_option(rafi.OPT_EXCHANGE)]
+        ctx.set_option(rafi.OPT_EXCHANGE, {"nccl": rafi.EXCHANGE_NCCL, "peer": rafi.EXCHANGE_PEER,
+                                           "fused": rafi.EXCHANGE_FUSED}[args.exchange])
+    exchange = {1: "nccl", 2: "peer", 3: "fused"}[ctx.get_option(rafi.OPT_EXCHANGE)]
 
     # resident inputs (generated on the host by the shared generator, uploaded once)
     items_h = synth.make_items(rank, 0, n, max(B, 16))[:, :B].copy()
@@ -318,7 +319,7 @@ def main():
         "emit": n * 2 * (B + 4),
         "hist": n * 4,
         "scatter": n * (B + 4 + B),
-        "payload_exchange": nin * 2 * B if N == 1 else None,
+        "payload_exchange": nin * 2 * B if (N == 1 and exchange != "fused") else None,
     }
     kern = {}
     for k, byts in alg.items():
@@ -339,10 +340,13 @@ def main():
                 "unit": "GB/s", "frac": kern[dom]["frac"], "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": kern[dom]["bytes"]}
     exch = None
-    if N > 1 and ph["payload_exchange"] > 0:
-        gbs = (remote / K) / (ph["payload_exchange"] / 1e3) / 1e9
-        exch = {"gbs_per_gpu": gbs, "frac_of_900": gbs / 900.0, "transport": exchange,
-                "remote_bytes_per_step": remote / K}
+    xfer_ms = ph["scatter"] if exchange == "fused" else ph["payload_exchange"]
+    if N > 1 and xfer_ms > 0:
+        # remote payload bytes this GPU sends per step / time of the kernel that moves them
+        # (FUSED: the scatter pushes over NVLink; staged: the copy kernel / NCCL send-recv)
+        gbs = (remote / K) / (xfer_ms / 1e3) / 1e9
+        exch = {"gbs_per_gpu": gbs, "frac_of_900": gbs / 900.0, "frac_of_770_measured_p2p": gbs / 770.0,
+                "transport": exchange, "remote_bytes_per_step": remote / K, "kernel_ms": xfer_ms}
 
     # ---- end to end through the C ABI with host buffers
     e2e = None

@@ -109,9 +109,13 @@ typedef struct {
 #define RAFI_OPT_TILE 3            /* binning tile in items (multiple of 256); 0 = auto from item size */
 #define RAFI_OPT_SELF_DIRECT 4     /* reserved (self run placement); 0 */
 
-#define RAFI_EXCHANGE_AUTO 0       /* PEER when every rank's buffers are addressable, else NCCL */
-#define RAFI_EXCHANGE_NCCL 1       /* grouped ncclSend/ncclRecv (one local rank per process) */
-#define RAFI_EXCHANGE_PEER 2       /* copy kernel over local / CUDA-IPC peer pointers (NVLink) */
+#define RAFI_EXCHANGE_AUTO 0       /* FUSED when every rank's queues are addressable, else NCCL */
+#define RAFI_EXCHANGE_NCCL 1       /* stage the sorted batch, grouped ncclSend/ncclRecv (one local rank per process) */
+#define RAFI_EXCHANGE_PEER 2       /* stage the sorted batch, receivers pull it with a copy kernel over
+                                      local / CUDA-IPC peer pointers (NVLink) */
+#define RAFI_EXCHANGE_FUSED 3      /* the scatter writes every destination run straight into the destination
+                                      rank's incoming queue (local HBM or NVLink peer memory); the count
+                                      matrix is all-gathered first; no send batch, no separate copy */
 
 /* ---- lifecycle ------------------------------------------------------------ */
 
@@ -185,7 +189,8 @@ int rafi_read_incoming(const rafi_ctx* ctx, int local, void* dst, uint64_t first
 int rafi_read_outgoing(const rafi_ctx* ctx, int local, void* items_dst, int32_t* dests_dst,
                        uint64_t* ctr, uint64_t* invalid);
 
-/* The destination-sorted send batch of the last forward (n_out items). */
+/* The destination-sorted send batch of the last forward (n_out items).
+ * RAFI_ERR_UNSUPPORTED after a FUSED forward, which writes no send batch. */
 int rafi_read_binned(const rafi_ctx* ctx, int local, void* dst, uint64_t count);
 
 /* The last forward's R x R count matrix, row = source rank, column = destination. */

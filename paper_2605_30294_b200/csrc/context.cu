@@ -52,6 +52,7 @@ static void close_ipc(Ctx* c) {
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   c->ipc_opened.clear();
   c->peer_binned.clear();
+  c->peer_in.clear();
   c->peer_ok = false;
 }
 
@@ -81,26 +82,41 @@ static int upload_rank_table(Ctx* c) {
   return RAFI_OK;
 }
 
-// Every rank learns every rank's binned[] pointers: local ones directly,
-// other processes' through CUDA IPC handles all-gathered over NCCL.
+// Every rank learns every rank's binned[0..1] and in pointers: local ones
+// directly, other processes' through CUDA IPC handles all-gathered over NCCL.
 // Collective.  peer_ok is decided identically on all ranks.
+static constexpr int kMapped = 3;  // binned[0], binned[1], in
+
+static uint8_t* mapped_buf(LocalRank& r, int b) { return b < 2 ? (r.binned[b] ? r.binned[b] : r.binned[0]) : r.in; }
+
+static int upload_in_table(Ctx* c) {
+  std::vector<uint8_t*> t(c->R, nullptr);
+  for (int g = 0; g < c->R; ++g) t[g] = c->peer_in.empty() ? nullptr : c->peer_in[g];
+  RAFI_CK_CUDA(cudaMemcpyAsync(c->in_table_dev, t.data(), sizeof(uint8_t*) * c->R, cudaMemcpyHostToDevice, c->stream));
+  RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
+  return RAFI_OK;
+}
+
 static int exchange_peer_pointers(Ctx* c) {
   close_ipc(c);
   c->peer_binned.assign((size_t)c->R * 2, nullptr);
+  c->peer_in.assign((size_t)c->R, nullptr);
+  auto place = [&](int g, int b, uint8_t* p) {
+    if (b < 2) c->peer_binned[(size_t)g * 2 + b] = p;
+    else c->peer_in[g] = p;
+  };
   for (int l = 0; l < c->L; ++l)
-    for (int b = 0; b < 2; ++b) {
-      LocalRank& r = c->lr[l];
-      c->peer_binned[(size_t)(c->proc * c->L + l) * 2 + b] = r.binned[b] ? r.binned[b] : r.binned[0];
-    }
-  if (c->nprocs == 1) { c->peer_ok = true; return RAFI_OK; }
-  const size_t per = sizeof(cudaIpcMemHandle_t) * 2 * c->L;
+    for (int b = 0; b < kMapped; ++b) place(c->proc * c->L + l, b, mapped_buf(c->lr[l], b));
+  if (c->nprocs == 1) { c->peer_ok = true; return upload_in_table(c); }
+  const size_t per = sizeof(cudaIpcMemHandle_t) * kMapped * c->L;
   std::vector<uint8_t> mine(per), all(per * c->nprocs);
   int ok = 1;
   for (int l = 0; l < c->L; ++l)
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kMapped; ++b) {
       cudaIpcMemHandle_t h;
-      if (cudaIpcGetMemHandle(&h, c->lr[l].binned[b]) != cudaSuccess) { ok = 0; cudaGetLastError(); }
-      std::memcpy(mine.data() + sizeof(h) * (2 * l + b), &h, sizeof(h));
+      std::memset(&h, 0, sizeof(h));
+      if (cudaIpcGetMemHandle(&h, mapped_buf(c->lr[l], b)) != cudaSuccess) { ok = 0; cudaGetLastError(); }
+      std::memcpy(mine.data() + sizeof(h) * (kMapped * l + b), &h, sizeof(h));
     }
   uint8_t* dbuf = nullptr;
   RAFI_CK(alloc_dev((void**)&dbuf, per * c->nprocs + sizeof(int)));
@@ -115,18 +131,18 @@ static int exchange_peer_pointers(Ctx* c) {
     for (int p = 0; p < c->nprocs && ok; ++p) {
       if (p == c->proc) continue;
       for (int l = 0; l < c->L && ok; ++l)
-        for (int b = 0; b < 2 && ok; ++b) {
+        for (int b = 0; b < kMapped && ok; ++b) {
           cudaIpcMemHandle_t h;
-          std::memcpy(&h, all.data() + per * p + sizeof(h) * (2 * l + b), sizeof(h));
+          std::memcpy(&h, all.data() + per * p + sizeof(h) * (kMapped * l + b), sizeof(h));
           void* ptr = nullptr;
           if (cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
             ok = 0; cudaGetLastError(); break;
           }
           c->ipc_opened.push_back(ptr);
-          c->peer_binned[(size_t)(p * c->L + l) * 2 + b] = (uint8_t*)ptr;
+          place(p * c->L + l, b, (uint8_t*)ptr);
         }
     }
-    // agree: peer mode only if every process mapped every peer
+    // agree: peer modes only if every process mapped every peer
     if (cudaMemcpyAsync(dflag, &ok, sizeof(int), cudaMemcpyHostToDevice, c->stream) != cudaSuccess) { rc = RAFI_ERR_CUDA; break; }
     nr = ncclAllReduce(dflag, dflag, 1, ncclInt32, ncclMin, c->comm, c->stream);
     if (nr != ncclSuccess) { set_error(std::string("ncclAllReduce(ipc ok): ") + ncclGetErrorString(nr)); rc = RAFI_ERR_NCCL; break; }
@@ -136,14 +152,19 @@ static int exchange_peer_pointers(Ctx* c) {
     c->peer_ok = all_ok != 0;
   } while (0);
   cudaFree(dbuf);
-  if (!c->peer_ok) close_ipc(c), c->peer_binned.assign((size_t)c->R * 2, nullptr);
+  if (!c->peer_ok) {
+    close_ipc(c);
+    c->peer_binned.assign((size_t)c->R * 2, nullptr);
+    c->peer_in.assign((size_t)c->R, nullptr);
+  }
+  if (rc == RAFI_OK) rc = upload_in_table(c);
   return rc;
 }
 
 static int resolve_exchange(Ctx* c) {
   int x = c->exchange;
-  if (x == RAFI_EXCHANGE_AUTO) x = (c->nprocs == 1 || c->peer_ok) ? RAFI_EXCHANGE_PEER : RAFI_EXCHANGE_NCCL;
-  if (x == RAFI_EXCHANGE_PEER && !(c->nprocs == 1 || c->peer_ok)) {
+  if (x == RAFI_EXCHANGE_AUTO) x = (c->nprocs == 1 || c->peer_ok) ? RAFI_EXCHANGE_FUSED : RAFI_EXCHANGE_NCCL;
+  if ((x == RAFI_EXCHANGE_PEER || x == RAFI_EXCHANGE_FUSED) && !(c->nprocs == 1 || c->peer_ok)) {
     set_error("PEER exchange needs every rank's buffers mapped (CUDA IPC failed)");
     return RAFI_ERR_UNSUPPORTED;
   }
@@ -170,6 +191,7 @@ static void destroy_ctx(Ctx* c) {
   close_ipc(c);
   for (auto& r : c->lr) free_rank(r);
   cudaFree(c->rank_dev); cudaFree(c->ctrl); cudaFree(c->Cdev); cudaFree(c->runs_dev); cudaFree(c->plan_dev);
+  cudaFree(c->off_dev); cudaFree(c->ovf_dev); cudaFree(c->in_table_dev);
   cudaFree(c->stage);
   cudaFreeHost(c->Chost); cudaFreeHost(c->ctrl_host); cudaFreeHost(c->runs_host); cudaFreeHost(c->plan_host);
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);
@@ -217,6 +239,9 @@ static int create(Ctx** out, const rafi_create_params* p) {
   if ((rc = alloc_dev((void**)&c->Cdev, sizeof(uint64_t) * c->R * c->R))) return fail(rc);
   if ((rc = alloc_dev((void**)&c->runs_dev, sizeof(CopyRun) * c->L * c->R))) return fail(rc);
   if ((rc = alloc_dev((void**)&c->plan_dev, sizeof(uint64_t) * c->L))) return fail(rc);
+  if ((rc = alloc_dev((void**)&c->off_dev, sizeof(int64_t) * c->L * c->R))) return fail(rc);
+  if ((rc = alloc_dev((void**)&c->ovf_dev, 2 * sizeof(int)))) return fail(rc);
+  if ((rc = alloc_dev((void**)&c->in_table_dev, sizeof(uint8_t*) * c->R))) return fail(rc);
   if (cudaMallocHost((void**)&c->Chost, sizeof(uint64_t) * c->R * c->R) != cudaSuccess ||
       cudaMallocHost((void**)&c->ctrl_host, sizeof(CtrlDev) * c->L) != cudaSuccess ||
       cudaMallocHost((void**)&c->runs_host, sizeof(CopyRun) * c->L * c->R) != cudaSuccess ||
@@ -226,6 +251,7 @@ static int create(Ctx** out, const rafi_create_params* p) {
     return fail(RAFI_ERR_NOMEM);
   }
   if (cudaMemsetAsync(c->ctrl, 0, sizeof(CtrlDev) * c->L, c->stream) != cudaSuccess ||
+      cudaMemsetAsync(c->ovf_dev, 0, 2 * sizeof(int), c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->Cdev, 0, sizeof(uint64_t) * c->R * c->R, c->stream) != cudaSuccess) {
     cudaGetLastError(); set_error("cudaMemsetAsync failed"); return fail(RAFI_ERR_CUDA);
   }
@@ -247,9 +273,92 @@ static float ev_ms(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
-static int64_t forward(Ctx* c) {
-  if (c->broken) { set_error("context unusable after an earlier collective error"); return RAFI_ERR_STATE; }
-  RAFI_CK_CUDA(cudaSetDevice(c->device));
+// Host bookkeeping from the mirrored count matrix and control blocks.
+// Returns 1 if some rank would receive more than its capacity (Z3).
+static int book_keep(Ctx* c, uint64_t* G_out) {
+  const int R = c->R, L = c->L;
+  uint64_t G = 0;
+  int overflow = 0;
+  for (int e = 0; e < R; ++e) {
+    uint64_t col = 0;
+    for (int s = 0; s < R; ++s) col += c->Chost[(size_t)s * R + e];
+    if (col > c->cap) overflow = 1;
+    G += col;
+  }
+  *G_out = G;
+  if (overflow) return 1;
+  for (int l = 0; l < L; ++l) {
+    const int g = c->proc * L + l;
+    LocalRank& r = c->lr[l];
+    uint64_t tot = 0, sent = 0, recv = 0;
+    for (int s = 0; s < R; ++s) {
+      const uint64_t in_c = c->Chost[(size_t)s * R + g];
+      tot += in_c;
+      if (s != g) { recv += in_c * c->B; sent += c->Chost[(size_t)g * R + s] * c->B; }
+    }
+    r.num_in = tot;
+    r.n_out = c->ctrl_host[l].n_out;
+    r.dropped = c->ctrl_host[l].dropped;
+    r.invalid = c->ctrl_host[l].invalid_last;
+    r.sent_remote = sent;
+    r.recv_remote = recv;
+  }
+  return 0;
+}
+
+// FUSED forward: counts first, then one kernel bins and pushes every run
+// straight into its destination's incoming queue (NEXT-1 of SURVEY §8(f)).
+//   hist -> scan -> [all-gather counts] -> plan -> scatter+push -> [barrier] -> wrap-up
+static int64_t forward_fused(Ctx* c) {
+  const int R = c->R, L = c->L;
+  c->fwd_launches = 0;
+  const bool T = c->timing;
+  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[0], c->stream));
+  RAFI_CK(launch_hist(c));
+  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[1], c->stream));
+  RAFI_CK(launch_scan(c));
+  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[2], c->stream));
+  // a5: the whole R x R matrix on every rank; offsets + overflow on device
+  if (c->nprocs > 1)
+    RAFI_CK_NCCL(ncclAllGather(c->Cdev + (size_t)c->proc * L * R, c->Cdev, (size_t)L * R, ncclUint64, c->comm,
+                               c->stream));
+  RAFI_CK(launch_plan(c));
+  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[3], c->stream));
+  // a4 + a6: stable scatter, each destination run written into its receiver's queue
+  RAFI_CK(launch_scatter(c, true));
+  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[4], c->stream));
+  // every push has landed before any rank's next app kernel reads its queue:
+  // the all-reduce completes only after every rank's scatter kernel completed
+  if (c->nprocs > 1)
+    RAFI_CK_NCCL(ncclAllReduce(c->ovf_dev + 1, c->ovf_dev + 1, 1, ncclInt32, ncclMax, c->comm, c->stream));
+  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[5], c->stream));
+  RAFI_CK(launch_wrapup(c));  // a7 (skipped on device if the overflow flag is set)
+  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[6], c->stream));
+  RAFI_CK_CUDA(cudaMemcpyAsync(c->Chost, c->Cdev, sizeof(uint64_t) * R * R, cudaMemcpyDeviceToHost, c->stream));
+  RAFI_CK_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl, sizeof(CtrlDev) * L, cudaMemcpyDeviceToHost, c->stream));
+  RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
+  uint64_t G = 0;
+  if (book_keep(c, &G)) {
+    c->broken = true;
+    set_error("receive overflow: some rank would receive more than its capacity");
+    return RAFI_ERR_RECV_OVERFLOW;
+  }
+  if (T) {
+    c->st.ms_hist = ev_ms(c->ev[0], c->ev[1]);
+    c->st.ms_scan = ev_ms(c->ev[1], c->ev[2]);
+    c->st.ms_count_exchange = ev_ms(c->ev[2], c->ev[3]);
+    c->st.ms_scatter = ev_ms(c->ev[3], c->ev[4]);
+    c->st.ms_payload_exchange = ev_ms(c->ev[4], c->ev[5]);  // the completion barrier
+    c->st.ms_wrapup = ev_ms(c->ev[5], c->ev[6]);
+    c->st.ms_total = ev_ms(c->ev[0], c->ev[6]);
+  }
+  c->last_fused = true;
+  c->round += 1;
+  c->last_G = (int64_t)G;  // a8
+  return (int64_t)G;
+}
+
+static int64_t forward_staged(Ctx* c) {
   const int R = c->R, L = c->L;
   const uint64_t B = c->B;
   c->fwd_launches = 0;
@@ -260,7 +369,7 @@ static int64_t forward(Ctx* c) {
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[1], c->stream));
   RAFI_CK(launch_scan(c));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[2], c->stream));
-  RAFI_CK(launch_scatter(c));
+  RAFI_CK(launch_scatter(c, false));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[3], c->stream));
   // a5: every process learns the whole R x R count matrix.  The all-gather is
   // ordered after each process's scatter on its stream, so once it completes
@@ -358,10 +467,17 @@ static int64_t forward(Ctx* c) {
     c->st.ms_total = ev_ms(c->ev[0], c->ev[6]);
   }
   c->last_cur = c->cur;
+  c->last_fused = false;
   if (double_buffered(c)) c->cur ^= 1;
   c->round += 1;
   c->last_G = (int64_t)G;  // a8: sum of all received counts, same on every rank
   return (int64_t)G;
+}
+
+static int64_t forward(Ctx* c) {
+  if (c->broken) { set_error("context unusable after an earlier collective error"); return RAFI_ERR_STATE; }
+  RAFI_CK_CUDA(cudaSetDevice(c->device));
+  return c->exchange_eff == RAFI_EXCHANGE_FUSED ? forward_fused(c) : forward_staged(c);
 }
 
 static bool bad_local(const Ctx* c, int local) { return !c || local < 0 || local >= c->L; }
@@ -563,6 +679,7 @@ int rafi_read_outgoing(const rafi_ctx* ctx, int local, void* items_dst, int32_t*
 int rafi_read_binned(const rafi_ctx* ctx, int local, void* dst, uint64_t count) {
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
   if (bad_local(c, local) || (count && !dst)) return RAFI_ERR_INVALID_ARG;
+  if (c->last_fused) { set_error("the FUSED exchange writes no send batch"); return RAFI_ERR_UNSUPPORTED; }
   const LocalRank& r = c->lr[local];
   if (count > r.n_out) return RAFI_ERR_INVALID_ARG;
   if (!count) return RAFI_OK;
@@ -605,7 +722,7 @@ int rafi_set_option(rafi_ctx* ctx, int key, long long v) {
   if (!c) return RAFI_ERR_INVALID_ARG;
   switch (key) {
     case RAFI_OPT_EXCHANGE: {
-      if (v < RAFI_EXCHANGE_AUTO || v > RAFI_EXCHANGE_PEER) return RAFI_ERR_INVALID_ARG;
+      if (v < RAFI_EXCHANGE_AUTO || v > RAFI_EXCHANGE_FUSED) return RAFI_ERR_INVALID_ARG;
       const int old = c->exchange;
       c->exchange = (int)v;
       int rc = resolve_exchange(c);

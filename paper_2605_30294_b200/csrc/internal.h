@@ -91,12 +91,13 @@ struct Ctx {
   uint32_t tile = 0;          // binning tile (items)
   uint64_t max_tiles = 0;     // ceil(cap / tile)
   int exchange = RAFI_EXCHANGE_AUTO;
-  int exchange_eff = RAFI_EXCHANGE_PEER;
+  int exchange_eff = RAFI_EXCHANGE_FUSED;
   bool timing = false;
   bool broken = false;
   uint64_t round = 0;
   int cur = 0;       // which binned buffer this round writes
   int last_cur = 0;  // which one the last forward wrote
+  bool last_fused = false;
   int64_t last_G = 0;
 
   std::vector<LocalRank> lr;
@@ -108,6 +109,10 @@ struct Ctx {
   CopyRun* runs_dev = nullptr;        // [L*R] copy plan, device
   CopyRun* runs_host = nullptr;       // [L*R] pinned
   uint64_t* plan_dev = nullptr;       // [L] per local dest: num_in (for wrap-up)
+  int64_t* off_dev = nullptr;         // [L][R] FUSED: recv_off_d[me] - send_off_me[d]
+  int* ovf_dev = nullptr;             // [1] FUSED: collective receive-overflow flag
+  uint8_t** in_table_dev = nullptr;   // [R] every global rank's incoming queue (local or IPC-mapped)
+  std::vector<uint8_t*> peer_in;      // host copy of in_table
   uint64_t* plan_host = nullptr;      // [L] pinned
   // peer pointers to every global rank's binned buffers ([R][2]); local ones
   // are our own allocations, remote ones are CUDA-IPC mappings
@@ -132,7 +137,8 @@ uint32_t choose_tile(uint64_t item_bytes);
 int launch_emit_bulk(Ctx* c, int local, const uint8_t* items, const int32_t* dests, uint64_t n);
 int launch_hist(Ctx* c);
 int launch_scan(Ctx* c);
-int launch_scatter(Ctx* c);
+int launch_scatter(Ctx* c, bool fused);
+int launch_plan(Ctx* c);
 int launch_copy(Ctx* c, int nruns_per_dest);
 int launch_wrapup(Ctx* c);
 size_t scatter_smem_bytes(uint32_t tile, uint64_t item_bytes, int R);

@@ -143,6 +143,15 @@ k_emit_bulk(const uint8_t* __restrict__ items, const int32_t* __restrict__ dests
 
 // ---------------------------------------------------------------- a2 histogram
 
+__device__ __forceinline__ uint32_t warp_sum(uint32_t x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+  return x;
+}
+
+// RMAX > 0: per-thread register counters for R <= RMAX (16-byte dest loads,
+// warp-shuffle reduction); RMAX == 0: generic __match_any_sync aggregation.
+template <int RMAX>
 __global__ void __launch_bounds__(kThreads)
 k_hist(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, int L, int R, uint64_t cap,
        uint32_t T) {
@@ -157,10 +166,35 @@ k_hist(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, int L, 
     const uint64_t t0 = t * T;
     const uint32_t nt = (uint32_t)umin64(T, n - t0);
     const int32_t* dest = rk[l].dest + t0;
-    for (uint32_t i = tid; i < (T + 0u); i += kThreads) {  // T is a multiple of kThreads
-      const int d = i < nt ? dest[i] : -1;
-      const unsigned m = __match_any_sync(kFull, d);
-      if (d >= 0 && lane == __ffs(m) - 1) atomicAdd(&cnt[d], (uint32_t)__popc(m));
+    if (RMAX > 0) {
+      uint32_t c[RMAX > 0 ? RMAX : 1];
+#pragma unroll
+      for (int r = 0; r < RMAX; ++r) c[r] = 0;
+      const int4* d4 = reinterpret_cast<const int4*>(dest);  // t0*4 is a multiple of 1 KiB
+      for (uint32_t q = tid; q * 4 < nt; q += kThreads) {
+        const int4 v = d4[q];
+        const int e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (q * 4 + j < nt) {
+#pragma unroll
+            for (int r = 0; r < RMAX; ++r) c[r] += (e[j] == r);
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RMAX; ++r) {
+        if (r < R) {
+          const uint32_t x = warp_sum(c[r]);
+          if (lane == 0 && x) atomicAdd(&cnt[r], x);
+        }
+      }
+    } else {
+      for (uint32_t i = tid; i < T; i += kThreads) {  // T is a multiple of kThreads
+        const int d = i < nt ? dest[i] : -1;
+        const unsigned m = __match_any_sync(kFull, d);
+        if (d >= 0 && lane == __ffs(m) - 1) atomicAdd(&cnt[d], (uint32_t)__popc(m));
+      }
     }
     __syncthreads();
     uint32_t* H = rk[l].H;
@@ -252,43 +286,141 @@ k_scan(const RankDev* __restrict__ rk, CtrlDev* __restrict__ ctrl, uint64_t* __r
 
 // ---------------------------------------------------------------- a4 scatter
 
-template <typename U, bool kStage>
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// 1-D bulk copy global -> shared through the TMA unit (cp.async.bulk, UBLKCP)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+// Shared-memory layout of k_scatter (host mirror: scatter_layout()).
+struct ScatterLayout {
+  uint32_t stage_items;   // bytes of one stage's item buffer (0 if items are read from global)
+  uint32_t stage_stride;  // bytes per stage (items + dests), 128-aligned
+  uint32_t off_mbar, off_src, off_pd, off_dpos, off_wcnt, off_wbase, off_rstart, off_tcnt, off_dbase, total;
+};
+
+__host__ __device__ inline ScatterLayout scatter_layout(uint32_t T, uint64_t B, int R, bool stage_items) {
+  ScatterLayout s;
+  auto al = [](uint64_t x, uint64_t a) { return (uint32_t)((x + a - 1) / a * a); };
+  s.stage_items = stage_items ? al((uint64_t)T * B, 16) : 0u;
+  s.stage_stride = al((uint64_t)s.stage_items + 4ull * T, 128);
+  uint32_t o = 2 * s.stage_stride;
+  s.off_mbar = o; o += 16;
+  s.off_src = o; o = al(o + 2ull * T, 16);
+  s.off_pd = o; o = al(o + 2ull * T, 16);
+  s.off_dpos = o; o += 4 * T;
+  s.off_wcnt = o; o += 4 * kWarps * R;
+  s.off_wbase = o; o += 4 * kWarps * R;
+  s.off_rstart = o; o += 4 * R;
+  s.off_tcnt = o; o = al(o + 4ull * R, 8);
+  s.off_dbase = o; o += 8 * R;
+  s.total = o;
+  return s;
+}
+
+// Stable scatter of each tile into one contiguous run per destination.
+//   * Tile loads (items + dests) are 1-D TMA bulk copies into a two-stage
+//     shared-memory ring guarded by mbarriers: tile i+1 (and i+2) stream in
+//     while tile i is ranked and written.
+//   * Ranking: __match_any_sync per warp chunk + per-warp running counts gives
+//     each item its rank among same-destination items of the tile in slot
+//     order (stability).
+//   * Writing: the tile is re-ordered destination-major in shared memory
+//     index space and written as consecutive 16/8/4/2/1-byte units, so every
+//     destination run is stored with fully coalesced transactions.
+//   * Destination: dst_table == nullptr -> the local send batch binned[cur]
+//     (position = offset in the destination-major batch).  Otherwise the
+//     FUSED exchange: unit goes straight to destination rank d's incoming
+//     queue, dst_table[d] (local HBM or a CUDA-IPC peer mapping over NVLink),
+//     at item index position + dst_off[l][d] (recv_off_d[me] - send_off_me[d]).
+template <typename U, bool kStageItems>
 __global__ void __launch_bounds__(kThreads, 2)
-k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, int L, int R, uint64_t cap,
-          uint32_t T, int cur, uint32_t B, uint32_t UPI, FastDiv divU, uint32_t items_smem_bytes) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  U* items_s = reinterpret_cast<U*>(smem);
-  uint16_t* src_of = reinterpret_cast<uint16_t*>(smem + items_smem_bytes);
-  uint32_t* dpos = reinterpret_cast<uint32_t*>(smem + items_smem_bytes + ((2 * T + 15) & ~15u));
-  uint32_t* wcnt = dpos + T;           // [W][R]
-  uint32_t* wbase = wcnt + kWarps * R; // [W][R]
-  uint32_t* rstart = wbase + kWarps * R;
-  uint32_t* gbase = rstart + R;
+k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint8_t* const* __restrict__ dst_table,
+          const int64_t* __restrict__ dst_off, const int* __restrict__ ovf, int L, int R, uint64_t cap, uint32_t T,
+          int cur, uint32_t B, uint32_t UPI, FastDiv divU, ScatterLayout lay) {
+  if (ovf && *ovf) return;  // collective receive overflow: move nothing (Z3)
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + lay.off_mbar);
+  uint16_t* src_of = reinterpret_cast<uint16_t*>(smem + lay.off_src);
+  uint16_t* pd = reinterpret_cast<uint16_t*>(smem + lay.off_pd);
+  uint32_t* dpos = reinterpret_cast<uint32_t*>(smem + lay.off_dpos);
+  uint32_t* wcnt = reinterpret_cast<uint32_t*>(smem + lay.off_wcnt);
+  uint32_t* wbase = reinterpret_cast<uint32_t*>(smem + lay.off_wbase);
+  uint32_t* rstart = reinterpret_cast<uint32_t*>(smem + lay.off_rstart);
+  uint32_t* tcnt = reinterpret_cast<uint32_t*>(smem + lay.off_tcnt);
+  uintptr_t* dbase = reinterpret_cast<uintptr_t*>(smem + lay.off_dbase);
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const uint32_t K = T / kThreads;
-  for (uint64_t g = blockIdx.x;; g += gridDim.x) {
+
+  auto issue = [&](uint32_t it) {  // thread 0: start loading iteration it's tile into stage it&1
+    const uint64_t g = blockIdx.x + (uint64_t)it * gridDim.x;
+    int l;
+    uint64_t t, n, tiles;
+    if (!tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) return;
+    const uint64_t t0 = t * T;
+    const uint32_t nt = (uint32_t)umin64(T, n - t0);
+    uint8_t* st = smem + (it & 1) * lay.stage_stride;
+    const uint32_t bi = kStageItems ? ((nt * B + 15) & ~15u) : 0u;
+    const uint32_t bd = (nt * 4 + 15) & ~15u;
+    mbar_expect_tx(&mbar[it & 1], bi + bd);
+    if (kStageItems) bulk_g2s(st, rk[l].out + t0 * B, bi, &mbar[it & 1]);
+    bulk_g2s(st + lay.stage_items, rk[l].dest + t0, bd, &mbar[it & 1]);
+  };
+
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) { issue(0); issue(1); }
+
+  for (uint32_t it = 0;; ++it) {
+    const uint64_t g = blockIdx.x + (uint64_t)it * gridDim.x;
     int l;
     uint64_t t, n, tiles;
     if (!tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) break;
     const uint64_t t0 = t * T;
     const uint32_t nt = (uint32_t)umin64(T, n - t0);
-    const uint8_t* src = rk[l].out + t0 * B;
-    if (kStage) {  // whole tile -> smem, 16-byte cp.async (LDGSTS), overlaps phase 1
-      const uint32_t n16 = (nt * B + 15) / 16;
-      for (uint32_t u = tid; u < n16; u += kThreads) cp_async16(smem + 16 * u, src + 16 * (uint64_t)u);
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    }
+    const uint8_t* st = smem + (it & 1) * lay.stage_stride;
+    const int32_t* dest_s = reinterpret_cast<const int32_t*>(st + lay.stage_items);
     for (int x = tid; x < kWarps * R; x += kThreads) wcnt[x] = 0;
+    // phase 2 inputs that do not depend on the tile data
+    for (int d = tid; d < R; d += kThreads) {
+      const int64_t o = dst_off ? dst_off[(uint64_t)l * R + d] : 0;
+      const uint8_t* base = dst_table ? dst_table[d] : rk[l].binned[cur];
+      dbase[d] = (uintptr_t)base + (uintptr_t)(o * (int64_t)B);
+      rstart[d] = rk[l].O[(uint64_t)d * tiles + t];  // global base of (d, t), parked in rstart for now
+    }
+    mbar_wait(&mbar[it & 1], (it >> 1) & 1);
     __syncthreads();
-    // phase 1: stable rank of each item among same-dest items of its warp
-    const int32_t* dest = rk[l].dest + t0;
+    // phase 1: stable rank among same-destination items of the warp's chunk
     int dk[kMaxK];
     uint32_t rk_[kMaxK];
 #pragma unroll
     for (int k = 0; k < kMaxK; ++k) {
       if (k < (int)K) {
         const uint32_t il = w * 32 * K + k * 32 + lane;
-        const int d = il < nt ? dest[il] : R;
+        const int d = il < nt ? dest_s[il] : R;
         const unsigned m = __match_any_sync(kFull, d);
         uint32_t c = 0;
         if (d < R) c = wcnt[w * R + d];
@@ -299,50 +431,82 @@ k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, int 
         rk_[k] = c + __popc(m & lanemask_lt());
       }
     }
-    if (kStage) cp_async_wait_all();
     __syncthreads();
-    // phase 2: per-dest warp bases, tile run starts, global bases
-    const uint32_t* O = rk[l].O;
+    // phase 2: warp bases per destination; tile-local run starts
     for (int d = tid; d < R; d += kThreads) {
       uint32_t run = 0;
       for (int i = 0; i < kWarps; ++i) { wbase[i * R + d] = run; run += wcnt[i * R + d]; }
-      rstart[d] = run;  // tile count for now
-      gbase[d] = O[(uint64_t)d * tiles + t];
+      tcnt[d] = run;
     }
     __syncthreads();
     if (tid == 0) {
       uint32_t acc = 0;
-      for (int d = 0; d < R; ++d) { const uint32_t c = rstart[d]; rstart[d] = acc; acc += c; }
+      for (int d = 0; d < R; ++d) { const uint32_t c = tcnt[d]; tcnt[d] = acc; acc += c; }  // tcnt := tile run start
     }
     __syncthreads();
-    // phase 3: tile-local dest-major order -> source index and global slot
+    // phase 3: destination-major order -> (source item, destination, position)
 #pragma unroll
     for (int k = 0; k < kMaxK; ++k) {
       if (k < (int)K && dk[k] < R) {
         const int d = dk[k];
         const uint32_t r = wbase[w * R + d] + rk_[k];
-        const uint32_t p = rstart[d] + r;
+        const uint32_t p = tcnt[d] + r;
         src_of[p] = (uint16_t)(w * 32 * K + k * 32 + lane);
-        dpos[p] = gbase[d] + r;
+        pd[p] = (uint16_t)d;
+        dpos[p] = rstart[d] + r;
       }
     }
     __syncthreads();
     // phase 4: coalesced write of every destination run
-    U* dstU = reinterpret_cast<U*>(rk[l].binned[cur]);
-    const U* srcU = kStage ? items_s : reinterpret_cast<const U*>(src);
+    const U* srcU = kStageItems ? reinterpret_cast<const U*>(st) : reinterpret_cast<const U*>(rk[l].out + t0 * B);
     if (UPI <= 64) {
       const uint32_t units = nt * UPI;
       for (uint32_t x = tid; x < units; x += kThreads) {
         const uint32_t p = divU.div(x), u = x - p * UPI;
-        dstU[(uint64_t)dpos[p] * UPI + u] = srcU[(uint32_t)src_of[p] * UPI + u];
+        U* dst = reinterpret_cast<U*>(dbase[pd[p]]);
+        dst[(uint64_t)dpos[p] * UPI + u] = srcU[(uint32_t)src_of[p] * UPI + u];
       }
     } else {
-      for (uint32_t p = w; p < nt; p += kWarps)
-        for (uint32_t u = lane; u < UPI; u += 32)
-          dstU[(uint64_t)dpos[p] * UPI + u] = srcU[(uint64_t)src_of[p] * UPI + u];
+      for (uint32_t p = w; p < nt; p += kWarps) {
+        U* dst = reinterpret_cast<U*>(dbase[pd[p]]) + (uint64_t)dpos[p] * UPI;
+        const U* src = srcU + (uint64_t)src_of[p] * UPI;
+        for (uint32_t u = lane; u < UPI; u += 32) dst[u] = src[u];
+      }
     }
-    __syncthreads();
+    __syncthreads();  // every thread is done with this stage
+    if (tid == 0) {
+      fence_proxy_async();  // order the generic-proxy reads before the async refill
+      issue(it + 2);
+    }
   }
+  if (dst_table) __threadfence_system();  // pushes to peer memory complete before the kernel does
+}
+
+// ---------------------------------------------------------------- a5 plan (FUSED)
+
+// One block per local rank l (global g): dst_off[l][d] = recv_off_d[g] -
+// send_off_g[d] from the all-gathered count matrix, the
+// rank's incoming count, and the collective overflow decision (Z3).
+__global__ void k_plan(const uint64_t* __restrict__ C, int grank0, int R, uint64_t cap, int64_t* __restrict__ dst_off,
+                       uint64_t* __restrict__ num_in, int* __restrict__ ovf) {
+  __shared__ int s_ovf;
+  const int l = blockIdx.x, g = grank0 + l;
+  if (threadIdx.x == 0) s_ovf = 0;
+  __syncthreads();
+  for (int d = threadIdx.x; d < R; d += blockDim.x) {
+    uint64_t recv_off = 0, col = 0, send_off = 0;
+    for (int s = 0; s < R; ++s) {
+      const uint64_t c = C[(uint64_t)s * R + d];
+      if (s < g) recv_off += c;
+      col += c;
+    }
+    for (int e = 0; e < d; ++e) send_off += C[(uint64_t)g * R + e];
+    dst_off[(uint64_t)l * R + d] = (int64_t)recv_off - (int64_t)send_off;
+    if (col > cap) s_ovf = 1;
+    if (d == g) num_in[l] = col;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && l == 0) *ovf = s_ovf;  // every block computes the same decision
 }
 
 // ---------------------------------------------------------------- a6 copy (PEER)
@@ -379,9 +543,9 @@ k_copy(const CopyRun* __restrict__ runs, const RankDev* __restrict__ rk, int R, 
 
 // ---------------------------------------------------------------- a7 wrap-up
 
-__global__ void k_wrapup(CtrlDev* ctrl, const uint64_t* num_in, int L) {
+__global__ void k_wrapup(CtrlDev* ctrl, const uint64_t* num_in, int L, const int* ovf) {
   const int l = threadIdx.x;
-  if (l < L) {
+  if (l < L && !(ovf && *ovf)) {
     ctrl[l].ctr = 0;
     ctrl[l].invalid = 0;
     ctrl[l].num_in = num_in[l];
@@ -409,20 +573,17 @@ static uint32_t unit_for(uint64_t B, uintptr_t align_bits) {
 }
 
 uint32_t choose_tile(uint64_t item_bytes) {
-  // smem per tile ~ T*(B + 6); keep ~100 KB so two CTAs fit on an SM.
-  uint64_t t = (96u * 1024u) / (item_bytes + 6);
+  // two pipeline stages of ~48 KiB (items + dests) so two CTAs fit on an SM
+  uint64_t t = (48u * 1024u) / (item_bytes + 4);
   t = (t / kThreads) * kThreads;
   if (t < (uint64_t)kThreads) t = kThreads;
   if (t > (uint64_t)kThreads * kMaxK) t = kThreads * kMaxK;
   return (uint32_t)t;
 }
 
-static bool stage_tile(uint32_t T, uint64_t B) { return (uint64_t)T * B <= 128u * 1024u; }
+static bool stage_items(uint32_t T, uint64_t B) { return 2ull * T * (B + 4) <= 200u * 1024u; }
 
-size_t scatter_smem_bytes(uint32_t T, uint64_t B, int R) {
-  const size_t items = stage_tile(T, B) ? (((size_t)T * B + 15) & ~(size_t)15) : 0;
-  return items + ((2 * (size_t)T + 15) & ~(size_t)15) + 4 * (size_t)T + 4 * (2 * (size_t)kWarps * R + 2 * (size_t)R);
-}
+size_t scatter_smem_bytes(uint32_t T, uint64_t B, int R) { return scatter_layout(T, B, R, stage_items(T, B)).total; }
 
 int launch_emit_bulk(Ctx* c, int local, const uint8_t* items, const int32_t* dests, uint64_t n) {
   if (n == 0) return RAFI_OK;
@@ -456,8 +617,15 @@ static int persistent_grid(Ctx* c, int per_sm) {
 
 int launch_hist(Ctx* c) {
   const int grid = persistent_grid(c, 8);
-  k_hist<<<grid, kThreads, sizeof(uint32_t) * c->R, c->stream>>>(rank_table(c), c->ctrl, c->L, c->R, c->cap,
-                                                                 c->tile);
+  const size_t sm = sizeof(uint32_t) * c->R;
+#define HIST(RM) k_hist<RM><<<grid, kThreads, sm, c->stream>>>(rank_table(c), c->ctrl, c->L, c->R, c->cap, c->tile)
+  if (c->R <= 1) HIST(1);
+  else if (c->R <= 2) HIST(2);
+  else if (c->R <= 4) HIST(4);
+  else if (c->R <= 8) HIST(8);
+  else if (c->R <= 16) HIST(16);
+  else HIST(0);
+#undef HIST
   RAFI_CK_CUDA(cudaGetLastError());
   c->launches += 1; c->fwd_launches += 1;
   return RAFI_OK;
@@ -472,41 +640,51 @@ int launch_scan(Ctx* c) {
 }
 
 template <typename U>
-static int launch_scatter_t(Ctx* c, uint32_t UPI, int grid, size_t smem, bool stage) {
+static int launch_scatter_t(Ctx* c, bool fused, uint32_t UPI, int grid) {
   const FastDiv dv(UPI);
-  const uint32_t items_smem = stage ? (uint32_t)(((uint64_t)c->tile * c->B + 15) & ~(uint64_t)15) : 0u;
-  if (stage) {
+  const bool si = stage_items(c->tile, c->B);
+  const ScatterLayout lay = scatter_layout(c->tile, c->B, c->R, si);
+  uint8_t* const* table = fused ? c->in_table_dev : nullptr;
+  const int64_t* off = fused ? c->off_dev : nullptr;
+  const int* ovf = fused ? c->ovf_dev : nullptr;
+  if (si) {
     auto k = k_scatter<U, true>;
-    RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<grid, kThreads, smem, c->stream>>>(rank_table(c), c->ctrl, c->L, c->R, c->cap, c->tile, c->cur,
-                                          (uint32_t)c->B, UPI, dv, items_smem);
+    RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
+    k<<<grid, kThreads, lay.total, c->stream>>>(rank_table(c), c->ctrl, table, off, ovf, c->L, c->R, c->cap, c->tile,
+                                               c->cur, (uint32_t)c->B, UPI, dv, lay);
   } else {
     auto k = k_scatter<U, false>;
-    RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<grid, kThreads, smem, c->stream>>>(rank_table(c), c->ctrl, c->L, c->R, c->cap, c->tile, c->cur,
-                                          (uint32_t)c->B, UPI, dv, items_smem);
+    RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
+    k<<<grid, kThreads, lay.total, c->stream>>>(rank_table(c), c->ctrl, table, off, ovf, c->L, c->R, c->cap, c->tile,
+                                               c->cur, (uint32_t)c->B, UPI, dv, lay);
   }
   RAFI_CK_CUDA(cudaGetLastError());
   return RAFI_OK;
 }
 
-int launch_scatter(Ctx* c) {
+int launch_scatter(Ctx* c, bool fused) {
   const uint32_t unit = unit_for(c->B, 0);
   const uint32_t UPI = (uint32_t)(c->B / unit);
-  const bool stage = stage_tile(c->tile, c->B);
   const size_t smem = scatter_smem_bytes(c->tile, c->B, c->R);
   const int per_sm = smem <= 110 * 1024 ? 2 : 1;
   const int grid = persistent_grid(c, per_sm);
   int rc;
   switch (unit) {
-    case 16: rc = launch_scatter_t<uint4>(c, UPI, grid, smem, stage); break;
-    case 8: rc = launch_scatter_t<uint2>(c, UPI, grid, smem, stage); break;
-    case 4: rc = launch_scatter_t<uint32_t>(c, UPI, grid, smem, stage); break;
-    case 2: rc = launch_scatter_t<uint16_t>(c, UPI, grid, smem, stage); break;
-    default: rc = launch_scatter_t<uint8_t>(c, UPI, grid, smem, stage); break;
+    case 16: rc = launch_scatter_t<uint4>(c, fused, UPI, grid); break;
+    case 8: rc = launch_scatter_t<uint2>(c, fused, UPI, grid); break;
+    case 4: rc = launch_scatter_t<uint32_t>(c, fused, UPI, grid); break;
+    case 2: rc = launch_scatter_t<uint16_t>(c, fused, UPI, grid); break;
+    default: rc = launch_scatter_t<uint8_t>(c, fused, UPI, grid); break;
   }
   if (rc == RAFI_OK) { c->launches += 1; c->fwd_launches += 1; }
   return rc;
+}
+
+int launch_plan(Ctx* c) {
+  k_plan<<<c->L, 256, 0, c->stream>>>(c->Cdev, c->proc * c->L, c->R, c->cap, c->off_dev, c->plan_dev, c->ovf_dev);
+  RAFI_CK_CUDA(cudaGetLastError());
+  c->launches += 1; c->fwd_launches += 1;
+  return RAFI_OK;
 }
 
 int launch_copy(Ctx* c, int max_chunks) {
@@ -530,7 +708,7 @@ int launch_copy(Ctx* c, int max_chunks) {
 }
 
 int launch_wrapup(Ctx* c) {
-  k_wrapup<<<1, 32 * ((c->L + 31) / 32), 0, c->stream>>>(c->ctrl, c->plan_dev, c->L);
+  k_wrapup<<<1, 32 * ((c->L + 31) / 32), 0, c->stream>>>(c->ctrl, c->plan_dev, c->L, c->ovf_dev);
   RAFI_CK_CUDA(cudaGetLastError());
   c->launches += 1; c->fwd_launches += 1;
   return RAFI_OK;

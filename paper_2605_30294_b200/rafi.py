@@ -28,7 +28,7 @@ OPT_EXCHANGE = 1
 OPT_TIMING = 2
 OPT_TILE = 3
 OPT_SELF_DIRECT = 4
-EXCHANGE_AUTO, EXCHANGE_NCCL, EXCHANGE_PEER = 0, 1, 2
+EXCHANGE_AUTO, EXCHANGE_NCCL, EXCHANGE_PEER, EXCHANGE_FUSED = 0, 1, 2, 3
 
 
 class DeviceView(C.Structure):

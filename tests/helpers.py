@@ -26,7 +26,11 @@ def snapshot_world(ctx, L, B):
 
 def p1_forward(ctx, L, B, check_binned=True):
     """One forward of a single-process context with L local ranks, checked
-    bit-exactly against the oracle run on the GPU's own snapshot."""
+    bit-exactly against the oracle run on the GPU's own snapshot.  The send
+    batch is compared too unless the FUSED exchange (which writes none) ran."""
+    from paper_2605_30294_b200 import rafi
+    if ctx.get_option(rafi.OPT_EXCHANGE) == rafi.EXCHANGE_FUSED:
+        check_binned = False
     w, snaps = snapshot_world(ctx, L, B)
     G_o = w.forward()
     G_g = ctx.forward_rc()

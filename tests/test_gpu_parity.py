@@ -79,11 +79,16 @@ CASES = [
 ]
 
 
+EXCHANGES = {"fused": 3, "peer": 2}
+
+
+@pytest.mark.parametrize("exchange", sorted(EXCHANGES))
 @pytest.mark.parametrize("B,L,n,pattern", CASES)
-def test_forward_snapshot_parity(B, L, n, pattern):
+def test_forward_snapshot_parity(B, L, n, pattern, exchange):
     inputs = make_inputs(L, n, B, pattern, 1234 + B, invalid_frac=0.01)
     cap = max(n * L, 1)
     with _ctx(B, cap, L) as ctx:
+        ctx.set_option(rafi.OPT_EXCHANGE, EXCHANGES[exchange])
         _emit_all(ctx, inputs)
         p1_forward(ctx, L, B)
         # a second round on the same context (counters reset, buffers reused)
@@ -121,6 +126,17 @@ def test_forward_canonical_parity(B, L, n, pattern):
 
 
 # ------------------------------------------------------------------ edge cases
+
+def test_default_exchange_is_fused_and_nccl_single_rank():
+    with _ctx(16, 1000, 1) as ctx:
+        assert ctx.get_option(rafi.OPT_EXCHANGE) == rafi.EXCHANGE_FUSED
+        ctx.set_option(rafi.OPT_EXCHANGE, rafi.EXCHANGE_NCCL)   # R=1: the self run is a local copy
+        ctx.emit_bulk(synth.make_items(0, 0, 777, 16), np.zeros(777, np.int32))
+        p1_forward(ctx, 1, 16)
+    with _ctx(16, 1000, 2) as ctx:   # NCCL staging needs one local rank per process
+        with pytest.raises(rafi.RafiError):
+            ctx.set_option(rafi.OPT_EXCHANGE, rafi.EXCHANGE_NCCL)
+
 
 def test_empty_forward_is_termination():
     with _ctx(32, 100, 3) as ctx:
@@ -223,13 +239,15 @@ def test_random_walk_cfg1_shape():
 
 # ------------------------------------------------------------------ full size (bench shape)
 
+@pytest.mark.parametrize("exchange", ["fused", "peer"])
 @pytest.mark.parametrize("L,n", [(1, 16 * 1024 * 1024), (8, 2 * 1024 * 1024)])
-def test_full_size_cfg2_shape(L, n):
+def test_full_size_cfg2_shape(L, n, exchange):
     """BASELINE configs[1] per-rank shape (16M x 48-B items, uniform) at R=1,
     and 8 logical ranks x 2M on one GPU; P1 bit-exact on everything."""
     B = 48
     cap = n if L == 1 else n + n // 8
     with _ctx(B, cap, L) as ctx:
+        ctx.set_option(rafi.OPT_EXCHANGE, EXCHANGES[exchange])
         for l in range(L):
             ctx.drv_emit_synthetic(synth.PATTERNS["uniform"], synth.CONFIG_SEEDS[2], 0, n, local=l)
         p1_forward(ctx, L, B)
