@@ -47,6 +47,37 @@ int rafi_drv_emit_synthetic(rafi_ctx* ctx, int local, int pattern, uint64_t seed
  * re-emitted once rnd > last_round (the walk ends). */
 int rafi_drv_random_walk(rafi_ctx* ctx, uint64_t seed, uint32_t rnd, uint32_t last_round);
 
+/* ---- cfg4: particle advection proxy (§5.4) ----------------
+ * Domain [0,1)^3 split into gx*gy*gz macrocells, rank = (cz*gy + cy)*gx + cx
+ * (R must equal gx*gy*gz).  Item (16 B): {u32 id; float x, y, z}.
+ * seed: local rank `local` creates n particles, id = rank*n + i, uniformly in
+ * its own cell (u_k = top 24 bits of splitmix64(seed ^ id<<3 ^ k) * 2^-24),
+ * and emits each to owner(position).
+ * step: every incoming particle of every local rank takes one RK4 step of
+ * v = omega*(-(y-1/2), x-1/2, 0) + (0, 0, eps) with step h; it
+ * retires if it left [0,1)^3 or rnd >= max_rounds, else it is emitted to
+ * owner(new position).  Float math is + - * / only, no FMA
+ * contraction, so the CPU twin in oracle/ matches bit for bit. */
+int rafi_drv_advect_seed(rafi_ctx* ctx, int local, uint64_t n, uint64_t seed, int gx, int gy, int gz);
+int rafi_drv_advect_step(rafi_ctx* ctx, uint32_t rnd, uint32_t max_rounds, float omega, float eps, float h, int gx,
+                         int gy, int gz);
+
+/* ---- cfg3: brick-decomposed ray marcher proxy ----
+ * Same brick decomposition.  Item (48 B): {float o[3], d[3], t; u32 id;
+ * float integral; u32 rng, bounces, pad}.
+ * seed: n rays per local rank, origin uniform in its brick, direction a
+ * normalised hashed vector (sqrt and /), emitted to owner(origin).
+ * step: every incoming ray marches with dt = 1/256: o += dt*d; if it left the
+ * domain it retires (result[id] = integral); if it entered another brick it is
+ * emitted to that brick's rank; else integral += rho(voxel)*dt with rho a
+ * hash of the 1/128 voxel, and with probability p_thr/2^32 per step it
+ * scatters to a new hashed direction (retiring after max_bounces).  After
+ * max_steps steps in one round it is re-emitted to its own rank.
+ * result: device float[R*n] indexed by id. */
+int rafi_drv_march_seed(rafi_ctx* ctx, int local, uint64_t n, uint64_t seed, int gx, int gy, int gz);
+int rafi_drv_march_step(rafi_ctx* ctx, uint32_t rnd, uint64_t seed, uint32_t p_thr, uint32_t max_bounces,
+                        uint32_t max_steps, int gx, int gy, int gz, float* result);
+
 #ifdef __cplusplus
 }
 #endif

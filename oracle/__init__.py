@@ -19,6 +19,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "rafi_oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "proxies.c")]
 _LIB = os.path.join(_HERE, "liborafi.so")
 
 OK = 0
@@ -28,10 +29,12 @@ ERR_RECV_OVERFLOW = -3
 
 
 def build(force: bool = False) -> str:
-    """Compile the oracle (plain gcc, -O2, no fast-math, single-threaded)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    """Compile the oracle (plain gcc, -O2, no fast-math, no FMA contraction,
+    single-threaded)."""
+    if force or not os.path.exists(_LIB) or any(os.path.getmtime(_LIB) < os.path.getmtime(s) for s in _SRCS):
         tmp = _LIB + ".tmp.%d" % os.getpid()
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-fPIC", "-shared", "-o", tmp, _SRC])
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-fPIC", "-shared", "-ffp-contract=off",
+                               "-fno-fast-math", "-o", tmp] + _SRCS + ["-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -76,6 +79,13 @@ def lib():
             "orc_send_off_ptr": (P, [P]),
             "orc_recv_off_ptr": (P, [P]),
             "orc_G": (u64, [P]),
+            # proxies.c (CPU twins of the proxy applications)
+            "orc_grid_owner": (i32, [C.c_float, C.c_float, C.c_float, i32, i32, i32]),
+            "orc_advect_seed": (None, [P, i32, u64, u64, i32, i32, i32]),
+            "orc_advect_step": (None, [P, i32, C.c_uint32, C.c_uint32, C.c_float, C.c_float, C.c_float,
+                                       i32, i32, i32]),
+            "orc_march_seed": (None, [P, i32, u64, u64, i32, i32, i32]),
+            "orc_march_step": (None, [P, i32, u64, C.c_uint32, C.c_uint32, C.c_uint32, i32, i32, i32, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -196,6 +206,32 @@ class World:
 
     def G(self) -> int:
         return int(lib().orc_G(self._w))
+
+    # -- proxy applications (oracle/proxies.c), CPU twins of the GPU drivers --
+    def advect_seed(self, r, n, seed, grid):
+        lib().orc_advect_seed(self._w, r, n, seed, *grid)
+
+    def advect_step(self, r, rnd, max_rounds, omega, eps, h, grid):
+        lib().orc_advect_step(self._w, r, rnd, max_rounds, omega, eps, h, *grid)
+
+    def march_seed(self, r, n, seed, grid):
+        lib().orc_march_seed(self._w, r, n, seed, *grid)
+
+    def march_step(self, r, seed, p_thr, max_bounces, max_steps, grid, result: np.ndarray):
+        assert result.dtype == np.float32 and result.flags["C_CONTIGUOUS"]
+        lib().orc_march_step(self._w, r, seed, p_thr, max_bounces, max_steps, *grid, result.ctypes.data)
+
+
+def grid_owner(x, y, z, grid) -> int:
+    return int(lib().orc_grid_owner(x, y, z, *grid))
+
+
+def grid_dims(R: int):
+    """Brick / macrocell decomposition of [0,1)^3 for R ranks (gx*gy*gz = R)."""
+    dims = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2), 16: (4, 2, 2), 32: (4, 4, 2), 64: (4, 4, 4)}
+    if R in dims:
+        return dims[R]
+    return (R, 1, 1)
 
 
 # -- pipeline pieces of the paper-literal forward, exposed for pinning ------

@@ -45,7 +45,7 @@
 #define ORC_ERR_NOMEM (-2)
 #define ORC_ERR_RECV_OVERFLOW (-3)
 
-typedef struct {
+typedef struct orc_world {
     int R;              /* ranks in the simulated communicator */
     uint64_t cap;       /* queue capacity in items (resizeRayQueues) */
     uint64_t B;         /* item size in bytes ("trivially copyable") */

@@ -23,6 +23,8 @@ BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "librafi.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# proxy drivers: IEEE-exact float (no FMA contraction) so the CPU twins match bit for bit
+PER_FILE = {"drivers.cu": ["-fmad=false", "-prec-div=true", "-prec-sqrt=true", "-ftz=false"]}
 
 
 def nccl_paths():
@@ -59,7 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(src):
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-        cmd = [NVCC] + common + ["-c", src, "-o", obj]
+        cmd = [NVCC] + common + PER_FILE.get(os.path.basename(src), []) + ["-c", src, "-o", obj]
         if src.endswith(".cpp"):
             cmd = [NVCC, "-x", "c++", "-std=c++17", "-O2", "-Xcompiler", "-fPIC,-Wall", "-I", INCLUDE, "-I", inc,
                    "-c", src, "-o", obj]

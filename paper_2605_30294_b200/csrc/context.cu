@@ -239,7 +239,7 @@ static int create(Ctx** out, const rafi_create_params* p) {
   if ((rc = alloc_dev((void**)&c->Cdev, sizeof(uint64_t) * c->R * c->R))) return fail(rc);
   if ((rc = alloc_dev((void**)&c->runs_dev, sizeof(CopyRun) * c->L * c->R))) return fail(rc);
   if ((rc = alloc_dev((void**)&c->plan_dev, sizeof(uint64_t) * c->L))) return fail(rc);
-  if ((rc = alloc_dev((void**)&c->off_dev, sizeof(int64_t) * c->L * c->R))) return fail(rc);
+  if ((rc = alloc_dev((void**)&c->off_dev, sizeof(uint64_t) * c->L * c->R))) return fail(rc);
   if ((rc = alloc_dev((void**)&c->ovf_dev, 2 * sizeof(int)))) return fail(rc);
   if ((rc = alloc_dev((void**)&c->in_table_dev, sizeof(uint8_t*) * c->R))) return fail(rc);
   if (cudaMallocHost((void**)&c->Chost, sizeof(uint64_t) * c->R * c->R) != cudaSuccess ||
@@ -322,7 +322,7 @@ static int64_t forward_fused(Ctx* c) {
   if (c->nprocs > 1)
     RAFI_CK_NCCL(ncclAllGather(c->Cdev + (size_t)c->proc * L * R, c->Cdev, (size_t)L * R, ncclUint64, c->comm,
                                c->stream));
-  RAFI_CK(launch_plan(c));
+  RAFI_CK(launch_plan(c, true));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[3], c->stream));
   // a4 + a6: stable scatter, each destination run written into its receiver's queue
   RAFI_CK(launch_scatter(c, true));
@@ -369,6 +369,7 @@ static int64_t forward_staged(Ctx* c) {
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[1], c->stream));
   RAFI_CK(launch_scan(c));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[2], c->stream));
+  RAFI_CK(launch_plan(c, false));
   RAFI_CK(launch_scatter(c, false));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[3], c->stream));
   // a5: every process learns the whole R x R count matrix.  The all-gather is
@@ -743,7 +744,7 @@ int rafi_set_option(rafi_ctx* ctx, int key, long long v) {
           RAFI_CK(alloc_dev((void**)&r.O, hb));
         }
         c->max_tiles = (c->cap + t - 1) / t;
-        RAFI_CK(upload_rank_table(c));
+              RAFI_CK(upload_rank_table(c));
       }
       c->tile = t;
       return RAFI_OK;

@@ -104,6 +104,176 @@ int launch_walk(rafi_impl::Ctx* c, const rafi_device_view& v, uint64_t seed, uin
   return cudaGetLastError() == cudaSuccess ? RAFI_OK : RAFI_ERR_CUDA;
 }
 
+// ------------------------------------------------------------------ proxies
+// Float arithmetic below is + - * / sqrt only; this file is compiled with
+// -fmad=false (IEEE-exact, no contraction) so the CPU twin matches bit for bit.
+
+constexpr float kTwoM24 = 5.9604644775390625e-08f;  // 2^-24
+
+__device__ __forceinline__ float u24(uint64_t h) { return (float)(uint32_t)(h >> 40) * kTwoM24; }
+
+struct Grid3 {
+  int gx, gy, gz;
+  __device__ __forceinline__ int clampi(int v, int hi) const { return v < 0 ? 0 : (v > hi ? hi : v); }
+  __device__ __forceinline__ int owner(float x, float y, float z) const {
+    const int cx = clampi((int)(x * (float)gx), gx - 1);
+    const int cy = clampi((int)(y * (float)gy), gy - 1);
+    const int cz = clampi((int)(z * (float)gz), gz - 1);
+    return (cz * gy + cy) * gx + cx;
+  }
+  __device__ __forceinline__ void cell(int r, int* cx, int* cy, int* cz) const {
+    *cx = r % gx;
+    *cy = (r / gx) % gy;
+    *cz = r / (gx * gy);
+  }
+};
+
+__device__ __forceinline__ bool inside(float x, float y, float z) {
+  return x >= 0.0f && x < 1.0f && y >= 0.0f && y < 1.0f && z >= 0.0f && z < 1.0f;
+}
+
+struct Particle {
+  uint32_t id;
+  float x, y, z;
+};
+static_assert(sizeof(Particle) == 16, "particle");
+
+struct Ray {
+  float ox, oy, oz, dx, dy, dz, t;
+  uint32_t id;
+  float integral;
+  uint32_t rng, bounces, pad;
+};
+static_assert(sizeof(Ray) == 48, "ray");
+
+__device__ __forceinline__ void seed_pos(uint64_t seed, uint32_t id, const Grid3& G, int r, float* x, float* y,
+                                         float* z) {
+  int cx, cy, cz;
+  G.cell(r, &cx, &cy, &cz);
+  *x = ((float)cx + u24(splitmix64(seed ^ ((uint64_t)id << 3) ^ 0ull))) / (float)G.gx;
+  *y = ((float)cy + u24(splitmix64(seed ^ ((uint64_t)id << 3) ^ 1ull))) / (float)G.gy;
+  *z = ((float)cz + u24(splitmix64(seed ^ ((uint64_t)id << 3) ^ 2ull))) / (float)G.gz;
+}
+
+__device__ __forceinline__ void unit_dir(float ax, float ay, float az, float* dx, float* dy, float* dz) {
+  const float len2 = ax * ax + ay * ay + az * az;
+  if (len2 < 1e-6f) { *dx = 1.0f; *dy = 0.0f; *dz = 0.0f; return; }
+  const float len = sqrtf(len2);
+  *dx = ax / len; *dy = ay / len; *dz = az / len;
+}
+
+__global__ void k_advect_seed(rafi_device_view v, uint64_t n, uint64_t seed, Grid3 G) {
+  rafi::Queue<Particle> q(v);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    Particle p;
+    p.id = (uint32_t)((uint64_t)v.my_rank * n + i);
+    seed_pos(seed, p.id, G, v.my_rank, &p.x, &p.y, &p.z);
+    q.emitOutgoing(p, G.owner(p.x, p.y, p.z));
+  }
+}
+
+__device__ __forceinline__ void field(float omega, float eps, float x, float y, float* vx, float* vy, float* vz) {
+  *vx = -(omega * (y - 0.5f));
+  *vy = omega * (x - 0.5f);
+  *vz = eps;
+}
+
+__global__ void k_advect_step(rafi_device_view v, uint32_t rnd, uint32_t max_rounds, float omega, float eps, float h,
+                              Grid3 G) {
+  rafi::Queue<Particle> q(v);
+  const unsigned long long n = q.numIncoming();
+  const float hh = 0.5f * h, h6 = h / 6.0f;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    Particle p = q.getIncoming(i);
+    float k1x, k1y, k1z, k2x, k2y, k2z, k3x, k3y, k3z, k4x, k4y, k4z;
+    field(omega, eps, p.x, p.y, &k1x, &k1y, &k1z);
+    field(omega, eps, p.x + hh * k1x, p.y + hh * k1y, &k2x, &k2y, &k2z);
+    field(omega, eps, p.x + hh * k2x, p.y + hh * k2y, &k3x, &k3y, &k3z);
+    field(omega, eps, p.x + h * k3x, p.y + h * k3y, &k4x, &k4y, &k4z);
+    p.x = p.x + h6 * (((k1x + 2.0f * k2x) + 2.0f * k3x) + k4x);
+    p.y = p.y + h6 * (((k1y + 2.0f * k2y) + 2.0f * k3y) + k4y);
+    p.z = p.z + h6 * (((k1z + 2.0f * k2z) + 2.0f * k3z) + k4z);
+    if (!inside(p.x, p.y, p.z) || rnd >= max_rounds) continue;  // retires
+    q.emitOutgoing(p, G.owner(p.x, p.y, p.z));
+  }
+}
+
+__global__ void k_march_seed(rafi_device_view v, uint64_t n, uint64_t seed, Grid3 G) {
+  rafi::Queue<Ray> q(v);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    Ray r;
+    r.id = (uint32_t)((uint64_t)v.my_rank * n + i);
+    seed_pos(seed, r.id, G, v.my_rank, &r.ox, &r.oy, &r.oz);
+    const uint64_t b = seed ^ ((uint64_t)r.id << 3);
+    const float ax = 2.0f * u24(splitmix64(b ^ 3ull)) - 1.0f;
+    const float ay = 2.0f * u24(splitmix64(b ^ 4ull)) - 1.0f;
+    const float az = 2.0f * u24(splitmix64(b ^ 5ull)) - 1.0f;
+    unit_dir(ax, ay, az, &r.dx, &r.dy, &r.dz);
+    r.t = 0.0f;
+    r.integral = 0.0f;
+    r.rng = (uint32_t)splitmix64(b ^ 6ull);
+    r.bounces = 0;
+    r.pad = 0;
+    q.emitOutgoing(r, G.owner(r.ox, r.oy, r.oz));
+  }
+}
+
+__global__ void k_march_step(rafi_device_view v, uint64_t seed, uint32_t p_thr, uint32_t max_bounces,
+                             uint32_t max_steps, Grid3 G, float* result) {
+  rafi::Queue<Ray> q(v);
+  const unsigned long long n = q.numIncoming();
+  const int me = v.my_rank;
+  const float D = 0.00390625f;  // 1/256
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    Ray r = q.getIncoming(i);
+    int dest = me;
+    bool retired = false;
+    for (uint32_t s = 0; s < max_steps; ++s) {
+      r.ox = r.ox + D * r.dx;
+      r.oy = r.oy + D * r.dy;
+      r.oz = r.oz + D * r.dz;
+      r.t = r.t + D;
+      if (!inside(r.ox, r.oy, r.oz)) { retired = true; break; }
+      const int o = G.owner(r.ox, r.oy, r.oz);
+      if (o != me) { dest = o; break; }
+      const int ix = G.clampi((int)(r.ox * 128.0f), 127), iy = G.clampi((int)(r.oy * 128.0f), 127),
+                iz = G.clampi((int)(r.oz * 128.0f), 127);
+      const uint64_t hv = splitmix64(seed ^ ((uint64_t)ix << 42) ^ ((uint64_t)iy << 21) ^ (uint64_t)iz);
+      r.integral = r.integral + u24(hv) * D;
+      const uint64_t hr = splitmix64(((uint64_t)r.id << 32) | r.rng);
+      r.rng = (uint32_t)(hr >> 32);
+      if ((uint32_t)hr < p_thr) {
+        r.bounces += 1;
+        if (r.bounces > max_bounces) { retired = true; break; }
+        const float ax = 2.0f * u24(splitmix64(hr ^ 1ull)) - 1.0f;
+        const float ay = 2.0f * u24(splitmix64(hr ^ 2ull)) - 1.0f;
+        const float az = 2.0f * u24(splitmix64(hr ^ 3ull)) - 1.0f;
+        unit_dir(ax, ay, az, &r.dx, &r.dy, &r.dz);
+      }
+    }
+    if (retired) result[r.id] = r.integral;
+    else q.emitOutgoing(r, dest);
+  }
+}
+
+template <class K, class... A>
+int launch_grid(rafi_impl::Ctx* c, uint64_t n, K kernel, A... args) {
+  if (!n) return RAFI_OK;
+  const uint64_t blocks = (n + 255) / 256;
+  const int grid = (int)(blocks < 148 * 16 ? blocks : 148 * 16);
+  kernel<<<grid, 256, 0, c->stream>>>(args...);
+  c->launches += 1;
+  return cudaGetLastError() == cudaSuccess ? RAFI_OK : RAFI_ERR_CUDA;
+}
+
+int check_grid(rafi_impl::Ctx* c, int gx, int gy, int gz) {
+  if (gx < 1 || gy < 1 || gz < 1 || gx * gy * gz != c->R) {
+    rafi_impl::set_error("proxy grid gx*gy*gz must equal the number of ranks");
+    return RAFI_ERR_INVALID_ARG;
+  }
+  return RAFI_OK;
+}
+
 #define RAFI_DRV_SIZES(X) X(16) X(20) X(24) X(32) X(40) X(44) X(48) X(64) X(96) X(128)
 
 }  // namespace
@@ -144,6 +314,66 @@ extern "C" int rafi_drv_random_walk(rafi_ctx* ctx, uint64_t seed, uint32_t rnd, 
     }
     if (rc != RAFI_OK) return rc;
     if (v.num_in) c->launches += 1;
+  }
+  return RAFI_OK;
+}
+
+extern "C" int rafi_drv_advect_seed(rafi_ctx* ctx, int local, uint64_t n, uint64_t seed, int gx, int gy, int gz) {
+  auto* c = reinterpret_cast<rafi_impl::Ctx*>(ctx);
+  if (!c) return RAFI_ERR_INVALID_ARG;
+  rafi_device_view v;
+  int rc = rafi_get_device_view(ctx, local, &v);
+  if (rc != RAFI_OK) return rc;
+  if (v.item_bytes != sizeof(Particle)) return RAFI_ERR_INVALID_ARG;
+  if ((rc = check_grid(c, gx, gy, gz)) != RAFI_OK) return rc;
+  if (cudaSetDevice(c->device) != cudaSuccess) return RAFI_ERR_CUDA;
+  return launch_grid(c, n, k_advect_seed, v, n, seed, Grid3{gx, gy, gz});
+}
+
+extern "C" int rafi_drv_advect_step(rafi_ctx* ctx, uint32_t rnd, uint32_t max_rounds, float omega, float eps, float h,
+                                    int gx, int gy, int gz) {
+  auto* c = reinterpret_cast<rafi_impl::Ctx*>(ctx);
+  if (!c) return RAFI_ERR_INVALID_ARG;
+  int rc = check_grid(c, gx, gy, gz);
+  if (rc != RAFI_OK) return rc;
+  if (c->B != sizeof(Particle)) return RAFI_ERR_INVALID_ARG;
+  if (cudaSetDevice(c->device) != cudaSuccess) return RAFI_ERR_CUDA;
+  for (int l = 0; l < c->L; ++l) {
+    rafi_device_view v;
+    if ((rc = rafi_get_device_view(ctx, l, &v)) != RAFI_OK) return rc;
+    if ((rc = launch_grid(c, v.num_in, k_advect_step, v, rnd, max_rounds, omega, eps, h, Grid3{gx, gy, gz})))
+      return rc;
+  }
+  return RAFI_OK;
+}
+
+extern "C" int rafi_drv_march_seed(rafi_ctx* ctx, int local, uint64_t n, uint64_t seed, int gx, int gy, int gz) {
+  auto* c = reinterpret_cast<rafi_impl::Ctx*>(ctx);
+  if (!c) return RAFI_ERR_INVALID_ARG;
+  rafi_device_view v;
+  int rc = rafi_get_device_view(ctx, local, &v);
+  if (rc != RAFI_OK) return rc;
+  if (v.item_bytes != sizeof(Ray)) return RAFI_ERR_INVALID_ARG;
+  if ((rc = check_grid(c, gx, gy, gz)) != RAFI_OK) return rc;
+  if (cudaSetDevice(c->device) != cudaSuccess) return RAFI_ERR_CUDA;
+  return launch_grid(c, n, k_march_seed, v, n, seed, Grid3{gx, gy, gz});
+}
+
+extern "C" int rafi_drv_march_step(rafi_ctx* ctx, uint32_t rnd, uint64_t seed, uint32_t p_thr, uint32_t max_bounces,
+                                   uint32_t max_steps, int gx, int gy, int gz, float* result) {
+  (void)rnd;
+  auto* c = reinterpret_cast<rafi_impl::Ctx*>(ctx);
+  if (!c || !result) return RAFI_ERR_INVALID_ARG;
+  int rc = check_grid(c, gx, gy, gz);
+  if (rc != RAFI_OK) return rc;
+  if (c->B != sizeof(Ray)) return RAFI_ERR_INVALID_ARG;
+  if (cudaSetDevice(c->device) != cudaSuccess) return RAFI_ERR_CUDA;
+  for (int l = 0; l < c->L; ++l) {
+    rafi_device_view v;
+    if ((rc = rafi_get_device_view(ctx, l, &v)) != RAFI_OK) return rc;
+    if ((rc = launch_grid(c, v.num_in, k_march_step, v, seed, p_thr, max_bounces, max_steps, Grid3{gx, gy, gz},
+                          result)))
+      return rc;
   }
   return RAFI_OK;
 }

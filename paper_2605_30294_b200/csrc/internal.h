@@ -72,8 +72,8 @@ struct LocalRank {
   int32_t* dest = nullptr;    // destination per slot
   uint8_t* binned[2] = {nullptr, nullptr};  // send batches (double-buffered for PEER)
   uint8_t* in = nullptr;      // incoming queue
-  uint32_t* H = nullptr;      // per-tile per-dest counts, dest-major [R][tiles]
-  uint32_t* O = nullptr;      // exclusive scan of H in dest-major order
+  uint32_t* H = nullptr;      // [R][tiles] per-tile per-destination counts
+  uint32_t* O = nullptr;      // [R][tiles] items per destination in earlier tiles
   uint64_t num_in = 0;        // host copy of numIncoming
   uint64_t n_out = 0, dropped = 0, invalid = 0;  // last forward
   uint64_t sent_remote = 0, recv_remote = 0;
@@ -109,7 +109,7 @@ struct Ctx {
   CopyRun* runs_dev = nullptr;        // [L*R] copy plan, device
   CopyRun* runs_host = nullptr;       // [L*R] pinned
   uint64_t* plan_dev = nullptr;       // [L] per local dest: num_in (for wrap-up)
-  int64_t* off_dev = nullptr;         // [L][R] FUSED: recv_off_d[me] - send_off_me[d]
+  uint64_t* off_dev = nullptr;        // [L][R] per-destination base: send_off (staged) / recv_off (FUSED)
   int* ovf_dev = nullptr;             // [1] FUSED: collective receive-overflow flag
   uint8_t** in_table_dev = nullptr;   // [R] every global rank's incoming queue (local or IPC-mapped)
   std::vector<uint8_t*> peer_in;      // host copy of in_table
@@ -138,7 +138,7 @@ int launch_emit_bulk(Ctx* c, int local, const uint8_t* items, const int32_t* des
 int launch_hist(Ctx* c);
 int launch_scan(Ctx* c);
 int launch_scatter(Ctx* c, bool fused);
-int launch_plan(Ctx* c);
+int launch_plan(Ctx* c, bool fused);
 int launch_copy(Ctx* c, int nruns_per_dest);
 int launch_wrapup(Ctx* c);
 size_t scatter_smem_bytes(uint32_t tile, uint64_t item_bytes, int R);

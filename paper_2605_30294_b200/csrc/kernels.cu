@@ -3,9 +3,10 @@
 //   k_emit_bulk   a1  bulk emitOutgoing: block-aggregated atomic append
 //   k_hist        a2  per-tile per-destination counts (replaces key gen +
 //                     radix-sort counting)
-//   k_scan        a3  exclusive scan in destination-major order: tile offsets,
-//                     send counts/offsets, the count-matrix row (replaces the
-//                     boundary kernel + D2H + host gap fill)
+//   k_scan        a3  per-destination prefix over tiles and the count-matrix
+//                     row (replaces the boundary kernel + D2H + host gap fill,
+//                     PAPER:121-124)
+//   k_plan        a5  per-destination bases from the count matrix
 //   k_scatter     a4  stable scatter into one contiguous block per
 //                     destination (replaces the gather), staged
 //                     through shared memory so that both the read of the tile
@@ -149,92 +150,115 @@ __device__ __forceinline__ uint32_t warp_sum(uint32_t x) {
   return x;
 }
 
-// RMAX > 0: per-thread register counters for R <= RMAX (16-byte dest loads,
-// warp-shuffle reduction); RMAX == 0: generic __match_any_sync aggregation.
+constexpr int kHistTilesPerWarp = 4;
+constexpr int kHistTilesPerCta = kWarps * kHistTilesPerWarp;
+constexpr int kHistVec = 8;  // 16-byte dest loads in flight per lane
+
+// Per-tile per-destination counts H[l][d][t] (the counting half of the
+// paper's radix sort by destination).  One warp per tile,
+// kHistTilesPerWarp consecutive tiles per warp, 16-byte loads, 8 in flight per
+// lane; no block-level synchronisation.  RMAX > 0: register counters for
+// R <= RMAX, reduced with warp shuffles; RMAX == 0: per-warp shared-memory
+// counters fed by __match_any_sync aggregation.
 template <int RMAX>
 __global__ void __launch_bounds__(kThreads)
-k_hist(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, int L, int R, uint64_t cap,
-       uint32_t T) {
-  extern __shared__ uint32_t cnt[];  // [R]
-  const int tid = threadIdx.x, lane = tid & 31;
-  for (uint64_t g = blockIdx.x;; g += gridDim.x) {
+k_hist(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, int L, int R, uint64_t cap, uint32_t T) {
+  extern __shared__ uint32_t wc[];  // RMAX == 0: [kWarps][R]
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = 0; k < kHistTilesPerWarp; ++k) {
+    const uint64_t g = ((uint64_t)blockIdx.x * kWarps + w) * kHistTilesPerWarp + k;
     int l;
     uint64_t t, n, tiles;
-    if (!tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) break;
-    for (int d = tid; d < R; d += kThreads) cnt[d] = 0;
-    __syncthreads();
+    if (!tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) return;
     const uint64_t t0 = t * T;
     const uint32_t nt = (uint32_t)umin64(T, n - t0);
-    const int32_t* dest = rk[l].dest + t0;
+    const int4* d4 = reinterpret_cast<const int4*>(rk[l].dest + t0);  // t0*4 is a multiple of 1 KiB
+    uint32_t* H = rk[l].H;
     if (RMAX > 0) {
       uint32_t c[RMAX > 0 ? RMAX : 1];
 #pragma unroll
       for (int r = 0; r < RMAX; ++r) c[r] = 0;
-      const int4* d4 = reinterpret_cast<const int4*>(dest);  // t0*4 is a multiple of 1 KiB
-      for (uint32_t q = tid; q * 4 < nt; q += kThreads) {
-        const int4 v = d4[q];
-        const int e[4] = {v.x, v.y, v.z, v.w};
+      const uint32_t nq = (nt + 3) / 4;
+      for (uint32_t q0 = 0; q0 < nq; q0 += 32 * kHistVec) {
+        int4 v[kHistVec];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (q * 4 + j < nt) {
+        for (int j = 0; j < kHistVec; ++j) {
+          const uint32_t q = q0 + j * 32 + lane;
+          v[j] = q < nq ? d4[q] : make_int4(-1, -1, -1, -1);
+        }
 #pragma unroll
-            for (int r = 0; r < RMAX; ++r) c[r] += (e[j] == r);
+        for (int j = 0; j < kHistVec; ++j) {
+          const uint32_t i0 = (q0 + j * 32 + lane) * 4;
+          const int e[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            const int d = i0 + m < nt ? e[m] : -1;
+#pragma unroll
+            for (int r = 0; r < RMAX; ++r) c[r] += (d == r);
           }
         }
       }
 #pragma unroll
       for (int r = 0; r < RMAX; ++r) {
-        if (r < R) {
-          const uint32_t x = warp_sum(c[r]);
-          if (lane == 0 && x) atomicAdd(&cnt[r], x);
-        }
+        const uint32_t x = warp_sum(c[r]);
+        if (lane == (r & 31) && r < R) H[(uint64_t)r * tiles + t] = x;
       }
     } else {
-      for (uint32_t i = tid; i < T; i += kThreads) {  // T is a multiple of kThreads
+      uint32_t* mine = wc + w * R;
+      for (int d = lane; d < R; d += 32) mine[d] = 0;
+      __syncwarp();
+      const int32_t* dest = rk[l].dest + t0;
+      for (uint32_t i = lane; i < T; i += 32) {  // T is a multiple of 32
         const int d = i < nt ? dest[i] : -1;
         const unsigned m = __match_any_sync(kFull, d);
-        if (d >= 0 && lane == __ffs(m) - 1) atomicAdd(&cnt[d], (uint32_t)__popc(m));
+        if (d >= 0 && lane == __ffs(m) - 1) mine[d] += __popc(m);
+        __syncwarp();
       }
+      for (int d = lane; d < R; d += 32) H[(uint64_t)d * tiles + t] = mine[d];
+      __syncwarp();
     }
-    __syncthreads();
-    uint32_t* H = rk[l].H;
-    for (int d = tid; d < R; d += kThreads) H[(uint64_t)d * tiles + t] = cnt[d];
-    __syncthreads();
   }
 }
 
 // ---------------------------------------------------------------- a3 scan
 
-// One block per local rank: O = exclusive scan of H (dest-major, dense over
-// the rank's actual tiles); the count-matrix row of this rank; counters.
+// One CTA per (destination d, local rank l): O[l][d][t] = sum of H[l][d][0..t)
+// over the rank's live tiles (the paper's segment tally, kept
+// on device), and the row total send_count[d] -> count matrix C[g][d].  The
+// per-destination base (send offset, or the receiver's recv offset under
+// FUSED) is added by k_plan / k_scatter.
 constexpr int kScanThreads = 1024;
-constexpr int kScanV = 4;
+constexpr int kScanV = 8;
 
 __global__ void __launch_bounds__(kScanThreads)
 k_scan(const RankDev* __restrict__ rk, CtrlDev* __restrict__ ctrl, uint64_t* __restrict__ Cmat,
        int grank0, int R, uint64_t cap, uint32_t T) {
   __shared__ uint32_t wsum[kScanThreads / 32];
   __shared__ uint32_t carry_s;
-  const int l = blockIdx.x;
+  const int d = blockIdx.x, l = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint64_t n = n_items(ctrl[l], cap);
-  const uint64_t tiles = (n + T - 1) / T;
-  const uint64_t M = (uint64_t)R * tiles;
-  const uint32_t* H = rk[l].H;
-  uint32_t* O = rk[l].O;
+  const uint64_t M = (n + T - 1) / T;  // live tiles
+  const uint32_t* H = rk[l].H + (uint64_t)d * M;
+  uint32_t* O = rk[l].O + (uint64_t)d * M;
   if (tid == 0) carry_s = 0;
   __syncthreads();
   for (uint64_t base = 0; base < M; base += (uint64_t)kScanThreads * kScanV) {
     uint32_t v[kScanV];
     uint32_t s = 0;
 #pragma unroll
-    for (int j = 0; j < kScanV; ++j) {
-      const uint64_t i = base + (uint64_t)tid * kScanV + j;
+    for (int j = 0; j < kScanV; ++j) {  // element base + j*1024 + tid: coalesced
+      const uint64_t i = base + (uint64_t)j * kScanThreads + tid;
       v[j] = i < M ? H[i] : 0u;
-      s += v[j];
     }
-    // inclusive warp scan of s
-    uint32_t x = s;
+    // this thread owns elements base + tid*kScanV + j: transpose through shared memory
+    __shared__ uint32_t sh[kScanThreads * kScanV];
+#pragma unroll
+    for (int j = 0; j < kScanV; ++j) sh[j * kScanThreads + tid] = v[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kScanV; ++j) { v[j] = sh[tid * kScanV + j]; s += v[j]; }
+    uint32_t x = s;  // inclusive warp scan
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(kFull, x, o);
@@ -243,7 +267,7 @@ k_scan(const RankDev* __restrict__ rk, CtrlDev* __restrict__ ctrl, uint64_t* __r
     if (lane == 31) wsum[w] = x;
     __syncthreads();
     if (w == 0) {
-      uint32_t ws = wsum[lane];
+      const uint32_t ws = wsum[lane];
       uint32_t z = ws;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -253,34 +277,26 @@ k_scan(const RankDev* __restrict__ rk, CtrlDev* __restrict__ ctrl, uint64_t* __r
       wsum[lane] = z - ws;  // exclusive
     }
     __syncthreads();
-    const uint32_t carry = carry_s;
-    uint32_t e = carry + wsum[w] + x - s;  // exclusive prefix of this thread's first element
+    uint32_t e = carry_s + wsum[w] + x - s;
+#pragma unroll
+    for (int j = 0; j < kScanV; ++j) { sh[tid * kScanV + j] = e; e += v[j]; }
+    __syncthreads();
 #pragma unroll
     for (int j = 0; j < kScanV; ++j) {
-      const uint64_t i = base + (uint64_t)tid * kScanV + j;
-      if (i < M) O[i] = e;
-      e += v[j];
+      const uint64_t i = base + (uint64_t)j * kScanThreads + tid;
+      if (i < M) O[i] = sh[j * kScanThreads + tid];
     }
-    __syncthreads();
     if (tid == kScanThreads - 1) carry_s = e;
     __syncthreads();
   }
-  // row of the count matrix: send_count[d] = O[(d+1)*tiles] - O[d*tiles]
-  const uint32_t total = carry_s;
-  for (int d = tid; d < R; d += kScanThreads) {
-    uint64_t c = 0;
-    if (tiles) {
-      const uint32_t a = O[(uint64_t)d * tiles];
-      const uint32_t b = (d + 1 < R) ? O[(uint64_t)(d + 1) * tiles] : total;
-      c = b - a;
-    }
-    Cmat[(uint64_t)(grank0 + l) * R + d] = c;
-  }
   if (tid == 0) {
-    CtrlDev& c = ctrl[l];
-    c.n_out = n;
-    c.dropped = c.ctr - n;
-    c.invalid_last = c.invalid;
+    Cmat[(uint64_t)(grank0 + l) * R + d] = carry_s;
+    if (d == 0) {
+      CtrlDev& c = ctrl[l];
+      c.n_out = n;
+      c.dropped = c.ctr - n;
+      c.invalid_last = c.invalid;
+    }
   }
 }
 
@@ -350,12 +366,14 @@ __host__ __device__ inline ScatterLayout scatter_layout(uint32_t T, uint64_t B, 
 //   * Destination: dst_table == nullptr -> the local send batch binned[cur]
 //     (position = offset in the destination-major batch).  Otherwise the
 //     FUSED exchange: unit goes straight to destination rank d's incoming
-//     queue, dst_table[d] (local HBM or a CUDA-IPC peer mapping over NVLink),
-//     at item index position + dst_off[l][d] (recv_off_d[me] - send_off_me[d]).
+//     queue, dst_table[d] (local HBM or a CUDA-IPC peer mapping over NVLink).
+//   Item index = O[l][d][t] (prefix over earlier tiles) + rank within the tile
+//   + dst_off[l][d], the per-destination base from k_plan: send_off_me[d]
+//   (staged) or recv_off_d[me] (FUSED).
 template <typename U, bool kStageItems>
 __global__ void __launch_bounds__(kThreads, 2)
 k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint8_t* const* __restrict__ dst_table,
-          const int64_t* __restrict__ dst_off, const int* __restrict__ ovf, int L, int R, uint64_t cap, uint32_t T,
+          const uint64_t* __restrict__ dst_off, const int* __restrict__ ovf, int L, int R, uint64_t cap, uint32_t T,
           int cur, uint32_t B, uint32_t UPI, FastDiv divU, ScatterLayout lay) {
   if (ovf && *ovf) return;  // collective receive overflow: move nothing (Z3)
   extern __shared__ __align__(128) uint8_t smem[];
@@ -406,10 +424,10 @@ k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint
     for (int x = tid; x < kWarps * R; x += kThreads) wcnt[x] = 0;
     // phase 2 inputs that do not depend on the tile data
     for (int d = tid; d < R; d += kThreads) {
-      const int64_t o = dst_off ? dst_off[(uint64_t)l * R + d] : 0;
       const uint8_t* base = dst_table ? dst_table[d] : rk[l].binned[cur];
-      dbase[d] = (uintptr_t)base + (uintptr_t)(o * (int64_t)B);
-      rstart[d] = rk[l].O[(uint64_t)d * tiles + t];  // global base of (d, t), parked in rstart for now
+      dbase[d] = (uintptr_t)base;
+      // global base of (d, t), parked in rstart until phase 3
+      rstart[d] = rk[l].O[(uint64_t)d * tiles + t] + (uint32_t)dst_off[(uint64_t)l * R + d];
     }
     mbar_wait(&mbar[it & 1], (it >> 1) & 1);
     __syncthreads();
@@ -482,31 +500,42 @@ k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint
   if (dst_table) __threadfence_system();  // pushes to peer memory complete before the kernel does
 }
 
-// ---------------------------------------------------------------- a5 plan (FUSED)
+// ---------------------------------------------------------------- a5 plan
 
-// One block per local rank l (global g): dst_off[l][d] = recv_off_d[g] -
-// send_off_g[d] from the all-gathered count matrix, the
-// rank's incoming count, and the collective overflow decision (Z3).
-__global__ void k_plan(const uint64_t* __restrict__ C, int grank0, int R, uint64_t cap, int64_t* __restrict__ dst_off,
+// One block per local rank l (global g), from the count matrix:
+//   staged (kFused = false, local rows only): dst_off[l][d] = send_off_g[d]
+//     = sum_{d'<d} C[g][d'] (where d's block starts in g's send batch);
+//   FUSED (all rows, after the all-gather): dst_off[l][d] = recv_off_d[g]
+//     = sum_{s<g} C[s][d] (where g's block starts in d's incoming queue),
+//     num_in[l] = sum_s C[s][g], and the collective overflow decision (Z3).
+template <bool kFused>
+__global__ void k_plan(const uint64_t* __restrict__ C, int grank0, int R, uint64_t cap, uint64_t* __restrict__ dst_off,
                        uint64_t* __restrict__ num_in, int* __restrict__ ovf) {
   __shared__ int s_ovf;
   const int l = blockIdx.x, g = grank0 + l;
   if (threadIdx.x == 0) s_ovf = 0;
   __syncthreads();
   for (int d = threadIdx.x; d < R; d += blockDim.x) {
-    uint64_t recv_off = 0, col = 0, send_off = 0;
-    for (int s = 0; s < R; ++s) {
-      const uint64_t c = C[(uint64_t)s * R + d];
-      if (s < g) recv_off += c;
-      col += c;
+    if (kFused) {
+      uint64_t recv_off = 0, col = 0;
+      for (int s = 0; s < R; ++s) {
+        const uint64_t c = C[(uint64_t)s * R + d];
+        if (s < g) recv_off += c;
+        col += c;
+      }
+      dst_off[(uint64_t)l * R + d] = recv_off;
+      if (col > cap) s_ovf = 1;
+      if (d == g) num_in[l] = col;
+    } else {
+      uint64_t send_off = 0;
+      for (int e = 0; e < d; ++e) send_off += C[(uint64_t)g * R + e];
+      dst_off[(uint64_t)l * R + d] = send_off;
     }
-    for (int e = 0; e < d; ++e) send_off += C[(uint64_t)g * R + e];
-    dst_off[(uint64_t)l * R + d] = (int64_t)recv_off - (int64_t)send_off;
-    if (col > cap) s_ovf = 1;
-    if (d == g) num_in[l] = col;
   }
-  __syncthreads();
-  if (threadIdx.x == 0 && l == 0) *ovf = s_ovf;  // every block computes the same decision
+  if (kFused) {
+    __syncthreads();
+    if (threadIdx.x == 0 && l == 0) *ovf = s_ovf;  // every block computes the same decision
+  }
 }
 
 // ---------------------------------------------------------------- a6 copy (PEER)
@@ -616,15 +645,21 @@ static int persistent_grid(Ctx* c, int per_sm) {
 }
 
 int launch_hist(Ctx* c) {
-  const int grid = persistent_grid(c, 8);
-  const size_t sm = sizeof(uint32_t) * c->R;
-#define HIST(RM) k_hist<RM><<<grid, kThreads, sm, c->stream>>>(rank_table(c), c->ctrl, c->L, c->R, c->cap, c->tile)
-  if (c->R <= 1) HIST(1);
-  else if (c->R <= 2) HIST(2);
-  else if (c->R <= 4) HIST(4);
-  else if (c->R <= 8) HIST(8);
-  else if (c->R <= 16) HIST(16);
-  else HIST(0);
+  const uint64_t tiles_all = std::max<uint64_t>(1, c->max_tiles * (uint64_t)c->L);
+  const int grid = (int)((tiles_all + kHistTilesPerCta - 1) / kHistTilesPerCta);
+#define HIST(RM, SM) \
+  k_hist<RM><<<grid, kThreads, SM, c->stream>>>(rank_table(c), c->ctrl, c->L, c->R, c->cap, c->tile)
+  if (c->R <= 1) HIST(1, 0);
+  else if (c->R <= 2) HIST(2, 0);
+  else if (c->R <= 4) HIST(4, 0);
+  else if (c->R <= 8) HIST(8, 0);
+  else if (c->R <= 16) HIST(16, 0);
+  else if (c->R <= 32) HIST(32, 0);
+  else {
+    const size_t sm = sizeof(uint32_t) * kWarps * c->R;
+    if (sm > 48 * 1024) RAFI_CK_CUDA(cudaFuncSetAttribute(k_hist<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    HIST(0, sm);
+  }
 #undef HIST
   RAFI_CK_CUDA(cudaGetLastError());
   c->launches += 1; c->fwd_launches += 1;
@@ -632,8 +667,8 @@ int launch_hist(Ctx* c) {
 }
 
 int launch_scan(Ctx* c) {
-  k_scan<<<c->L, kScanThreads, 0, c->stream>>>(rank_table(c), c->ctrl, c->Cdev, c->proc * c->L, c->R, c->cap,
-                                               c->tile);
+  k_scan<<<dim3(c->R, c->L), kScanThreads, 0, c->stream>>>(rank_table(c), c->ctrl, c->Cdev, c->proc * c->L, c->R,
+                                                           c->cap, c->tile);
   RAFI_CK_CUDA(cudaGetLastError());
   c->launches += 1; c->fwd_launches += 1;
   return RAFI_OK;
@@ -645,7 +680,7 @@ static int launch_scatter_t(Ctx* c, bool fused, uint32_t UPI, int grid) {
   const bool si = stage_items(c->tile, c->B);
   const ScatterLayout lay = scatter_layout(c->tile, c->B, c->R, si);
   uint8_t* const* table = fused ? c->in_table_dev : nullptr;
-  const int64_t* off = fused ? c->off_dev : nullptr;
+  const uint64_t* off = c->off_dev;
   const int* ovf = fused ? c->ovf_dev : nullptr;
   if (si) {
     auto k = k_scatter<U, true>;
@@ -680,8 +715,11 @@ int launch_scatter(Ctx* c, bool fused) {
   return rc;
 }
 
-int launch_plan(Ctx* c) {
-  k_plan<<<c->L, 256, 0, c->stream>>>(c->Cdev, c->proc * c->L, c->R, c->cap, c->off_dev, c->plan_dev, c->ovf_dev);
+int launch_plan(Ctx* c, bool fused) {
+  if (fused)
+    k_plan<true><<<c->L, 256, 0, c->stream>>>(c->Cdev, c->proc * c->L, c->R, c->cap, c->off_dev, c->plan_dev, c->ovf_dev);
+  else
+    k_plan<false><<<c->L, 256, 0, c->stream>>>(c->Cdev, c->proc * c->L, c->R, c->cap, c->off_dev, c->plan_dev, c->ovf_dev);
   RAFI_CK_CUDA(cudaGetLastError());
   c->launches += 1; c->fwd_launches += 1;
   return RAFI_OK;

@@ -94,6 +94,12 @@ SIGNATURES = {
     "rafi_drv_emit_synthetic": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_uint32, C.c_uint64,
                                           C.c_uint64, C.c_int, C.c_uint64]),
     "rafi_drv_random_walk": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32]),
+    "rafi_drv_advect_seed": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int]),
+    "rafi_drv_advect_step": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_float, C.c_float, C.c_float,
+                                       C.c_int, C.c_int, C.c_int]),
+    "rafi_drv_march_seed": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int]),
+    "rafi_drv_march_step": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                      C.c_int, C.c_int, C.c_int, C.c_void_p]),
     "rafi_plan": (C.c_int, [C.c_int, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                             C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_int)]),
 }
@@ -269,6 +275,19 @@ class Context:
 
     def drv_random_walk(self, seed: int, rnd: int, last_round: int):
         _check(lib().rafi_drv_random_walk(self._h, seed, rnd, last_round), "rafi_drv_random_walk")
+
+    def drv_advect_seed(self, n: int, seed: int, grid, local: int = 0):
+        _check(lib().rafi_drv_advect_seed(self._h, local, n, seed, *grid), "rafi_drv_advect_seed")
+
+    def drv_advect_step(self, rnd: int, max_rounds: int, omega: float, eps: float, h: float, grid):
+        _check(lib().rafi_drv_advect_step(self._h, rnd, max_rounds, omega, eps, h, *grid), "rafi_drv_advect_step")
+
+    def drv_march_seed(self, n: int, seed: int, grid, local: int = 0):
+        _check(lib().rafi_drv_march_seed(self._h, local, n, seed, *grid), "rafi_drv_march_seed")
+
+    def drv_march_step(self, rnd: int, seed: int, p_thr: int, max_bounces: int, max_steps: int, grid, result):
+        _check(lib().rafi_drv_march_step(self._h, rnd, seed, p_thr, max_bounces, max_steps, *grid, _ptr(result)),
+               "rafi_drv_march_step")
 
     # -- introspection --------------------------------------------------------------
     def num_incoming(self, local=0) -> int:

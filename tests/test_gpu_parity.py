@@ -76,6 +76,7 @@ CASES = [
     (44, 4, 50000, "uniform"), (48, 8, 30000, "uniform"), (64, 8, 12345, "skewed"),
     (96, 3, 9000, "all_to_one"), (128, 4, 7000, "uniform"), (3, 2, 6000, "uniform"),
     (20, 7, 5001, "uniform"), (520, 3, 2000, "uniform"), (200, 2, 3000, "self"),
+    (32, 20, 2000, "skewed"), (16, 40, 1000, "uniform"), (8, 64, 700, "round_robin"),
 ]
 
 
