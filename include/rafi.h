@@ -171,6 +171,33 @@ int rafi_emit_bulk(rafi_ctx* ctx, int local, const void* items, const int32_t* d
  * anything ordered after it on the stream sees the new incoming queues. */
 int64_t rafi_forward(rafi_ctx* ctx);
 
+/* ---- device-side termination and CUDA graphs --------- */
+
+/* The FUSED forward without any host synchronisation: enqueues the complete
+ * forward on the context stream (so it can be captured into a CUDA graph,
+ * NCCL collectives included) and, when the work runs, writes G -- the same
+ * value rafi_forward returns -- to *G_dev (device-visible u64;
+ * it may be mapped pinned host memory).  On a receive overflow nothing moves
+ * and *G_dev = ~0ull; the context becomes unusable at the next
+ * rafi_sync_host.  Host-side counters (rafi_num_incoming, rafi_get_stats and
+ * the num_in field of views) are NOT refreshed: device code must read
+ * numIncoming through num_in_dev (rafi::Queue does), and launches sized on
+ * the host should cover the capacity.  COLLECTIVE.  Needs the FUSED exchange
+ * (RAFI_ERR_UNSUPPORTED otherwise). */
+int rafi_forward_async(rafi_ctx* ctx, unsigned long long* G_dev);
+
+/* Blocks until the context stream is idle and refreshes the host-side
+ * counters from the device (after rafi_forward_async / graph launches). */
+int rafi_sync_host(rafi_ctx* ctx);
+
+/* Capture work issued on the context stream (app kernels, rafi_forward_async)
+ * into an executable CUDA graph (*exec, cudaGraphExec_t), and replay it.  The
+ * context stream must not be the legacy default stream. */
+int rafi_capture_begin(rafi_ctx* ctx);
+int rafi_capture_end(rafi_ctx* ctx, void** exec);
+int rafi_graph_launch(rafi_ctx* ctx, void* exec);
+int rafi_graph_destroy(void* exec);
+
 /* ---- introspection (host copies; ordered on the context stream, blocking) --- */
 
 int rafi_num_ranks(const rafi_ctx* ctx);                 /* R, or < 0 on error */

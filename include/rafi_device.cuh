@@ -47,8 +47,16 @@ struct Queue {
 
   __host__ __device__ explicit Queue(const rafi_device_view& view) : v(view) {}
 
-  /* numIncoming(): valid on host and device. */
-  __host__ __device__ unsigned long long numIncoming() const { return v.num_in; }
+  /* numIncoming(): valid on host and device.  Device code reads the
+     device-resident count, so it stays correct across rafi_forward_async /
+     graph replays; the host reads the copy in the view. */
+  __host__ __device__ unsigned long long numIncoming() const {
+#ifdef __CUDA_ARCH__
+    return *reinterpret_cast<const unsigned long long*>(v.num_in_dev);
+#else
+    return v.num_in;
+#endif
+  }
 
   /* getIncoming(i). */
   __device__ T getIncoming(unsigned long long i) const {

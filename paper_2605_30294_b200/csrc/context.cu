@@ -309,10 +309,9 @@ static int book_keep(Ctx* c, uint64_t* G_out) {
 // FUSED forward: counts first, then one kernel bins and pushes every run
 // straight into its destination's incoming queue (NEXT-1 of SURVEY §8(f)).
 //   hist -> scan -> [all-gather counts] -> plan -> scatter+push -> [barrier] -> wrap-up
-static int64_t forward_fused(Ctx* c) {
+static int enqueue_fused(Ctx* c, unsigned long long* G_dev, bool T) {
   const int R = c->R, L = c->L;
   c->fwd_launches = 0;
-  const bool T = c->timing;
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[0], c->stream));
   RAFI_CK(launch_hist(c));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[1], c->stream));
@@ -322,7 +321,7 @@ static int64_t forward_fused(Ctx* c) {
   if (c->nprocs > 1)
     RAFI_CK_NCCL(ncclAllGather(c->Cdev + (size_t)c->proc * L * R, c->Cdev, (size_t)L * R, ncclUint64, c->comm,
                                c->stream));
-  RAFI_CK(launch_plan(c, true));
+  RAFI_CK(launch_plan(c, true, G_dev));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[3], c->stream));
   // a4 + a6: stable scatter, each destination run written into its receiver's queue
   RAFI_CK(launch_scatter(c, true));
@@ -334,15 +333,28 @@ static int64_t forward_fused(Ctx* c) {
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[5], c->stream));
   RAFI_CK(launch_wrapup(c));  // a7 (skipped on device if the overflow flag is set)
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[6], c->stream));
-  RAFI_CK_CUDA(cudaMemcpyAsync(c->Chost, c->Cdev, sizeof(uint64_t) * R * R, cudaMemcpyDeviceToHost, c->stream));
-  RAFI_CK_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl, sizeof(CtrlDev) * L, cudaMemcpyDeviceToHost, c->stream));
+  return RAFI_OK;
+}
+
+// Host refresh after device work: count matrix + counters -> host bookkeeping.
+static int refresh_host(Ctx* c, uint64_t* G) {
+  RAFI_CK_CUDA(cudaMemcpyAsync(c->Chost, c->Cdev, sizeof(uint64_t) * c->R * c->R, cudaMemcpyDeviceToHost, c->stream));
+  RAFI_CK_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl, sizeof(CtrlDev) * c->L, cudaMemcpyDeviceToHost, c->stream));
   RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
-  uint64_t G = 0;
-  if (book_keep(c, &G)) {
+  c->host_stale = false;
+  if (book_keep(c, G)) {
     c->broken = true;
     set_error("receive overflow: some rank would receive more than its capacity");
     return RAFI_ERR_RECV_OVERFLOW;
   }
+  return RAFI_OK;
+}
+
+static int64_t forward_fused(Ctx* c) {
+  const bool T = c->timing;
+  RAFI_CK(enqueue_fused(c, nullptr, T));
+  uint64_t G = 0;
+  RAFI_CK(refresh_host(c, &G));
   if (T) {
     c->st.ms_hist = ev_ms(c->ev[0], c->ev[1]);
     c->st.ms_scan = ev_ms(c->ev[1], c->ev[2]);
@@ -634,6 +646,67 @@ int64_t rafi_forward(rafi_ctx* ctx) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c) return RAFI_ERR_INVALID_ARG;
   return forward(c);
+}
+
+int rafi_forward_async(rafi_ctx* ctx, unsigned long long* G_dev) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !G_dev) return RAFI_ERR_INVALID_ARG;
+  if (c->broken) { set_error("context unusable after an earlier collective error"); return RAFI_ERR_STATE; }
+  if (c->exchange_eff != RAFI_EXCHANGE_FUSED) {
+    set_error("rafi_forward_async needs the FUSED exchange");
+    return RAFI_ERR_UNSUPPORTED;
+  }
+  RAFI_CK_CUDA(cudaSetDevice(c->device));
+  RAFI_CK(enqueue_fused(c, G_dev, false));
+  c->last_fused = true;
+  c->host_stale = true;
+  c->round += 1;
+  return RAFI_OK;
+}
+
+int rafi_sync_host(rafi_ctx* ctx) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return RAFI_ERR_INVALID_ARG;
+  RAFI_CK_CUDA(cudaSetDevice(c->device));
+  uint64_t G = 0;
+  RAFI_CK(refresh_host(c, &G));
+  c->last_G = (int64_t)G;
+  return RAFI_OK;
+}
+
+int rafi_capture_begin(rafi_ctx* ctx) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !c->stream) { set_error("capture needs a non-default context stream"); return RAFI_ERR_INVALID_ARG; }
+  RAFI_CK_CUDA(cudaSetDevice(c->device));
+  RAFI_CK_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
+  return RAFI_OK;
+}
+
+int rafi_capture_end(rafi_ctx* ctx, void** exec) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !exec) return RAFI_ERR_INVALID_ARG;
+  cudaGraph_t g = nullptr;
+  RAFI_CK_CUDA(cudaStreamEndCapture(c->stream, &g));
+  cudaGraphExec_t e = nullptr;
+  cudaError_t r = cudaGraphInstantiate(&e, g, 0);
+  cudaGraphDestroy(g);
+  RAFI_CK_CUDA(r);
+  *exec = e;
+  return RAFI_OK;
+}
+
+int rafi_graph_launch(rafi_ctx* ctx, void* exec) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !exec) return RAFI_ERR_INVALID_ARG;
+  RAFI_CK_CUDA(cudaSetDevice(c->device));
+  RAFI_CK_CUDA(cudaGraphLaunch((cudaGraphExec_t)exec, c->stream));
+  c->host_stale = true;
+  return RAFI_OK;
+}
+
+int rafi_graph_destroy(void* exec) {
+  if (exec) RAFI_CK_CUDA(cudaGraphExecDestroy((cudaGraphExec_t)exec));
+  return RAFI_OK;
 }
 
 int rafi_num_ranks(const rafi_ctx* ctx) { const Ctx* c = reinterpret_cast<const Ctx*>(ctx); return c ? c->R : RAFI_ERR_INVALID_ARG; }

@@ -83,6 +83,11 @@ __global__ void k_drv_walk(rafi_device_view v, uint64_t seed, uint32_t rnd, uint
   }
 }
 
+// Threads to launch for an app step over the incoming queue: the host-known
+// count, or the capacity when the count lives only on the device (after
+// rafi_forward_async; the kernels read numIncoming from num_in_dev).
+uint64_t launch_count(const rafi_impl::Ctx* c, const rafi_device_view& v) { return c->host_stale ? c->cap : v.num_in; }
+
 template <int B>
 int launch_emit(rafi_impl::Ctx* c, const rafi_device_view& v, int pattern, uint64_t seed, uint32_t rnd, uint64_t n,
                 uint64_t seq0, int target, uint64_t thr) {
@@ -96,7 +101,7 @@ int launch_emit(rafi_impl::Ctx* c, const rafi_device_view& v, int pattern, uint6
 template <int B>
 int launch_walk(rafi_impl::Ctx* c, const rafi_device_view& v, uint64_t seed, uint32_t rnd, uint32_t last) {
   const int threads = 256;
-  const uint64_t n = v.num_in;
+  const uint64_t n = launch_count(c, v);
   if (!n) return RAFI_OK;
   const uint64_t blocks = (n + threads - 1) / threads;
   const int grid = (int)(blocks < 148 * 16 ? blocks : 148 * 16);
@@ -313,7 +318,7 @@ extern "C" int rafi_drv_random_walk(rafi_ctx* ctx, uint64_t seed, uint32_t rnd, 
       default: rafi_impl::set_error("rafi_drv_random_walk: unsupported item size"); return RAFI_ERR_UNSUPPORTED;
     }
     if (rc != RAFI_OK) return rc;
-    if (v.num_in) c->launches += 1;
+    if (launch_count(c, v)) c->launches += 1;
   }
   return RAFI_OK;
 }
@@ -341,7 +346,7 @@ extern "C" int rafi_drv_advect_step(rafi_ctx* ctx, uint32_t rnd, uint32_t max_ro
   for (int l = 0; l < c->L; ++l) {
     rafi_device_view v;
     if ((rc = rafi_get_device_view(ctx, l, &v)) != RAFI_OK) return rc;
-    if ((rc = launch_grid(c, v.num_in, k_advect_step, v, rnd, max_rounds, omega, eps, h, Grid3{gx, gy, gz})))
+    if ((rc = launch_grid(c, launch_count(c, v), k_advect_step, v, rnd, max_rounds, omega, eps, h, Grid3{gx, gy, gz})))
       return rc;
   }
   return RAFI_OK;
@@ -371,7 +376,7 @@ extern "C" int rafi_drv_march_step(rafi_ctx* ctx, uint32_t rnd, uint64_t seed, u
   for (int l = 0; l < c->L; ++l) {
     rafi_device_view v;
     if ((rc = rafi_get_device_view(ctx, l, &v)) != RAFI_OK) return rc;
-    if ((rc = launch_grid(c, v.num_in, k_march_step, v, seed, p_thr, max_bounces, max_steps, Grid3{gx, gy, gz},
+    if ((rc = launch_grid(c, launch_count(c, v), k_march_step, v, seed, p_thr, max_bounces, max_steps, Grid3{gx, gy, gz},
                           result)))
       return rc;
   }

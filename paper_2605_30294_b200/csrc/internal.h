@@ -98,6 +98,7 @@ struct Ctx {
   int cur = 0;       // which binned buffer this round writes
   int last_cur = 0;  // which one the last forward wrote
   bool last_fused = false;
+  bool host_stale = false;  // rafi_forward_async ran since the last host refresh
   int64_t last_G = 0;
 
   std::vector<LocalRank> lr;
@@ -138,7 +139,7 @@ int launch_emit_bulk(Ctx* c, int local, const uint8_t* items, const int32_t* des
 int launch_hist(Ctx* c);
 int launch_scan(Ctx* c);
 int launch_scatter(Ctx* c, bool fused);
-int launch_plan(Ctx* c, bool fused);
+int launch_plan(Ctx* c, bool fused, unsigned long long* G_out = nullptr);
 int launch_copy(Ctx* c, int nruns_per_dest);
 int launch_wrapup(Ctx* c);
 size_t scatter_smem_bytes(uint32_t tile, uint64_t item_bytes, int R);

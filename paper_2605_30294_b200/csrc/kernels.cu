@@ -151,30 +151,40 @@ __device__ __forceinline__ uint32_t warp_sum(uint32_t x) {
 }
 
 constexpr int kHistTilesPerWarp = 4;
-constexpr int kHistTilesPerCta = kWarps * kHistTilesPerWarp;
+constexpr int kHistTilesPerCta = kWarps * kHistTilesPerWarp;  // 32 tiles = one "block" of the scan
 constexpr int kHistVec = 8;  // 16-byte dest loads in flight per lane
 
-// Per-tile per-destination counts H[l][d][t] (the counting half of the
-// paper's radix sort by destination).  One warp per tile,
-// kHistTilesPerWarp consecutive tiles per warp, 16-byte loads, 8 in flight per
-// lane; no block-level synchronisation.  RMAX > 0: register counters for
-// R <= RMAX, reduced with warp shuffles; RMAX == 0: per-warp shared-memory
+// Per-tile per-destination counts (the counting half of the paper's radix
+// sort by destination), one warp per tile, 16-byte loads with
+// 8 in flight per lane.  CTA (b, l) covers tiles 32b..32b+31 of local rank l
+// and also does the first level of the tile scan: for every destination d it
+// writes O[l][d][t] = items with dest d in tiles 32b..t-1 of the block, and
+// the block aggregate H[l][d][b] (scanned by k_scan).  RMAX > 0: register
+// counters for R <= RMAX reduced with warp shuffles; RMAX == 0: shared
 // counters fed by __match_any_sync aggregation.
 template <int RMAX>
 __global__ void __launch_bounds__(kThreads)
-k_hist(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, int L, int R, uint64_t cap, uint32_t T) {
-  extern __shared__ uint32_t wc[];  // RMAX == 0: [kWarps][R]
+k_hist(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, int R, uint64_t cap, uint32_t T) {
+  extern __shared__ uint32_t tc[];  // [kHistTilesPerCta][R] tile counts
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int l = blockIdx.y;
+  const uint64_t n = n_items(ctrl[l], cap);
+  const uint64_t tiles = (n + T - 1) / T;
+  const uint64_t tb = (uint64_t)blockIdx.x * kHistTilesPerCta;
+  if (tb >= tiles) return;  // uniform over the CTA
+  const uint64_t nblk = (tiles + kHistTilesPerCta - 1) / kHistTilesPerCta;
   for (int k = 0; k < kHistTilesPerWarp; ++k) {
-    const uint64_t g = ((uint64_t)blockIdx.x * kWarps + w) * kHistTilesPerWarp + k;
-    int l;
-    uint64_t t, n, tiles;
-    if (!tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) return;
+    const int ti = w * kHistTilesPerWarp + k;  // tile within the CTA
+    const uint64_t t = tb + ti;
+    uint32_t* mine = tc + ti * R;
+    if (t >= tiles) {
+      for (int d = lane; d < R; d += 32) mine[d] = 0;
+      continue;
+    }
     const uint64_t t0 = t * T;
     const uint32_t nt = (uint32_t)umin64(T, n - t0);
-    const int4* d4 = reinterpret_cast<const int4*>(rk[l].dest + t0);  // t0*4 is a multiple of 1 KiB
-    uint32_t* H = rk[l].H;
     if (RMAX > 0) {
+      const int4* d4 = reinterpret_cast<const int4*>(rk[l].dest + t0);  // t0*4 is a multiple of 1 KiB
       uint32_t c[RMAX > 0 ? RMAX : 1];
 #pragma unroll
       for (int r = 0; r < RMAX; ++r) c[r] = 0;
@@ -201,10 +211,9 @@ k_hist(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, int L, 
 #pragma unroll
       for (int r = 0; r < RMAX; ++r) {
         const uint32_t x = warp_sum(c[r]);
-        if (lane == (r & 31) && r < R) H[(uint64_t)r * tiles + t] = x;
+        if (lane == (r & 31) && r < R) mine[r] = x;
       }
     } else {
-      uint32_t* mine = wc + w * R;
       for (int d = lane; d < R; d += 32) mine[d] = 0;
       __syncwarp();
       const int32_t* dest = rk[l].dest + t0;
@@ -214,47 +223,55 @@ k_hist(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, int L, 
         if (d >= 0 && lane == __ffs(m) - 1) mine[d] += __popc(m);
         __syncwarp();
       }
-      for (int d = lane; d < R; d += 32) H[(uint64_t)d * tiles + t] = mine[d];
-      __syncwarp();
     }
+  }
+  __syncthreads();
+  // first scan level: exclusive prefix over the CTA's tiles, per destination
+  uint32_t* O = rk[l].O;
+  for (int d = threadIdx.x; d < R; d += kThreads) {
+    uint32_t acc = 0;
+    for (int ti = 0; ti < kHistTilesPerCta; ++ti) {
+      const uint64_t t = tb + ti;
+      if (t < tiles) O[(uint64_t)d * tiles + t] = acc;
+      acc += tc[ti * R + d];
+    }
+    rk[l].H[(uint64_t)d * nblk + blockIdx.x] = acc;
   }
 }
 
 // ---------------------------------------------------------------- a3 scan
 
-// One CTA per (destination d, local rank l): O[l][d][t] = sum of H[l][d][0..t)
-// over the rank's live tiles (the paper's segment tally, kept
-// on device), and the row total send_count[d] -> count matrix C[g][d].  The
+// One CTA per (destination d, local rank l): in place, H[l][d][b] := items
+// with dest d in blocks 0..b-1 (second scan level; the tile offset is then
+// O[l][d][t] + H[l][d][t/32]), and the row total send_count[d] -> count matrix
+// C[g][d] (the paper's segment tally, kept on device).  The
 // per-destination base (send offset, or the receiver's recv offset under
 // FUSED) is added by k_plan / k_scatter.
 constexpr int kScanThreads = 1024;
-constexpr int kScanV = 8;
+constexpr int kScanV = 4;
 
 __global__ void __launch_bounds__(kScanThreads)
 k_scan(const RankDev* __restrict__ rk, CtrlDev* __restrict__ ctrl, uint64_t* __restrict__ Cmat,
        int grank0, int R, uint64_t cap, uint32_t T) {
   __shared__ uint32_t wsum[kScanThreads / 32];
   __shared__ uint32_t carry_s;
+  __shared__ uint32_t sh[kScanThreads * kScanV];
   const int d = blockIdx.x, l = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint64_t n = n_items(ctrl[l], cap);
-  const uint64_t M = (n + T - 1) / T;  // live tiles
-  const uint32_t* H = rk[l].H + (uint64_t)d * M;
-  uint32_t* O = rk[l].O + (uint64_t)d * M;
+  const uint64_t tiles = (n + T - 1) / T;
+  const uint64_t M = (tiles + kHistTilesPerCta - 1) / kHistTilesPerCta;  // live blocks
+  uint32_t* H = rk[l].H + (uint64_t)d * M;
   if (tid == 0) carry_s = 0;
   __syncthreads();
   for (uint64_t base = 0; base < M; base += (uint64_t)kScanThreads * kScanV) {
     uint32_t v[kScanV];
     uint32_t s = 0;
 #pragma unroll
-    for (int j = 0; j < kScanV; ++j) {  // element base + j*1024 + tid: coalesced
+    for (int j = 0; j < kScanV; ++j) {  // coalesced load, transposed through shared memory
       const uint64_t i = base + (uint64_t)j * kScanThreads + tid;
-      v[j] = i < M ? H[i] : 0u;
+      sh[j * kScanThreads + tid] = i < M ? H[i] : 0u;
     }
-    // this thread owns elements base + tid*kScanV + j: transpose through shared memory
-    __shared__ uint32_t sh[kScanThreads * kScanV];
-#pragma unroll
-    for (int j = 0; j < kScanV; ++j) sh[j * kScanThreads + tid] = v[j];
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < kScanV; ++j) { v[j] = sh[tid * kScanV + j]; s += v[j]; }
@@ -284,7 +301,7 @@ k_scan(const RankDev* __restrict__ rk, CtrlDev* __restrict__ ctrl, uint64_t* __r
 #pragma unroll
     for (int j = 0; j < kScanV; ++j) {
       const uint64_t i = base + (uint64_t)j * kScanThreads + tid;
-      if (i < M) O[i] = sh[j * kScanThreads + tid];
+      if (i < M) H[i] = sh[j * kScanThreads + tid];
     }
     if (tid == kScanThreads - 1) carry_s = e;
     __syncthreads();
@@ -349,7 +366,7 @@ __host__ __device__ inline ScatterLayout scatter_layout(uint32_t T, uint64_t B, 
   s.off_rstart = o; o += 4 * R;
   s.off_tcnt = o; o = al(o + 4ull * R, 8);
   s.off_dbase = o; o += 8 * R;
-  s.total = o;
+  s.total = al(o, 16);
   return s;
 }
 
@@ -427,7 +444,9 @@ k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint
       const uint8_t* base = dst_table ? dst_table[d] : rk[l].binned[cur];
       dbase[d] = (uintptr_t)base;
       // global base of (d, t), parked in rstart until phase 3
-      rstart[d] = rk[l].O[(uint64_t)d * tiles + t] + (uint32_t)dst_off[(uint64_t)l * R + d];
+      const uint64_t nblk = (tiles + kHistTilesPerCta - 1) / kHistTilesPerCta;
+      rstart[d] = rk[l].O[(uint64_t)d * tiles + t] + rk[l].H[(uint64_t)d * nblk + t / kHistTilesPerCta] +
+                  (uint32_t)dst_off[(uint64_t)l * R + d];
     }
     mbar_wait(&mbar[it & 1], (it >> 1) & 1);
     __syncthreads();
@@ -508,12 +527,16 @@ k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint
 //   FUSED (all rows, after the all-gather): dst_off[l][d] = recv_off_d[g]
 //     = sum_{s<g} C[s][d] (where g's block starts in d's incoming queue),
 //     num_in[l] = sum_s C[s][g], and the collective overflow decision (Z3).
+//   It also writes G = sum of all entries (the distributed-termination count,
+//   PAPER:136) to *G_out (if non-null), or ~0 on overflow -- the device-side
+//   termination value of rafi_forward_async.
 template <bool kFused>
 __global__ void k_plan(const uint64_t* __restrict__ C, int grank0, int R, uint64_t cap, uint64_t* __restrict__ dst_off,
-                       uint64_t* __restrict__ num_in, int* __restrict__ ovf) {
+                       uint64_t* __restrict__ num_in, int* __restrict__ ovf, unsigned long long* __restrict__ G_out) {
   __shared__ int s_ovf;
+  __shared__ unsigned long long s_G;
   const int l = blockIdx.x, g = grank0 + l;
-  if (threadIdx.x == 0) s_ovf = 0;
+  if (threadIdx.x == 0) { s_ovf = 0; s_G = 0; }
   __syncthreads();
   for (int d = threadIdx.x; d < R; d += blockDim.x) {
     if (kFused) {
@@ -526,6 +549,7 @@ __global__ void k_plan(const uint64_t* __restrict__ C, int grank0, int R, uint64
       dst_off[(uint64_t)l * R + d] = recv_off;
       if (col > cap) s_ovf = 1;
       if (d == g) num_in[l] = col;
+      if (G_out && l == 0) atomicAdd(&s_G, (unsigned long long)col);
     } else {
       uint64_t send_off = 0;
       for (int e = 0; e < d; ++e) send_off += C[(uint64_t)g * R + e];
@@ -534,7 +558,10 @@ __global__ void k_plan(const uint64_t* __restrict__ C, int grank0, int R, uint64
   }
   if (kFused) {
     __syncthreads();
-    if (threadIdx.x == 0 && l == 0) *ovf = s_ovf;  // every block computes the same decision
+    if (threadIdx.x == 0 && l == 0) {
+      *ovf = s_ovf;  // every block computes the same decision
+      if (G_out) *G_out = s_ovf ? ~0ull : s_G;
+    }
   }
 }
 
@@ -602,8 +629,9 @@ static uint32_t unit_for(uint64_t B, uintptr_t align_bits) {
 }
 
 uint32_t choose_tile(uint64_t item_bytes) {
-  // two pipeline stages of ~48 KiB (items + dests) so two CTAs fit on an SM
-  uint64_t t = (48u * 1024u) / (item_bytes + 4);
+  // two pipeline stages (items + dests) plus 8 B/item of indices in ~110 KiB,
+  // so two CTAs fit on an SM
+  uint64_t t = (110u * 1024u) / (2 * item_bytes + 16);
   t = (t / kThreads) * kThreads;
   if (t < (uint64_t)kThreads) t = kThreads;
   if (t > (uint64_t)kThreads * kMaxK) t = kThreads * kMaxK;
@@ -645,21 +673,21 @@ static int persistent_grid(Ctx* c, int per_sm) {
 }
 
 int launch_hist(Ctx* c) {
-  const uint64_t tiles_all = std::max<uint64_t>(1, c->max_tiles * (uint64_t)c->L);
-  const int grid = (int)((tiles_all + kHistTilesPerCta - 1) / kHistTilesPerCta);
-#define HIST(RM, SM) \
-  k_hist<RM><<<grid, kThreads, SM, c->stream>>>(rank_table(c), c->ctrl, c->L, c->R, c->cap, c->tile)
-  if (c->R <= 1) HIST(1, 0);
-  else if (c->R <= 2) HIST(2, 0);
-  else if (c->R <= 4) HIST(4, 0);
-  else if (c->R <= 8) HIST(8, 0);
-  else if (c->R <= 16) HIST(16, 0);
-  else if (c->R <= 32) HIST(32, 0);
-  else {
-    const size_t sm = sizeof(uint32_t) * kWarps * c->R;
-    if (sm > 48 * 1024) RAFI_CK_CUDA(cudaFuncSetAttribute(k_hist<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    HIST(0, sm);
-  }
+  const dim3 grid((unsigned)std::max<uint64_t>(1, (c->max_tiles + kHistTilesPerCta - 1) / kHistTilesPerCta), c->L);
+  const size_t sm = sizeof(uint32_t) * kHistTilesPerCta * c->R;
+#define HIST(RM)                                                                                        \
+  do {                                                                                                  \
+    if (sm > 48 * 1024)                                                                                 \
+      RAFI_CK_CUDA(cudaFuncSetAttribute(k_hist<RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    k_hist<RM><<<grid, kThreads, sm, c->stream>>>(rank_table(c), c->ctrl, c->R, c->cap, c->tile);      \
+  } while (0)
+  if (c->R <= 1) HIST(1);
+  else if (c->R <= 2) HIST(2);
+  else if (c->R <= 4) HIST(4);
+  else if (c->R <= 8) HIST(8);
+  else if (c->R <= 16) HIST(16);
+  else if (c->R <= 32) HIST(32);
+  else HIST(0);
 #undef HIST
   RAFI_CK_CUDA(cudaGetLastError());
   c->launches += 1; c->fwd_launches += 1;
@@ -682,14 +710,21 @@ static int launch_scatter_t(Ctx* c, bool fused, uint32_t UPI, int grid) {
   uint8_t* const* table = fused ? c->in_table_dev : nullptr;
   const uint64_t* off = c->off_dev;
   const int* ovf = fused ? c->ovf_dev : nullptr;
+  static int set_true = 0, set_false = 0;  // per instantiation: the largest smem opt-in already granted
   if (si) {
     auto k = k_scatter<U, true>;
-    RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
+    if ((int)lay.total > set_true) {
+      RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
+      set_true = (int)lay.total;
+    }
     k<<<grid, kThreads, lay.total, c->stream>>>(rank_table(c), c->ctrl, table, off, ovf, c->L, c->R, c->cap, c->tile,
                                                c->cur, (uint32_t)c->B, UPI, dv, lay);
   } else {
     auto k = k_scatter<U, false>;
-    RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
+    if ((int)lay.total > set_false) {
+      RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
+      set_false = (int)lay.total;
+    }
     k<<<grid, kThreads, lay.total, c->stream>>>(rank_table(c), c->ctrl, table, off, ovf, c->L, c->R, c->cap, c->tile,
                                                c->cur, (uint32_t)c->B, UPI, dv, lay);
   }
@@ -715,11 +750,13 @@ int launch_scatter(Ctx* c, bool fused) {
   return rc;
 }
 
-int launch_plan(Ctx* c, bool fused) {
+int launch_plan(Ctx* c, bool fused, unsigned long long* G_out) {
   if (fused)
-    k_plan<true><<<c->L, 256, 0, c->stream>>>(c->Cdev, c->proc * c->L, c->R, c->cap, c->off_dev, c->plan_dev, c->ovf_dev);
+    k_plan<true><<<c->L, 256, 0, c->stream>>>(c->Cdev, c->proc * c->L, c->R, c->cap, c->off_dev, c->plan_dev,
+                                              c->ovf_dev, G_out);
   else
-    k_plan<false><<<c->L, 256, 0, c->stream>>>(c->Cdev, c->proc * c->L, c->R, c->cap, c->off_dev, c->plan_dev, c->ovf_dev);
+    k_plan<false><<<c->L, 256, 0, c->stream>>>(c->Cdev, c->proc * c->L, c->R, c->cap, c->off_dev, c->plan_dev,
+                                               c->ovf_dev, nullptr);
   RAFI_CK_CUDA(cudaGetLastError());
   c->launches += 1; c->fwd_launches += 1;
   return RAFI_OK;

@@ -100,6 +100,12 @@ SIGNATURES = {
     "rafi_drv_march_seed": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int]),
     "rafi_drv_march_step": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                                       C.c_int, C.c_int, C.c_int, C.c_void_p]),
+    "rafi_forward_async": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "rafi_sync_host": (C.c_int, [C.c_void_p]),
+    "rafi_capture_begin": (C.c_int, [C.c_void_p]),
+    "rafi_capture_end": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "rafi_graph_launch": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "rafi_graph_destroy": (C.c_int, [C.c_void_p]),
     "rafi_plan": (C.c_int, [C.c_int, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                             C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_int)]),
 }
@@ -262,6 +268,28 @@ class Context:
         if G < 0:
             raise RafiError(int(G), "rafi_forward")
         return int(G)
+
+    def forward_async(self, G_dev):
+        """NEXT-3: enqueue a FUSED forward with no host sync; G lands in G_dev (device u64)."""
+        _check(lib().rafi_forward_async(self._h, _ptr(G_dev)), "rafi_forward_async")
+
+    def sync_host(self):
+        _check(lib().rafi_sync_host(self._h), "rafi_sync_host")
+
+    def capture_begin(self):
+        _check(lib().rafi_capture_begin(self._h), "rafi_capture_begin")
+
+    def capture_end(self) -> int:
+        e = C.c_void_p()
+        _check(lib().rafi_capture_end(self._h, C.byref(e)), "rafi_capture_end")
+        return e.value
+
+    def graph_launch(self, exec_handle: int):
+        _check(lib().rafi_graph_launch(self._h, exec_handle), "rafi_graph_launch")
+
+    @staticmethod
+    def graph_destroy(exec_handle: int):
+        _check(lib().rafi_graph_destroy(exec_handle), "rafi_graph_destroy")
 
     def forward_rc(self) -> int:
         """rafi_forward's raw return (G >= 0 or a negative status)."""
