@@ -191,7 +191,7 @@ static void destroy_ctx(Ctx* c) {
   close_ipc(c);
   for (auto& r : c->lr) free_rank(r);
   cudaFree(c->rank_dev); cudaFree(c->ctrl); cudaFree(c->Cdev); cudaFree(c->runs_dev); cudaFree(c->plan_dev);
-  cudaFree(c->off_dev); cudaFree(c->ovf_dev); cudaFree(c->in_table_dev);
+  cudaFree(c->off_dev); cudaFree(c->ovf_dev); cudaFree(c->in_table_dev); cudaFree(c->done_dev);
   cudaFree(c->stage);
   cudaFreeHost(c->Chost); cudaFreeHost(c->ctrl_host); cudaFreeHost(c->runs_host); cudaFreeHost(c->plan_host);
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);
@@ -241,6 +241,7 @@ static int create(Ctx** out, const rafi_create_params* p) {
   if ((rc = alloc_dev((void**)&c->plan_dev, sizeof(uint64_t) * c->L))) return fail(rc);
   if ((rc = alloc_dev((void**)&c->off_dev, sizeof(uint64_t) * c->L * c->R))) return fail(rc);
   if ((rc = alloc_dev((void**)&c->ovf_dev, 2 * sizeof(int)))) return fail(rc);
+  if ((rc = alloc_dev((void**)&c->done_dev, 2 * sizeof(unsigned)))) return fail(rc);
   if ((rc = alloc_dev((void**)&c->in_table_dev, sizeof(uint8_t*) * c->R))) return fail(rc);
   if (cudaMallocHost((void**)&c->Chost, sizeof(uint64_t) * c->R * c->R) != cudaSuccess ||
       cudaMallocHost((void**)&c->ctrl_host, sizeof(CtrlDev) * c->L) != cudaSuccess ||
@@ -252,6 +253,7 @@ static int create(Ctx** out, const rafi_create_params* p) {
   }
   if (cudaMemsetAsync(c->ctrl, 0, sizeof(CtrlDev) * c->L, c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->ovf_dev, 0, 2 * sizeof(int), c->stream) != cudaSuccess ||
+      cudaMemsetAsync(c->done_dev, 0, 2 * sizeof(unsigned), c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->Cdev, 0, sizeof(uint64_t) * c->R * c->R, c->stream) != cudaSuccess) {
     cudaGetLastError(); set_error("cudaMemsetAsync failed"); return fail(RAFI_ERR_CUDA);
   }
@@ -315,23 +317,25 @@ static int enqueue_fused(Ctx* c, unsigned long long* G_dev, bool T) {
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[0], c->stream));
   RAFI_CK(launch_hist(c));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[1], c->stream));
-  RAFI_CK(launch_scan(c));
+  // a3 (+ a5's plan when this process holds every rank: the scan's last block plans)
+  RAFI_CK(launch_scan(c, c->nprocs == 1 ? 2 : 0, G_dev));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[2], c->stream));
-  // a5: the whole R x R matrix on every rank; offsets + overflow on device
-  if (c->nprocs > 1)
+  if (c->nprocs > 1) {
+    // a5: the whole R x R matrix on every rank; offsets + overflow on device
     RAFI_CK_NCCL(ncclAllGather(c->Cdev + (size_t)c->proc * L * R, c->Cdev, (size_t)L * R, ncclUint64, c->comm,
                                c->stream));
-  RAFI_CK(launch_plan(c, true, G_dev));
+    RAFI_CK(launch_plan(c, true, G_dev));
+  }
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[3], c->stream));
-  // a4 + a6: stable scatter, each destination run written into its receiver's queue
-  RAFI_CK(launch_scatter(c, true));
+  // a4 + a6: stable scatter, each destination run written into its receiver's
+  // queue; a7 wrap-up by its last block (skipped on overflow)
+  RAFI_CK(launch_scatter(c, true, true));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[4], c->stream));
   // every push has landed before any rank's next app kernel reads its queue:
   // the all-reduce completes only after every rank's scatter kernel completed
   if (c->nprocs > 1)
     RAFI_CK_NCCL(ncclAllReduce(c->ovf_dev + 1, c->ovf_dev + 1, 1, ncclInt32, ncclMax, c->comm, c->stream));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[5], c->stream));
-  RAFI_CK(launch_wrapup(c));  // a7 (skipped on device if the overflow flag is set)
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[6], c->stream));
   return RAFI_OK;
 }
@@ -379,10 +383,9 @@ static int64_t forward_staged(Ctx* c) {
   // a2-a4: bin every local rank's outgoing batch by destination
   RAFI_CK(launch_hist(c));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[1], c->stream));
-  RAFI_CK(launch_scan(c));
+  RAFI_CK(launch_scan(c, 1));  // + the send offsets, by the scan's last block
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[2], c->stream));
-  RAFI_CK(launch_plan(c, false));
-  RAFI_CK(launch_scatter(c, false));
+  RAFI_CK(launch_scatter(c, false, false));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[3], c->stream));
   // a5: every process learns the whole R x R count matrix.  The all-gather is
   // ordered after each process's scatter on its stream, so once it completes
@@ -624,7 +627,14 @@ int rafi_emit_bulk(rafi_ctx* ctx, int local, const void* items, const int32_t* d
   RAFI_CK_CUDA(cudaSetDevice(c->device));
   const uint8_t* it = static_cast<const uint8_t*>(items);
   const int32_t* ds = dests;
-  const bool dev_items = is_device_ptr(items), dev_dests = is_device_ptr(dests);
+  // memory type of the two pointers; UVA ranges of host and device memory are
+  // disjoint, so the last answer per pointer can be reused (saves two driver
+  // queries per call on the hot path)
+  auto classify = [&](int k, const void* p) {
+    if (c->cls_ptr[k] != p) { c->cls_ptr[k] = p; c->cls_dev[k] = is_device_ptr(p); }
+    return c->cls_dev[k];
+  };
+  const bool dev_items = classify(0, items), dev_dests = classify(1, dests);
   if (!dev_items || !dev_dests) {
     const size_t ib = (size_t)n * c->B, need = ((ib + 255) & ~(size_t)255) + (size_t)n * 4;
     if (need > c->stage_bytes) {

@@ -112,6 +112,7 @@ struct Ctx {
   uint64_t* plan_dev = nullptr;       // [L] per local dest: num_in (for wrap-up)
   uint64_t* off_dev = nullptr;        // [L][R] per-destination base: send_off (staged) / recv_off (FUSED)
   int* ovf_dev = nullptr;             // [1] FUSED: collective receive-overflow flag
+  unsigned* done_dev = nullptr;       // [2] last-block counters (scan+plan, scatter+wrap-up)
   uint8_t** in_table_dev = nullptr;   // [R] every global rank's incoming queue (local or IPC-mapped)
   std::vector<uint8_t*> peer_in;      // host copy of in_table
   uint64_t* plan_host = nullptr;      // [L] pinned
@@ -121,6 +122,8 @@ struct Ctx {
   std::vector<void*> ipc_opened;      // mappings to close
   bool peer_ok = false;
 
+  const void* cls_ptr[2] = {nullptr, nullptr};  // rafi_emit_bulk pointer-type cache
+  bool cls_dev[2] = {false, false};
   // host staging for rafi_emit_bulk from host memory
   uint8_t* stage = nullptr;
   size_t stage_bytes = 0;
@@ -137,8 +140,8 @@ inline RankDev* rank_table(Ctx* c) { return c->rank_dev; }
 uint32_t choose_tile(uint64_t item_bytes);
 int launch_emit_bulk(Ctx* c, int local, const uint8_t* items, const int32_t* dests, uint64_t n);
 int launch_hist(Ctx* c);
-int launch_scan(Ctx* c);
-int launch_scatter(Ctx* c, bool fused);
+int launch_scan(Ctx* c, int plan_mode, unsigned long long* G_out = nullptr);
+int launch_scatter(Ctx* c, bool fused, bool wrap);
 int launch_plan(Ctx* c, bool fused, unsigned long long* G_out = nullptr);
 int launch_copy(Ctx* c, int nruns_per_dest);
 int launch_wrapup(Ctx* c);

@@ -239,6 +239,73 @@ k_hist(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, int R, 
   }
 }
 
+// ---------------------------------------------------------------- a5 plan (device part)
+
+// Per-destination bases of local rank l (global g) from the count matrix
+// (PAPER:124-126), run by one whole block:
+//   staged (fused = false, row g only): dst_off[d] = send_off_g[d]
+//     = sum_{d'<d} C[g][d'] (where d's block starts in g's send batch);
+//   FUSED (all rows, after the all-gather): dst_off[d] = recv_off_d[g]
+//     = sum_{s<g} C[s][d] (where g's block starts in d's incoming queue),
+//     *num_in = sum_s C[s][g], and the collective overflow decision (Z3) and
+//     G = sum of all entries accumulated into *s_ovf / *s_G
+//     (block-shared).
+__device__ void plan_block(const uint64_t* __restrict__ C, int g, int R, uint64_t cap, bool fused,
+                           uint64_t* __restrict__ dst_off, uint64_t* __restrict__ num_in, int* s_ovf,
+                           unsigned long long* s_G) {
+  for (int d = threadIdx.x; d < R; d += blockDim.x) {
+    if (fused) {
+      uint64_t recv_off = 0, col = 0;
+      for (int s = 0; s < R; ++s) {
+        const uint64_t c = C[(uint64_t)s * R + d];
+        if (s < g) recv_off += c;
+        col += c;
+      }
+      dst_off[d] = recv_off;
+      if (col > cap) *s_ovf = 1;
+      if (d == g) *num_in = col;
+      if (s_G) atomicAdd(s_G, (unsigned long long)col);
+    } else {
+      uint64_t send_off = 0;
+      for (int e = 0; e < d; ++e) send_off += C[(uint64_t)g * R + e];
+      dst_off[d] = send_off;
+    }
+  }
+}
+
+// Plan of every local rank by the calling block; writes *ovf and *G_out (FUSED).
+__device__ void plan_all(const uint64_t* __restrict__ C, int grank0, int L, int R, uint64_t cap, bool fused,
+                         uint64_t* __restrict__ dst_off, uint64_t* __restrict__ num_in, int* __restrict__ ovf,
+                         unsigned long long* __restrict__ G_out) {
+  __shared__ int s_ovf;
+  __shared__ unsigned long long s_G;
+  if (threadIdx.x == 0) { s_ovf = 0; s_G = 0; }
+  __syncthreads();
+  for (int l = 0; l < L; ++l)
+    plan_block(C, grank0 + l, R, cap, fused, dst_off + (uint64_t)l * R, num_in + l, &s_ovf, l == 0 ? &s_G : nullptr);
+  __syncthreads();
+  if (fused && threadIdx.x == 0) {
+    *ovf = s_ovf;
+    if (G_out) *G_out = s_ovf ? ~0ull : s_G;
+  }
+}
+
+// "Last block done" detection for single-launch epilogues: every block
+// publishes its writes and counts itself in *done; the last one returns true
+// (and re-arms the counter for the next launch).
+__device__ __forceinline__ bool last_block(unsigned* done) {
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned total = gridDim.x * gridDim.y * gridDim.z;
+    s_last = atomicAdd(done, 1u) == total - 1;
+    if (s_last) { *done = 0; __threadfence(); }
+  }
+  __syncthreads();
+  return s_last;
+}
+
 // ---------------------------------------------------------------- a3 scan
 
 // One CTA per (destination d, local rank l): in place, H[l][d][b] := items
@@ -252,7 +319,9 @@ constexpr int kScanV = 4;
 
 __global__ void __launch_bounds__(kScanThreads)
 k_scan(const RankDev* __restrict__ rk, CtrlDev* __restrict__ ctrl, uint64_t* __restrict__ Cmat,
-       int grank0, int R, uint64_t cap, uint32_t T) {
+       int grank0, int R, uint64_t cap, uint32_t T, int L, int plan_mode, unsigned* __restrict__ done,
+       uint64_t* __restrict__ dst_off, uint64_t* __restrict__ num_in, int* __restrict__ ovf,
+       unsigned long long* __restrict__ G_out) {
   __shared__ uint32_t wsum[kScanThreads / 32];
   __shared__ uint32_t carry_s;
   __shared__ uint32_t sh[kScanThreads * kScanV];
@@ -315,6 +384,10 @@ k_scan(const RankDev* __restrict__ rk, CtrlDev* __restrict__ ctrl, uint64_t* __r
       c.invalid_last = c.invalid;
     }
   }
+  // plan_mode 1 (staged) / 2 (FUSED, single process): the last block also
+  // computes every local rank's plan, saving a launch
+  if (plan_mode && last_block(done))
+    plan_all(Cmat, grank0, L, R, cap, plan_mode == 2, dst_off, num_in, ovf, G_out);
 }
 
 // ---------------------------------------------------------------- a4 scatter
@@ -391,7 +464,8 @@ template <typename U, bool kStageItems>
 __global__ void __launch_bounds__(kThreads, 2)
 k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint8_t* const* __restrict__ dst_table,
           const uint64_t* __restrict__ dst_off, const int* __restrict__ ovf, int L, int R, uint64_t cap, uint32_t T,
-          int cur, uint32_t B, uint32_t UPI, FastDiv divU, ScatterLayout lay) {
+          int cur, uint32_t B, uint32_t UPI, FastDiv divU, ScatterLayout lay, unsigned* __restrict__ wrap_done,
+          CtrlDev* __restrict__ ctrl_w, const uint64_t* __restrict__ wrap_num_in) {
   if (ovf && *ovf) return;  // collective receive overflow: move nothing (Z3)
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + lay.off_mbar);
@@ -517,52 +591,26 @@ k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint
     }
   }
   if (dst_table) __threadfence_system();  // pushes to peer memory complete before the kernel does
+  // wrap-up epilogue by the last block: every block has finished
+  // reading the emit counters, so they can be reset for the next round
+  if (wrap_done && last_block(wrap_done)) {
+    for (int l2 = threadIdx.x; l2 < L; l2 += blockDim.x) {
+      ctrl_w[l2].ctr = 0;
+      ctrl_w[l2].invalid = 0;
+      ctrl_w[l2].num_in = wrap_num_in[l2];
+    }
+  }
 }
 
 // ---------------------------------------------------------------- a5 plan
 
-// One block per local rank l (global g), from the count matrix:
-//   staged (kFused = false, local rows only): dst_off[l][d] = send_off_g[d]
-//     = sum_{d'<d} C[g][d'] (where d's block starts in g's send batch);
-//   FUSED (all rows, after the all-gather): dst_off[l][d] = recv_off_d[g]
-//     = sum_{s<g} C[s][d] (where g's block starts in d's incoming queue),
-//     num_in[l] = sum_s C[s][g], and the collective overflow decision (Z3).
-//   It also writes G = sum of all entries (the distributed-termination count,
-//   PAPER:136) to *G_out (if non-null), or ~0 on overflow -- the device-side
-//   termination value of rafi_forward_async.
+// Standalone plan (after the count all-gather when several processes share
+// the communicator): one block computes every local rank's bases.
 template <bool kFused>
-__global__ void k_plan(const uint64_t* __restrict__ C, int grank0, int R, uint64_t cap, uint64_t* __restrict__ dst_off,
-                       uint64_t* __restrict__ num_in, int* __restrict__ ovf, unsigned long long* __restrict__ G_out) {
-  __shared__ int s_ovf;
-  __shared__ unsigned long long s_G;
-  const int l = blockIdx.x, g = grank0 + l;
-  if (threadIdx.x == 0) { s_ovf = 0; s_G = 0; }
-  __syncthreads();
-  for (int d = threadIdx.x; d < R; d += blockDim.x) {
-    if (kFused) {
-      uint64_t recv_off = 0, col = 0;
-      for (int s = 0; s < R; ++s) {
-        const uint64_t c = C[(uint64_t)s * R + d];
-        if (s < g) recv_off += c;
-        col += c;
-      }
-      dst_off[(uint64_t)l * R + d] = recv_off;
-      if (col > cap) s_ovf = 1;
-      if (d == g) num_in[l] = col;
-      if (G_out && l == 0) atomicAdd(&s_G, (unsigned long long)col);
-    } else {
-      uint64_t send_off = 0;
-      for (int e = 0; e < d; ++e) send_off += C[(uint64_t)g * R + e];
-      dst_off[(uint64_t)l * R + d] = send_off;
-    }
-  }
-  if (kFused) {
-    __syncthreads();
-    if (threadIdx.x == 0 && l == 0) {
-      *ovf = s_ovf;  // every block computes the same decision
-      if (G_out) *G_out = s_ovf ? ~0ull : s_G;
-    }
-  }
+__global__ void k_plan(const uint64_t* __restrict__ C, int grank0, int L, int R, uint64_t cap,
+                       uint64_t* __restrict__ dst_off, uint64_t* __restrict__ num_in, int* __restrict__ ovf,
+                       unsigned long long* __restrict__ G_out) {
+  plan_all(C, grank0, L, R, cap, kFused, dst_off, num_in, ovf, G_out);
 }
 
 // ---------------------------------------------------------------- a6 copy (PEER)
@@ -694,16 +742,17 @@ int launch_hist(Ctx* c) {
   return RAFI_OK;
 }
 
-int launch_scan(Ctx* c) {
+int launch_scan(Ctx* c, int plan_mode, unsigned long long* G_out) {
   k_scan<<<dim3(c->R, c->L), kScanThreads, 0, c->stream>>>(rank_table(c), c->ctrl, c->Cdev, c->proc * c->L, c->R,
-                                                           c->cap, c->tile);
+                                                           c->cap, c->tile, c->L, plan_mode, c->done_dev, c->off_dev,
+                                                           c->plan_dev, c->ovf_dev, G_out);
   RAFI_CK_CUDA(cudaGetLastError());
   c->launches += 1; c->fwd_launches += 1;
   return RAFI_OK;
 }
 
 template <typename U>
-static int launch_scatter_t(Ctx* c, bool fused, uint32_t UPI, int grid) {
+static int launch_scatter_t(Ctx* c, bool fused, bool wrap, uint32_t UPI, int grid) {
   const FastDiv dv(UPI);
   const bool si = stage_items(c->tile, c->B);
   const ScatterLayout lay = scatter_layout(c->tile, c->B, c->R, si);
@@ -718,7 +767,8 @@ static int launch_scatter_t(Ctx* c, bool fused, uint32_t UPI, int grid) {
       set_true = (int)lay.total;
     }
     k<<<grid, kThreads, lay.total, c->stream>>>(rank_table(c), c->ctrl, table, off, ovf, c->L, c->R, c->cap, c->tile,
-                                               c->cur, (uint32_t)c->B, UPI, dv, lay);
+                                               c->cur, (uint32_t)c->B, UPI, dv, lay, wrap ? c->done_dev + 1 : nullptr,
+                                               c->ctrl, c->plan_dev);
   } else {
     auto k = k_scatter<U, false>;
     if ((int)lay.total > set_false) {
@@ -726,13 +776,14 @@ static int launch_scatter_t(Ctx* c, bool fused, uint32_t UPI, int grid) {
       set_false = (int)lay.total;
     }
     k<<<grid, kThreads, lay.total, c->stream>>>(rank_table(c), c->ctrl, table, off, ovf, c->L, c->R, c->cap, c->tile,
-                                               c->cur, (uint32_t)c->B, UPI, dv, lay);
+                                               c->cur, (uint32_t)c->B, UPI, dv, lay, wrap ? c->done_dev + 1 : nullptr,
+                                               c->ctrl, c->plan_dev);
   }
   RAFI_CK_CUDA(cudaGetLastError());
   return RAFI_OK;
 }
 
-int launch_scatter(Ctx* c, bool fused) {
+int launch_scatter(Ctx* c, bool fused, bool wrap) {
   const uint32_t unit = unit_for(c->B, 0);
   const uint32_t UPI = (uint32_t)(c->B / unit);
   const size_t smem = scatter_smem_bytes(c->tile, c->B, c->R);
@@ -740,11 +791,11 @@ int launch_scatter(Ctx* c, bool fused) {
   const int grid = persistent_grid(c, per_sm);
   int rc;
   switch (unit) {
-    case 16: rc = launch_scatter_t<uint4>(c, fused, UPI, grid); break;
-    case 8: rc = launch_scatter_t<uint2>(c, fused, UPI, grid); break;
-    case 4: rc = launch_scatter_t<uint32_t>(c, fused, UPI, grid); break;
-    case 2: rc = launch_scatter_t<uint16_t>(c, fused, UPI, grid); break;
-    default: rc = launch_scatter_t<uint8_t>(c, fused, UPI, grid); break;
+    case 16: rc = launch_scatter_t<uint4>(c, fused, wrap, UPI, grid); break;
+    case 8: rc = launch_scatter_t<uint2>(c, fused, wrap, UPI, grid); break;
+    case 4: rc = launch_scatter_t<uint32_t>(c, fused, wrap, UPI, grid); break;
+    case 2: rc = launch_scatter_t<uint16_t>(c, fused, wrap, UPI, grid); break;
+    default: rc = launch_scatter_t<uint8_t>(c, fused, wrap, UPI, grid); break;
   }
   if (rc == RAFI_OK) { c->launches += 1; c->fwd_launches += 1; }
   return rc;
@@ -752,11 +803,11 @@ int launch_scatter(Ctx* c, bool fused) {
 
 int launch_plan(Ctx* c, bool fused, unsigned long long* G_out) {
   if (fused)
-    k_plan<true><<<c->L, 256, 0, c->stream>>>(c->Cdev, c->proc * c->L, c->R, c->cap, c->off_dev, c->plan_dev,
-                                              c->ovf_dev, G_out);
+    k_plan<true><<<1, 256, 0, c->stream>>>(c->Cdev, c->proc * c->L, c->L, c->R, c->cap, c->off_dev, c->plan_dev,
+                                           c->ovf_dev, G_out);
   else
-    k_plan<false><<<c->L, 256, 0, c->stream>>>(c->Cdev, c->proc * c->L, c->R, c->cap, c->off_dev, c->plan_dev,
-                                               c->ovf_dev, nullptr);
+    k_plan<false><<<1, 256, 0, c->stream>>>(c->Cdev, c->proc * c->L, c->L, c->R, c->cap, c->off_dev, c->plan_dev,
+                                            c->ovf_dev, nullptr);
   RAFI_CK_CUDA(cudaGetLastError());
   c->launches += 1; c->fwd_launches += 1;
   return RAFI_OK;
