@@ -106,7 +106,7 @@ typedef struct {
 /* ---- options (rafi_set_option / rafi_get_option) --------------------------- */
 #define RAFI_OPT_EXCHANGE 1        /* payload exchange: RAFI_EXCHANGE_* (default AUTO) */
 #define RAFI_OPT_TIMING 2          /* 1 = record per-phase CUDA events (adds one sync); default 0 */
-#define RAFI_OPT_TILE 3            /* binning tile in items (multiple of 256); 0 = auto from item size */
+#define RAFI_OPT_TILE 3            /* binning tile in items (256 * 2^k, k <= 4); 0 = auto from item size */
 #define RAFI_OPT_SELF_DIRECT 4     /* reserved (self run placement); 0 */
 
 #define RAFI_EXCHANGE_AUTO 0       /* FUSED when every rank's queues are addressable, else NCCL */

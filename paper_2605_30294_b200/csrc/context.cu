@@ -816,7 +816,7 @@ int rafi_set_option(rafi_ctx* ctx, int key, long long v) {
     case RAFI_OPT_TIMING: c->timing = v != 0; return RAFI_OK;
     case RAFI_OPT_TILE: {
       // only between rounds with an empty outgoing queue; re-sizes H/O
-      if (v != 0 && (v % 256 != 0 || v > 4096 || v < 256)) return RAFI_ERR_INVALID_ARG;
+      if (v != 0 && (v < 256 || v > 4096 || (v & (v - 1)) != 0)) return RAFI_ERR_INVALID_ARG;  // 256 * 2^k
       const uint32_t t = v ? (uint32_t)v : choose_tile(c->B);
       if ((uint64_t)(c->cap + t - 1) / t > c->max_tiles) {
         // need larger H/O

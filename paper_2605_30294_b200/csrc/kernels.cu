@@ -421,7 +421,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 struct ScatterLayout {
   uint32_t stage_items;   // bytes of one stage's item buffer (0 if items are read from global)
   uint32_t stage_stride;  // bytes per stage (items + dests), 128-aligned
-  uint32_t off_mbar, off_src, off_pd, off_dpos, off_wcnt, off_wbase, off_rstart, off_tcnt, off_dbase, total;
+  uint32_t off_mbar, off_src, off_wcnt, off_wbase, off_rstart, off_tcnt, off_dbase, total;
 };
 
 __host__ __device__ inline ScatterLayout scatter_layout(uint32_t T, uint64_t B, int R, bool stage_items) {
@@ -432,8 +432,6 @@ __host__ __device__ inline ScatterLayout scatter_layout(uint32_t T, uint64_t B, 
   uint32_t o = 2 * s.stage_stride;
   s.off_mbar = o; o += 16;
   s.off_src = o; o = al(o + 2ull * T, 16);
-  s.off_pd = o; o = al(o + 2ull * T, 16);
-  s.off_dpos = o; o += 4 * T;
   s.off_wcnt = o; o += 4 * kWarps * R;
   s.off_wbase = o; o += 4 * kWarps * R;
   s.off_rstart = o; o += 4 * R;
@@ -460,7 +458,7 @@ __host__ __device__ inline ScatterLayout scatter_layout(uint32_t T, uint64_t B, 
 //   Item index = O[l][d][t] (prefix over earlier tiles) + rank within the tile
 //   + dst_off[l][d], the per-destination base from k_plan: send_off_me[d]
 //   (staged) or recv_off_d[me] (FUSED).
-template <typename U, bool kStageItems>
+template <typename U, bool kStageItems, int kK>
 __global__ void __launch_bounds__(kThreads, 2)
 k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint8_t* const* __restrict__ dst_table,
           const uint64_t* __restrict__ dst_off, const int* __restrict__ ovf, int L, int R, uint64_t cap, uint32_t T,
@@ -470,15 +468,13 @@ k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + lay.off_mbar);
   uint16_t* src_of = reinterpret_cast<uint16_t*>(smem + lay.off_src);
-  uint16_t* pd = reinterpret_cast<uint16_t*>(smem + lay.off_pd);
-  uint32_t* dpos = reinterpret_cast<uint32_t*>(smem + lay.off_dpos);
   uint32_t* wcnt = reinterpret_cast<uint32_t*>(smem + lay.off_wcnt);
   uint32_t* wbase = reinterpret_cast<uint32_t*>(smem + lay.off_wbase);
   uint32_t* rstart = reinterpret_cast<uint32_t*>(smem + lay.off_rstart);
   uint32_t* tcnt = reinterpret_cast<uint32_t*>(smem + lay.off_tcnt);
   uintptr_t* dbase = reinterpret_cast<uintptr_t*>(smem + lay.off_dbase);
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const uint32_t K = T / kThreads;
+  constexpr uint32_t K = kK;  // items per thread per tile (T = 256 * kK)
 
   auto issue = [&](uint32_t it) {  // thread 0: start loading iteration it's tile into stage it&1
     const uint64_t g = blockIdx.x + (uint64_t)it * gridDim.x;
@@ -525,11 +521,11 @@ k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint
     mbar_wait(&mbar[it & 1], (it >> 1) & 1);
     __syncthreads();
     // phase 1: stable rank among same-destination items of the warp's chunk
-    int dk[kMaxK];
-    uint32_t rk_[kMaxK];
+    int dk[kK];
+    uint32_t rk_[kK];
 #pragma unroll
-    for (int k = 0; k < kMaxK; ++k) {
-      if (k < (int)K) {
+    for (int k = 0; k < kK; ++k) {
+      {
         const uint32_t il = w * 32 * K + k * 32 + lane;
         const int d = il < nt ? dest_s[il] : R;
         const unsigned m = __match_any_sync(kFull, d);
@@ -557,29 +553,59 @@ k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint
     __syncthreads();
     // phase 3: destination-major order -> (source item, destination, position)
 #pragma unroll
-    for (int k = 0; k < kMaxK; ++k) {
-      if (k < (int)K && dk[k] < R) {
+    for (int k = 0; k < kK; ++k) {
+      if (dk[k] < R) {
         const int d = dk[k];
         const uint32_t r = wbase[w * R + d] + rk_[k];
         const uint32_t p = tcnt[d] + r;
         src_of[p] = (uint16_t)(w * 32 * K + k * 32 + lane);
-        pd[p] = (uint16_t)d;
-        dpos[p] = rstart[d] + r;
       }
     }
+    // per-run destination base, shifted so that position p of run d lands at
+    // base_d + p*B (runs are contiguous in both the tile order and the output)
+    for (int d = tid; d < R; d += kThreads)
+      dbase[d] += (uintptr_t)(((int64_t)rstart[d] - (int64_t)tcnt[d]) * (int64_t)B);
     __syncthreads();
     // phase 4: coalesced write of every destination run
     const U* srcU = kStageItems ? reinterpret_cast<const U*>(st) : reinterpret_cast<const U*>(rk[l].out + t0 * B);
+    // A thread walks its units in increasing order, so the run it is in only
+    // moves forward: one shared-memory read (src_of) per unit besides the data.
     if (UPI <= 64) {
       const uint32_t units = nt * UPI;
-      for (uint32_t x = tid; x < units; x += kThreads) {
-        const uint32_t p = divU.div(x), u = x - p * UPI;
-        U* dst = reinterpret_cast<U*>(dbase[pd[p]]);
-        dst[(uint64_t)dpos[p] * UPI + u] = srcU[(uint32_t)src_of[p] * UPI + u];
+      int d = 0;
+      uint32_t nb = R > 1 ? tcnt[1] : nt;  // first position after run d
+      U* dst = reinterpret_cast<U*>(dbase[0]);
+      constexpr int kU = 4;  // independent units per thread in flight (ILP)
+      for (uint32_t x0 = tid; x0 < units; x0 += kU * kThreads) {
+        uint32_t p[kU], u[kU], s[kU];
+        U v[kU];
+        U* dd[kU];
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+          const uint32_t x = x0 + j * kThreads;
+          p[j] = divU.div(x);
+          u[j] = x - p[j] * UPI;
+          s[j] = x < units ? (uint32_t)src_of[p[j]] : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+          v[j] = srcU[s[j] * UPI + u[j]];
+          if (x0 + j * kThreads < units && p[j] >= nb) {
+            do { ++d; nb = d + 1 < R ? tcnt[d + 1] : nt; } while (p[j] >= nb);
+            dst = reinterpret_cast<U*>(dbase[d]);
+          }
+          dd[j] = dst;
+        }
+#pragma unroll
+        for (int j = 0; j < kU; ++j)
+          if (x0 + j * kThreads < units) dd[j][(uint64_t)p[j] * UPI + u[j]] = v[j];
       }
     } else {
+      int d = 0;
+      uint32_t nb = R > 1 ? tcnt[1] : nt;
       for (uint32_t p = w; p < nt; p += kWarps) {
-        U* dst = reinterpret_cast<U*>(dbase[pd[p]]) + (uint64_t)dpos[p] * UPI;
+        while (p >= nb) { ++d; nb = d + 1 < R ? tcnt[d + 1] : nt; }
+        U* dst = reinterpret_cast<U*>(dbase[d]) + (uint64_t)p * UPI;
         const U* src = srcU + (uint64_t)src_of[p] * UPI;
         for (uint32_t u = lane; u < UPI; u += 32) dst[u] = src[u];
       }
@@ -677,13 +703,12 @@ static uint32_t unit_for(uint64_t B, uintptr_t align_bits) {
 }
 
 uint32_t choose_tile(uint64_t item_bytes) {
-  // two pipeline stages (items + dests) plus 8 B/item of indices in ~110 KiB,
+  // two pipeline stages (items + dests) plus 2 B/item of indices in ~110 KiB,
   // so two CTAs fit on an SM
-  uint64_t t = (110u * 1024u) / (2 * item_bytes + 16);
-  t = (t / kThreads) * kThreads;
-  if (t < (uint64_t)kThreads) t = kThreads;
-  if (t > (uint64_t)kThreads * kMaxK) t = kThreads * kMaxK;
-  return (uint32_t)t;
+  const uint64_t t = (110u * 1024u) / (2 * item_bytes + 10);
+  uint32_t k = 1;  // items per thread: a power of two (the scatter is templated on it)
+  while (k < (uint32_t)kMaxK && (uint64_t)kThreads * k * 2 <= t) k *= 2;
+  return kThreads * k;
 }
 
 static bool stage_items(uint32_t T, uint64_t B) { return 2ull * T * (B + 4) <= 200u * 1024u; }
@@ -751,8 +776,8 @@ int launch_scan(Ctx* c, int plan_mode, unsigned long long* G_out) {
   return RAFI_OK;
 }
 
-template <typename U>
-static int launch_scatter_t(Ctx* c, bool fused, bool wrap, uint32_t UPI, int grid) {
+template <typename U, int kK>
+static int launch_scatter_k(Ctx* c, bool fused, bool wrap, uint32_t UPI, int grid) {
   const FastDiv dv(UPI);
   const bool si = stage_items(c->tile, c->B);
   const ScatterLayout lay = scatter_layout(c->tile, c->B, c->R, si);
@@ -761,7 +786,7 @@ static int launch_scatter_t(Ctx* c, bool fused, bool wrap, uint32_t UPI, int gri
   const int* ovf = fused ? c->ovf_dev : nullptr;
   static int set_true = 0, set_false = 0;  // per instantiation: the largest smem opt-in already granted
   if (si) {
-    auto k = k_scatter<U, true>;
+    auto k = k_scatter<U, true, kK>;
     if ((int)lay.total > set_true) {
       RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
       set_true = (int)lay.total;
@@ -770,7 +795,7 @@ static int launch_scatter_t(Ctx* c, bool fused, bool wrap, uint32_t UPI, int gri
                                                c->cur, (uint32_t)c->B, UPI, dv, lay, wrap ? c->done_dev + 1 : nullptr,
                                                c->ctrl, c->plan_dev);
   } else {
-    auto k = k_scatter<U, false>;
+    auto k = k_scatter<U, false, kK>;
     if ((int)lay.total > set_false) {
       RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
       set_false = (int)lay.total;
@@ -781,6 +806,18 @@ static int launch_scatter_t(Ctx* c, bool fused, bool wrap, uint32_t UPI, int gri
   }
   RAFI_CK_CUDA(cudaGetLastError());
   return RAFI_OK;
+}
+
+template <typename U>
+static int launch_scatter_t(Ctx* c, bool fused, bool wrap, uint32_t UPI, int grid) {
+  switch (c->tile / kThreads) {
+    case 1: return launch_scatter_k<U, 1>(c, fused, wrap, UPI, grid);
+    case 2: return launch_scatter_k<U, 2>(c, fused, wrap, UPI, grid);
+    case 4: return launch_scatter_k<U, 4>(c, fused, wrap, UPI, grid);
+    case 8: return launch_scatter_k<U, 8>(c, fused, wrap, UPI, grid);
+    case 16: return launch_scatter_k<U, 16>(c, fused, wrap, UPI, grid);
+    default: set_error("tile must be 256 * 2^k"); return RAFI_ERR_INVALID_ARG;
+  }
 }
 
 int launch_scatter(Ctx* c, bool fused, bool wrap) {
