@@ -165,6 +165,44 @@ def run_latency(env, args):
     ctx.close()
 
 
+def run_nbody(env, args):
+    """NEXT-2: the three-context N-body exchange pattern at
+    R=8: migrate 40-B particles, broadcast 24-B root nodes, 4-B refinement
+    requests, 24-B subtree responses -- four forwards per step."""
+    R = 8
+    L = R // env.world
+    n = args.items or 1024 * 1024
+    torch = env.torch
+    P = env.ctx(40, 2 * n, L)
+    V = env.ctx(24, 64 * R, L)
+    Q = env.ctx(4, 4 * R, L)
+    stats = torch.zeros((L, 42), dtype=torch.int64, device=env.dev)
+    for l in range(L):
+        P.drv_nbody_seed(n, 0x5EED0005, local=l)
+    P.forward()
+    G = [0, 0, 0, 0]
+
+    def step():
+        P.drv_nbody_migrate(1.0 / 64)
+        G[0] = P.forward()
+        P.drv_nbody_stats(stats)
+        V.drv_nbody_root(stats)
+        G[1] = V.forward()
+        V.drv_nbody_refine(Q, stats, 0.25)
+        G[2] = Q.forward()
+        Q.drv_nbody_respond(V, stats)
+        G[3] = V.forward()
+
+    for _ in range(3):
+        step()
+    K = 10
+    ms, _ = env.timed(lambda: [step() for _ in range(K)])
+    env.emit({"workload": "nbody: 3 contexts (40/24/4-B items), R=8, %d particles/rank, 4 forwards per step" % n,
+              "metric": "ms per N-body exchange step", "ms_per_step": ms / K,
+              "particles_per_s": R * n * K / (ms / 1e3), "G_last_step": list(G), "local_ranks": L})
+    P.close(); V.close(); Q.close()
+
+
 # ----------------------------------------------------------------------------- cfg3 / cfg4
 
 def run_cfg3(env, args):
@@ -285,13 +323,13 @@ def run_sweep(env, args):
 
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("workload", choices=["cfg1", "cfg3", "cfg4", "cfg5", "sweep", "latency"])
+    p.add_argument("workload", choices=["cfg1", "cfg3", "cfg4", "cfg5", "sweep", "latency", "nbody"])
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--items", type=int, default=0)
     args = p.parse_args()
     env = Env(args)
     {"cfg1": run_cfg1, "cfg3": run_cfg3, "cfg4": run_cfg4, "cfg5": run_cfg5, "sweep": run_sweep,
-     "latency": run_latency}[args.workload](
+     "latency": run_latency, "nbody": run_nbody}[args.workload](
         env, args)
     if env.comm:
         env.rafi.nccl_comm_destroy(env.comm)

@@ -78,6 +78,27 @@ int rafi_drv_march_seed(rafi_ctx* ctx, int local, uint64_t n, uint64_t seed, int
 int rafi_drv_march_step(rafi_ctx* ctx, uint32_t rnd, uint64_t seed, uint32_t p_thr, uint32_t max_bounces,
                         uint32_t max_steps, int gx, int gy, int gz, float* result);
 
+/* ---- N-body exchange pattern: three contexts, three item types
+ * P: Particle (40 B) {float pos[3], vel[3], force[3], mass};
+ * V: VirtualParticle (24 B) {float com[3], mass, smax; int sourceRank};
+ * Q: RefinementReq (4 B) {int senderRank}.
+ * Owner of a position: Morton order, 10 bits per axis, R equal code
+ * intervals.  Multipole statistics are exact integer sums of
+ * positions quantised to 2^-20 (order independent): stats[L][42] u64 =
+ * count, sum[3], min[3], max[3], then 8 octants x (count, sum[3]) about the
+ * root centre of mass.  One step, with a forward of the named context after
+ * each call: migrate (P) -> stats -> root (V) -> refine (V -> Q) ->
+ * respond (Q -> V).  Contexts used together must share the stream and R. */
+int rafi_drv_nbody_seed(rafi_ctx* P, int local, uint64_t n, uint64_t seed);
+int rafi_drv_nbody_migrate(rafi_ctx* P, float dt);  /* pos += dt*vel (periodic), emit to the owner */
+int rafi_drv_nbody_stats(rafi_ctx* P, unsigned long long* stats_dev);
+int rafi_drv_nbody_root(rafi_ctx* V, const unsigned long long* stats_dev);  /* root VP to every other rank */
+/* each received root whose smax^2 > theta2 * dist^2 to this rank's centre
+ * of mass gets a RefinementReq back to its source */
+int rafi_drv_nbody_refine(rafi_ctx* V, rafi_ctx* Q, const unsigned long long* stats_dev, float theta2);
+/* each request is answered with this rank's non-empty octant nodes */
+int rafi_drv_nbody_respond(rafi_ctx* Q, rafi_ctx* V, const unsigned long long* stats_dev);
+
 #ifdef __cplusplus
 }
 #endif

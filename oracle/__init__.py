@@ -19,7 +19,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "rafi_oracle.c")
-_SRCS = [_SRC, os.path.join(_HERE, "proxies.c")]
+_SRCS = [_SRC, os.path.join(_HERE, "proxies.c"), os.path.join(_HERE, "nbody.c")]
 _LIB = os.path.join(_HERE, "liborafi.so")
 
 OK = 0
@@ -86,6 +86,14 @@ def lib():
                                        i32, i32, i32]),
             "orc_march_seed": (None, [P, i32, u64, u64, i32, i32, i32]),
             "orc_march_step": (None, [P, i32, u64, C.c_uint32, C.c_uint32, C.c_uint32, i32, i32, i32, vp]),
+            # nbody.c (CPU twin of the multi-context N-body exchange pattern)
+            "orc_morton_owner": (i32, [C.c_float, C.c_float, C.c_float, i32]),
+            "orc_nbody_seed": (None, [P, i32, u64, u64]),
+            "orc_nbody_migrate": (None, [P, i32, C.c_float]),
+            "orc_nbody_stats": (None, [P, i32, vp]),
+            "orc_nbody_root": (None, [P, i32, vp]),
+            "orc_nbody_refine": (None, [P, P, i32, vp, C.c_float]),
+            "orc_nbody_respond": (None, [P, P, i32, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -220,6 +228,47 @@ class World:
     def march_step(self, r, seed, p_thr, max_bounces, max_steps, grid, result: np.ndarray):
         assert result.dtype == np.float32 and result.flags["C_CONTIGUOUS"]
         lib().orc_march_step(self._w, r, seed, p_thr, max_bounces, max_steps, *grid, result.ctypes.data)
+
+
+NB_STATS = 42
+
+
+class NBody:
+    """The three-context N-body exchange pattern on R simulated ranks
+    (oracle/nbody.c): P (40-B particles), V (24-B virtual particles),
+    Q (4-B refinement requests)."""
+
+    def __init__(self, R, cap_p, cap_v, cap_q):
+        self.R = R
+        self.P, self.V, self.Q = World(R, cap_p, 40), World(R, cap_v, 24), World(R, cap_q, 4)
+        self.stats = np.zeros((R, NB_STATS), np.uint64)
+
+    def seed(self, r, n, seed):
+        lib().orc_nbody_seed(self.P._w, r, n, seed)
+
+    def migrate(self, dt):
+        for r in range(self.R):
+            lib().orc_nbody_migrate(self.P._w, r, dt)
+
+    def compute_stats(self):
+        for r in range(self.R):
+            lib().orc_nbody_stats(self.P._w, r, self.stats[r].ctypes.data)
+
+    def root(self):
+        for r in range(self.R):
+            lib().orc_nbody_root(self.V._w, r, self.stats[r].ctypes.data)
+
+    def refine(self, theta2):
+        for r in range(self.R):
+            lib().orc_nbody_refine(self.V._w, self.Q._w, r, self.stats[r].ctypes.data, theta2)
+
+    def respond(self):
+        for r in range(self.R):
+            lib().orc_nbody_respond(self.Q._w, self.V._w, r, self.stats[r].ctypes.data)
+
+
+def morton_owner(x, y, z, R) -> int:
+    return int(lib().orc_morton_owner(x, y, z, R))
 
 
 def grid_owner(x, y, z, grid) -> int:

@@ -49,18 +49,21 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, defines=None, out: str | None = None) -> str:
+    """Build librafi.so (or, with `defines`, a tuning variant at `out`)."""
+    lib_path = out or LIB
+    if not force and not defines and up_to_date():
         return LIB
     inc, libdir = nccl_paths()
-    os.makedirs(BUILD, exist_ok=True)
+    bdir = BUILD if not defines else os.path.join(BUILD, "v_" + os.path.basename(lib_path))
+    os.makedirs(bdir, exist_ok=True)
     common = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-Wall",
-                     "-I", INCLUDE, "-I", inc, "-Xptxas", "-warn-spills"]
+                     "-I", INCLUDE, "-I", inc, "-Xptxas", "-warn-spills"] + ["-D" + d for d in (defines or [])]
     if verbose:
         common += ["-Xptxas", "-v"]
 
     def compile_one(src):
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        obj = os.path.join(bdir, os.path.basename(src) + ".o")
         cmd = [NVCC] + common + PER_FILE.get(os.path.basename(src), []) + ["-c", src, "-o", obj]
         if src.endswith(".cpp"):
             cmd = [NVCC, "-x", "c++", "-std=c++17", "-O2", "-Xcompiler", "-fPIC,-Wall", "-I", INCLUDE, "-I", inc,
@@ -74,15 +77,32 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(compile_one, _sources()))
-    tmp = LIB + ".tmp.%d" % os.getpid()
+    tmp = lib_path + ".tmp.%d" % os.getpid()
     cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs + [
         "-L", libdir, "-l:libnccl.so.2", "-Xlinker", "-rpath," + libdir]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n%s\n%s" % (r.stdout, r.stderr))
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib_path)
+    return lib_path
+
+
+VARIANTS = {  # scatter tuning experiments: name -> defines (build with --variants)
+    "minb3": ["RAFI_SCATTER_MINB=3", "RAFI_SCATTER_SMEM_KB=72u"],
+    "minb4": ["RAFI_SCATTER_MINB=4", "RAFI_SCATTER_SMEM_KB=54u"],
+    "ilp8": ["RAFI_SCATTER_ILP=8"],
+    "minb3_ilp8": ["RAFI_SCATTER_MINB=3", "RAFI_SCATTER_SMEM_KB=72u", "RAFI_SCATTER_ILP=8"],
+}
+
+
+def build_variants():
+    os.makedirs(os.path.join(PKG, "_variants"), exist_ok=True)
+    return [build(force=True, defines=d, out=os.path.join(PKG, "_variants", "librafi_%s.so" % n))
+            for n, d in VARIANTS.items()]
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--variants" in sys.argv:
+        print(build_variants())
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

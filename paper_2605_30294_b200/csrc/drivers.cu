@@ -382,3 +382,287 @@ extern "C" int rafi_drv_march_step(rafi_ctx* ctx, uint32_t rnd, uint64_t seed, u
   }
   return RAFI_OK;
 }
+
+// ------------------------------------------------------------------ N-body exchange (NEXT-2)
+// Three contexts of different item types on one communicator:
+// particle migration, root-multipole broadcast, refinement requests and
+// subtree responses.  Multipole statistics use exact integer sums of
+// positions quantised to 2^-20, so they do not depend on summation order.
+
+namespace {
+
+struct NbParticle {
+  float px, py, pz, vx, vy, vz, fx, fy, fz, mass;
+};
+struct NbVirtual {
+  float cx, cy, cz, mass, smax;
+  int32_t sourceRank;
+};
+struct NbRequest {
+  int32_t senderRank;
+};
+static_assert(sizeof(NbParticle) == 40 && sizeof(NbVirtual) == 24 && sizeof(NbRequest) == 4, "nbody types");
+
+constexpr int kNbStats = 10 + 8 * 4;  // count, sum[3], min[3], max[3]; 8 x (count, sum[3])
+constexpr float kQ = 1048576.0f, kIQ = 9.5367431640625e-07f;  // 2^20, 2^-20
+
+__device__ __forceinline__ uint32_t q20(float x) { return (uint32_t)(x * kQ); }
+
+// owner by Morton order: 10 bits per axis, equal-width code intervals
+__device__ __forceinline__ int morton_owner(float x, float y, float z, int R) {
+  const uint32_t qx = min((uint32_t)(x * 1024.0f), 1023u), qy = min((uint32_t)(y * 1024.0f), 1023u),
+                 qz = min((uint32_t)(z * 1024.0f), 1023u);
+  uint64_t code = 0;
+#pragma unroll
+  for (int b = 0; b < 10; ++b)
+    code |= ((uint64_t)((qx >> b) & 1) << (3 * b)) | ((uint64_t)((qy >> b) & 1) << (3 * b + 1)) |
+            ((uint64_t)((qz >> b) & 1) << (3 * b + 2));
+  return (int)((code * (uint64_t)R) >> 30);
+}
+
+__device__ __forceinline__ float wrap01(float x) {
+  if (x < 0.0f) x = x + 1.0f;
+  if (x >= 1.0f) x = x - 1.0f;
+  return x;
+}
+
+__global__ void k_nb_seed(rafi_device_view v, uint64_t n, uint64_t seed) {
+  rafi::Queue<NbParticle> q(v);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t id = (uint64_t)v.my_rank * n + i;
+    const uint64_t b = seed ^ (id << 3);
+    NbParticle p;
+    p.px = u24(splitmix64(b ^ 0ull));
+    p.py = u24(splitmix64(b ^ 1ull));
+    p.pz = u24(splitmix64(b ^ 2ull));
+    p.vx = (u24(splitmix64(b ^ 3ull)) - 0.5f) * 0.25f;
+    p.vy = (u24(splitmix64(b ^ 4ull)) - 0.5f) * 0.25f;
+    p.vz = (u24(splitmix64(b ^ 5ull)) - 0.5f) * 0.25f;
+    p.fx = p.fy = p.fz = 0.0f;
+    p.mass = 1.0f;
+    q.emitOutgoing(p, morton_owner(p.px, p.py, p.pz, v.num_ranks));
+  }
+}
+
+__global__ void k_nb_migrate(rafi_device_view v, float dt) {
+  rafi::Queue<NbParticle> q(v);
+  const unsigned long long n = q.numIncoming();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    NbParticle p = q.getIncoming(i);
+    p.px = wrap01(p.px + dt * p.vx);
+    p.py = wrap01(p.py + dt * p.vy);
+    p.pz = wrap01(p.pz + dt * p.vz);
+    q.emitOutgoing(p, morton_owner(p.px, p.py, p.pz, v.num_ranks));
+  }
+}
+
+__global__ void k_nb_stats_init(unsigned long long* st) {
+  const int i = threadIdx.x;
+  if (i < kNbStats) st[blockIdx.x * kNbStats + i] = (i >= 4 && i < 7) ? 0xFFFFFFFFull : 0ull;
+}
+
+// Statistics are reduced per thread in registers, then per block in shared
+// memory, then one global atomic per value and block (integer sums: exact in
+// any order).
+__global__ void k_nb_stats_root(rafi_device_view v, unsigned long long* st) {
+  __shared__ unsigned long long s[10];
+  rafi::Queue<NbParticle> q(v);
+  const unsigned long long n = q.numIncoming();
+  if (threadIdx.x < 10) s[threadIdx.x] = (threadIdx.x >= 4 && threadIdx.x < 7) ? 0xFFFFFFFFull : 0ull;
+  __syncthreads();
+  unsigned long long c = 0, sx = 0, sy = 0, sz = 0;
+  uint32_t mnx = 0xFFFFFFFFu, mny = 0xFFFFFFFFu, mnz = 0xFFFFFFFFu, mxx = 0, mxy = 0, mxz = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const NbParticle p = q.getIncoming(i);
+    const uint32_t x = q20(p.px), y = q20(p.py), z = q20(p.pz);
+    c += 1; sx += x; sy += y; sz += z;
+    mnx = min(mnx, x); mny = min(mny, y); mnz = min(mnz, z);
+    mxx = max(mxx, x); mxy = max(mxy, y); mxz = max(mxz, z);
+  }
+  if (c) {
+    atomicAdd(&s[0], c); atomicAdd(&s[1], sx); atomicAdd(&s[2], sy); atomicAdd(&s[3], sz);
+    atomicMin(&s[4], (unsigned long long)mnx); atomicMin(&s[5], (unsigned long long)mny);
+    atomicMin(&s[6], (unsigned long long)mnz); atomicMax(&s[7], (unsigned long long)mxx);
+    atomicMax(&s[8], (unsigned long long)mxy); atomicMax(&s[9], (unsigned long long)mxz);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && s[0]) {
+    atomicAdd(&st[0], s[0]); atomicAdd(&st[1], s[1]); atomicAdd(&st[2], s[2]); atomicAdd(&st[3], s[3]);
+    atomicMin(&st[4], s[4]); atomicMin(&st[5], s[5]); atomicMin(&st[6], s[6]);
+    atomicMax(&st[7], s[7]); atomicMax(&st[8], s[8]); atomicMax(&st[9], s[9]);
+  }
+}
+
+__global__ void k_nb_stats_oct(rafi_device_view v, unsigned long long* st) {
+  __shared__ unsigned long long s[32];
+  rafi::Queue<NbParticle> q(v);
+  const unsigned long long n = q.numIncoming();
+  if (st[0] == 0) return;
+  if (threadIdx.x < 32) s[threadIdx.x] = 0;
+  __syncthreads();
+  const uint64_t cx = st[1] / st[0], cy = st[2] / st[0], cz = st[3] / st[0];
+  unsigned long long a[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) a[j] = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const NbParticle p = q.getIncoming(i);
+    const uint32_t x = q20(p.px), y = q20(p.py), z = q20(p.pz);
+    const int o = (x >= cx) | ((y >= cy) << 1) | ((z >= cz) << 2);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)  // register-resident per-octant sums (no dynamic indexing)
+      if (j == o) { a[4 * j] += 1; a[4 * j + 1] += x; a[4 * j + 2] += y; a[4 * j + 3] += z; }
+  }
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (a[j]) atomicAdd(&s[j], a[j]);
+  __syncthreads();
+  if (threadIdx.x < 32 && s[threadIdx.x]) atomicAdd(&st[10 + threadIdx.x], s[threadIdx.x]);
+}
+
+__device__ __forceinline__ NbVirtual nb_node(const unsigned long long* s, float smax, int me) {
+  NbVirtual n;
+  n.cx = (float)(s[1] / s[0]) * kIQ;
+  n.cy = (float)(s[2] / s[0]) * kIQ;
+  n.cz = (float)(s[3] / s[0]) * kIQ;
+  n.mass = (float)s[0];
+  n.smax = smax;
+  n.sourceRank = me;
+  return n;
+}
+
+__device__ __forceinline__ float nb_root_smax(const unsigned long long* st) {
+  const uint64_t ex = st[7] - st[4], ey = st[8] - st[5], ez = st[9] - st[6];
+  const uint64_t e = ex > ey ? (ex > ez ? ex : ez) : (ey > ez ? ey : ez);
+  return (float)e * kIQ;
+}
+
+// root broadcast: one VirtualParticle to every other rank
+__global__ void k_nb_root(rafi_device_view v, const unsigned long long* st) {
+  rafi::Queue<NbVirtual> q(v);
+  if (st[0] == 0) return;
+  const NbVirtual root = nb_node(st, nb_root_smax(st), v.my_rank);
+  for (int d = threadIdx.x; d < v.num_ranks; d += blockDim.x)
+    if (d != v.my_rank) q.emitOutgoing(root, d);
+}
+
+// MAC test on each received root; request refinement from its source
+__global__ void k_nb_refine(rafi_device_view vv, rafi_device_view vq, const unsigned long long* st, float theta2) {
+  rafi::Queue<NbVirtual> in(vv);
+  rafi::Queue<NbRequest> out(vq);
+  const unsigned long long n = in.numIncoming();
+  if (st[0] == 0) return;
+  const float mx = (float)(st[1] / st[0]) * kIQ, my = (float)(st[2] / st[0]) * kIQ,
+              mz = (float)(st[3] / st[0]) * kIQ;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const NbVirtual r = in.getIncoming(i);
+    const float dx = r.cx - mx, dy = r.cy - my, dz = r.cz - mz;
+    const float d2 = dx * dx + dy * dy + dz * dz;
+    if (r.smax * r.smax > theta2 * d2) out.emitOutgoing(NbRequest{vq.my_rank}, r.sourceRank);
+  }
+}
+
+// respond to each request with the (non-empty) octant children
+__global__ void k_nb_respond(rafi_device_view vq, rafi_device_view vv, const unsigned long long* st) {
+  rafi::Queue<NbRequest> in(vq);
+  rafi::Queue<NbVirtual> out(vv);
+  const unsigned long long n = in.numIncoming();
+  if (st[0] == 0) return;
+  const float half = nb_root_smax(st) * 0.5f;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n * 8; i += (uint64_t)gridDim.x * blockDim.x) {
+    const NbRequest r = in.getIncoming(i / 8);
+    const unsigned long long* s = st + 10 + 4 * (i % 8);
+    if (s[0]) out.emitOutgoing(nb_node(s, half, vv.my_rank), r.senderRank);
+  }
+}
+
+int nb_check(rafi_impl::Ctx* c, uint64_t B) {
+  if (!c) return RAFI_ERR_INVALID_ARG;
+  if (c->B != B) { rafi_impl::set_error("nbody driver: wrong item size for this context"); return RAFI_ERR_INVALID_ARG; }
+  return cudaSetDevice(c->device) == cudaSuccess ? RAFI_OK : RAFI_ERR_CUDA;
+}
+
+}  // namespace
+
+extern "C" int rafi_drv_nbody_seed(rafi_ctx* ctx, int local, uint64_t n, uint64_t seed) {
+  auto* c = reinterpret_cast<rafi_impl::Ctx*>(ctx);
+  int rc = nb_check(c, sizeof(NbParticle));
+  if (rc) return rc;
+  rafi_device_view v;
+  if ((rc = rafi_get_device_view(ctx, local, &v))) return rc;
+  return launch_grid(c, n, k_nb_seed, v, n, seed);
+}
+
+extern "C" int rafi_drv_nbody_migrate(rafi_ctx* ctx, float dt) {
+  auto* c = reinterpret_cast<rafi_impl::Ctx*>(ctx);
+  int rc = nb_check(c, sizeof(NbParticle));
+  if (rc) return rc;
+  for (int l = 0; l < c->L; ++l) {
+    rafi_device_view v;
+    if ((rc = rafi_get_device_view(ctx, l, &v))) return rc;
+    if ((rc = launch_grid(c, launch_count(c, v), k_nb_migrate, v, dt))) return rc;
+  }
+  return RAFI_OK;
+}
+
+extern "C" int rafi_drv_nbody_stats(rafi_ctx* ctx, unsigned long long* stats) {
+  auto* c = reinterpret_cast<rafi_impl::Ctx*>(ctx);
+  int rc = nb_check(c, sizeof(NbParticle));
+  if (rc) return rc;
+  if (!stats) return RAFI_ERR_INVALID_ARG;
+  k_nb_stats_init<<<c->L, 64, 0, c->stream>>>(stats);
+  c->launches += 1;
+  for (int l = 0; l < c->L; ++l) {
+    rafi_device_view v;
+    if ((rc = rafi_get_device_view(ctx, l, &v))) return rc;
+    if ((rc = launch_grid(c, launch_count(c, v), k_nb_stats_root, v, stats + (uint64_t)l * kNbStats))) return rc;
+  }
+  for (int l = 0; l < c->L; ++l) {
+    rafi_device_view v;
+    if ((rc = rafi_get_device_view(ctx, l, &v))) return rc;
+    if ((rc = launch_grid(c, launch_count(c, v), k_nb_stats_oct, v, stats + (uint64_t)l * kNbStats))) return rc;
+  }
+  return cudaGetLastError() == cudaSuccess ? RAFI_OK : RAFI_ERR_CUDA;
+}
+
+extern "C" int rafi_drv_nbody_root(rafi_ctx* vctx, const unsigned long long* stats) {
+  auto* c = reinterpret_cast<rafi_impl::Ctx*>(vctx);
+  int rc = nb_check(c, sizeof(NbVirtual));
+  if (rc) return rc;
+  for (int l = 0; l < c->L; ++l) {
+    rafi_device_view v;
+    if ((rc = rafi_get_device_view(vctx, l, &v))) return rc;
+    k_nb_root<<<1, 256, 0, c->stream>>>(v, stats + (uint64_t)l * kNbStats);
+    c->launches += 1;
+  }
+  return cudaGetLastError() == cudaSuccess ? RAFI_OK : RAFI_ERR_CUDA;
+}
+
+extern "C" int rafi_drv_nbody_refine(rafi_ctx* vctx, rafi_ctx* qctx, const unsigned long long* stats, float theta2) {
+  auto* cv = reinterpret_cast<rafi_impl::Ctx*>(vctx);
+  auto* cq = reinterpret_cast<rafi_impl::Ctx*>(qctx);
+  int rc = nb_check(cv, sizeof(NbVirtual));
+  if (rc || (rc = nb_check(cq, sizeof(NbRequest)))) return rc;
+  if (cv->L != cq->L || cv->R != cq->R || cv->stream != cq->stream) return RAFI_ERR_INVALID_ARG;
+  for (int l = 0; l < cv->L; ++l) {
+    rafi_device_view a, b;
+    if ((rc = rafi_get_device_view(vctx, l, &a)) || (rc = rafi_get_device_view(qctx, l, &b))) return rc;
+    if ((rc = launch_grid(cv, launch_count(cv, a), k_nb_refine, a, b, stats + (uint64_t)l * kNbStats, theta2)))
+      return rc;
+  }
+  return RAFI_OK;
+}
+
+extern "C" int rafi_drv_nbody_respond(rafi_ctx* qctx, rafi_ctx* vctx, const unsigned long long* stats) {
+  auto* cq = reinterpret_cast<rafi_impl::Ctx*>(qctx);
+  auto* cv = reinterpret_cast<rafi_impl::Ctx*>(vctx);
+  int rc = nb_check(cq, sizeof(NbRequest));
+  if (rc || (rc = nb_check(cv, sizeof(NbVirtual)))) return rc;
+  if (cv->L != cq->L || cv->R != cq->R || cv->stream != cq->stream) return RAFI_ERR_INVALID_ARG;
+  for (int l = 0; l < cq->L; ++l) {
+    rafi_device_view a, b;
+    if ((rc = rafi_get_device_view(qctx, l, &a)) || (rc = rafi_get_device_view(vctx, l, &b))) return rc;
+    if ((rc = launch_grid(cq, 8 * launch_count(cq, a), k_nb_respond, a, b, stats + (uint64_t)l * kNbStats)))
+      return rc;
+  }
+  return RAFI_OK;
+}

@@ -26,6 +26,18 @@
 
 namespace rafi_impl {
 
+// Scatter tuning (build-time; see paper_2605_30294_b200/build.py variants):
+// resident CTAs per SM, shared-memory budget per CTA (KiB), units in flight.
+#ifndef RAFI_SCATTER_MINB
+#define RAFI_SCATTER_MINB 2
+#endif
+#ifndef RAFI_SCATTER_SMEM_KB
+#define RAFI_SCATTER_SMEM_KB 110u
+#endif
+#ifndef RAFI_SCATTER_ILP
+#define RAFI_SCATTER_ILP 4
+#endif
+
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxK = 16;          // items per thread per tile (tile <= 4096)
@@ -459,7 +471,7 @@ __host__ __device__ inline ScatterLayout scatter_layout(uint32_t T, uint64_t B, 
 //   + dst_off[l][d], the per-destination base from k_plan: send_off_me[d]
 //   (staged) or recv_off_d[me] (FUSED).
 template <typename U, bool kStageItems, int kK>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, RAFI_SCATTER_MINB)
 k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint8_t* const* __restrict__ dst_table,
           const uint64_t* __restrict__ dst_off, const int* __restrict__ ovf, int L, int R, uint64_t cap, uint32_t T,
           int cur, uint32_t B, uint32_t UPI, FastDiv divU, ScatterLayout lay, unsigned* __restrict__ wrap_done,
@@ -575,7 +587,7 @@ k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint
       int d = 0;
       uint32_t nb = R > 1 ? tcnt[1] : nt;  // first position after run d
       U* dst = reinterpret_cast<U*>(dbase[0]);
-      constexpr int kU = 4;  // independent units per thread in flight (ILP)
+      constexpr int kU = RAFI_SCATTER_ILP;  // independent units per thread in flight (ILP)
       for (uint32_t x0 = tid; x0 < units; x0 += kU * kThreads) {
         uint32_t p[kU], u[kU], s[kU];
         U v[kU];
@@ -705,7 +717,7 @@ static uint32_t unit_for(uint64_t B, uintptr_t align_bits) {
 uint32_t choose_tile(uint64_t item_bytes) {
   // two pipeline stages (items + dests) plus 2 B/item of indices in ~110 KiB,
   // so two CTAs fit on an SM
-  const uint64_t t = (110u * 1024u) / (2 * item_bytes + 10);
+  const uint64_t t = (RAFI_SCATTER_SMEM_KB * 1024u) / (2 * item_bytes + 10);
   uint32_t k = 1;  // items per thread: a power of two (the scatter is templated on it)
   while (k < (uint32_t)kMaxK && (uint64_t)kThreads * k * 2 <= t) k *= 2;
   return kThreads * k;
@@ -824,7 +836,7 @@ int launch_scatter(Ctx* c, bool fused, bool wrap) {
   const uint32_t unit = unit_for(c->B, 0);
   const uint32_t UPI = (uint32_t)(c->B / unit);
   const size_t smem = scatter_smem_bytes(c->tile, c->B, c->R);
-  const int per_sm = smem <= 110 * 1024 ? 2 : 1;
+  const int per_sm = smem <= (size_t)RAFI_SCATTER_SMEM_KB * 1024 ? RAFI_SCATTER_MINB : 1;
   const int grid = persistent_grid(c, per_sm);
   int rc;
   switch (unit) {

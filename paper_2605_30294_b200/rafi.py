@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librafi.so")
+# RAFI_LIB_PATH selects a tuning variant built by `build.py --variants` (benchmarks only)
+LIB_PATH = os.environ.get("RAFI_LIB_PATH") or os.path.join(_HERE, "librafi.so")
 
 OK = 0
 ERR_INVALID_ARG = -1
@@ -100,6 +101,12 @@ SIGNATURES = {
     "rafi_drv_march_seed": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int]),
     "rafi_drv_march_step": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
                                       C.c_int, C.c_int, C.c_int, C.c_void_p]),
+    "rafi_drv_nbody_seed": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, C.c_uint64]),
+    "rafi_drv_nbody_migrate": (C.c_int, [C.c_void_p, C.c_float]),
+    "rafi_drv_nbody_stats": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "rafi_drv_nbody_root": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "rafi_drv_nbody_refine": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_float]),
+    "rafi_drv_nbody_respond": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "rafi_forward_async": (C.c_int, [C.c_void_p, C.c_void_p]),
     "rafi_sync_host": (C.c_int, [C.c_void_p]),
     "rafi_capture_begin": (C.c_int, [C.c_void_p]),
@@ -268,6 +275,25 @@ class Context:
         if G < 0:
             raise RafiError(int(G), "rafi_forward")
         return int(G)
+
+    # N-body exchange pattern (three contexts; include/rafi_drivers.h)
+    def drv_nbody_seed(self, n: int, seed: int, local: int = 0):
+        _check(lib().rafi_drv_nbody_seed(self._h, local, n, seed), "rafi_drv_nbody_seed")
+
+    def drv_nbody_migrate(self, dt: float):
+        _check(lib().rafi_drv_nbody_migrate(self._h, dt), "rafi_drv_nbody_migrate")
+
+    def drv_nbody_stats(self, stats_dev):
+        _check(lib().rafi_drv_nbody_stats(self._h, _ptr(stats_dev)), "rafi_drv_nbody_stats")
+
+    def drv_nbody_root(self, stats_dev):
+        _check(lib().rafi_drv_nbody_root(self._h, _ptr(stats_dev)), "rafi_drv_nbody_root")
+
+    def drv_nbody_refine(self, qctx: "Context", stats_dev, theta2: float):
+        _check(lib().rafi_drv_nbody_refine(self._h, qctx._h, _ptr(stats_dev), theta2), "rafi_drv_nbody_refine")
+
+    def drv_nbody_respond(self, vctx: "Context", stats_dev):
+        _check(lib().rafi_drv_nbody_respond(self._h, vctx._h, _ptr(stats_dev)), "rafi_drv_nbody_respond")
 
     def forward_async(self, G_dev):
         """NEXT-3: enqueue a FUSED forward with no host sync; G lands in G_dev (device u64)."""
