@@ -101,11 +101,18 @@ typedef struct {
   float ms_reserved;
   uint64_t kernel_launches;   /* cumulative kernels this context has launched */
   uint64_t forward_launches;  /* kernels launched by the last forward */
+  /* sums of the phase times over the forwards (and bulk emits) timed since
+     RAFI_OPT_TIMING was last set; acc_forwards / acc_emits count them */
+  double acc_ms_emit, acc_ms_hist, acc_ms_scan, acc_ms_scatter, acc_ms_count_exchange, acc_ms_payload_exchange,
+      acc_ms_wrapup, acc_ms_total;
+  uint64_t acc_forwards, acc_emits;
 } rafi_stats;
 
 /* ---- options (rafi_set_option / rafi_get_option) --------------------------- */
 #define RAFI_OPT_EXCHANGE 1        /* payload exchange: RAFI_EXCHANGE_* (default AUTO) */
-#define RAFI_OPT_TIMING 2          /* 1 = record per-phase CUDA events (adds one sync); default 0 */
+#define RAFI_OPT_TIMING 2          /* 1 = record per-phase CUDA events (forward: adds one event sync;
+                                      bulk emit: events around the kernel); setting it resets the
+                                      accumulated sums in rafi_stats; default 0 */
 #define RAFI_OPT_TILE 3            /* binning tile in items (256 * 2^k, k <= 4); 0 = auto from item size */
 #define RAFI_OPT_SELF_DIRECT 4     /* reserved (self run placement); 0 */
 

@@ -88,10 +88,8 @@ def build(force: bool = False, verbose: bool = False, defines=None, out: str | N
 
 
 VARIANTS = {  # scatter tuning experiments: name -> defines (build with --variants)
-    "minb3": ["RAFI_SCATTER_MINB=3", "RAFI_SCATTER_SMEM_KB=72u"],
-    "minb4": ["RAFI_SCATTER_MINB=4", "RAFI_SCATTER_SMEM_KB=54u"],
+    "ilp2": ["RAFI_SCATTER_ILP=2"],
     "ilp8": ["RAFI_SCATTER_ILP=8"],
-    "minb3_ilp8": ["RAFI_SCATTER_MINB=3", "RAFI_SCATTER_SMEM_KB=72u", "RAFI_SCATTER_ILP=8"],
 }
 
 

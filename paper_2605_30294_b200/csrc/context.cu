@@ -190,11 +190,13 @@ static void destroy_ctx(Ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   close_ipc(c);
   for (auto& r : c->lr) free_rank(r);
-  cudaFree(c->rank_dev); cudaFree(c->ctrl); cudaFree(c->Cdev); cudaFree(c->runs_dev); cudaFree(c->plan_dev);
+  cudaFree(c->rank_dev); cudaFree(c->ctrl); cudaFree(c->runs_dev); cudaFree(c->plan_dev);
   cudaFree(c->off_dev); cudaFree(c->ovf_dev); cudaFree(c->in_table_dev); cudaFree(c->done_dev);
   cudaFree(c->stage);
-  cudaFreeHost(c->Chost); cudaFreeHost(c->ctrl_host); cudaFreeHost(c->runs_host); cudaFreeHost(c->plan_host);
+  cudaFreeHost(c->ctrl_host); cudaFreeHost(c->runs_host); cudaFreeHost(c->plan_host);
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);
+  for (auto& pr : c->ev_emit)
+    for (auto& e : pr) if (e) cudaEventDestroy(e);
   cudaGetLastError();
   delete c;
 }
@@ -235,30 +237,33 @@ static int create(Ctx** out, const rafi_create_params* p) {
   c->cap = p->capacity;
   c->tile = choose_tile(c->B);
   if ((rc = alloc_dev((void**)&c->rank_dev, sizeof(RankDev) * c->L))) return fail(rc);
-  if ((rc = alloc_dev((void**)&c->ctrl, sizeof(CtrlDev) * c->L))) return fail(rc);
-  if ((rc = alloc_dev((void**)&c->Cdev, sizeof(uint64_t) * c->R * c->R))) return fail(rc);
+  if ((rc = alloc_dev((void**)&c->ctrl, ctrl_c_bytes(c)))) return fail(rc);
+  c->Cdev = reinterpret_cast<uint64_t*>(c->ctrl + c->L);  // count matrix right after the control blocks
   if ((rc = alloc_dev((void**)&c->runs_dev, sizeof(CopyRun) * c->L * c->R))) return fail(rc);
   if ((rc = alloc_dev((void**)&c->plan_dev, sizeof(uint64_t) * c->L))) return fail(rc);
   if ((rc = alloc_dev((void**)&c->off_dev, sizeof(uint64_t) * c->L * c->R))) return fail(rc);
   if ((rc = alloc_dev((void**)&c->ovf_dev, 2 * sizeof(int)))) return fail(rc);
   if ((rc = alloc_dev((void**)&c->done_dev, 2 * sizeof(unsigned)))) return fail(rc);
   if ((rc = alloc_dev((void**)&c->in_table_dev, sizeof(uint8_t*) * c->R))) return fail(rc);
-  if (cudaMallocHost((void**)&c->Chost, sizeof(uint64_t) * c->R * c->R) != cudaSuccess ||
-      cudaMallocHost((void**)&c->ctrl_host, sizeof(CtrlDev) * c->L) != cudaSuccess ||
+  if (cudaMallocHost((void**)&c->ctrl_host, ctrl_c_bytes(c)) != cudaSuccess ||
       cudaMallocHost((void**)&c->runs_host, sizeof(CopyRun) * c->L * c->R) != cudaSuccess ||
       cudaMallocHost((void**)&c->plan_host, sizeof(uint64_t) * c->L) != cudaSuccess) {
     cudaGetLastError();
     set_error("cudaMallocHost failed");
     return fail(RAFI_ERR_NOMEM);
   }
-  if (cudaMemsetAsync(c->ctrl, 0, sizeof(CtrlDev) * c->L, c->stream) != cudaSuccess ||
+  c->Chost = reinterpret_cast<uint64_t*>(c->ctrl_host + c->L);
+  if (cudaMemsetAsync(c->ctrl, 0, ctrl_c_bytes(c), c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->ovf_dev, 0, 2 * sizeof(int), c->stream) != cudaSuccess ||
       cudaMemsetAsync(c->done_dev, 0, 2 * sizeof(unsigned), c->stream) != cudaSuccess ||
-      cudaMemsetAsync(c->Cdev, 0, sizeof(uint64_t) * c->R * c->R, c->stream) != cudaSuccess) {
+      false) {
     cudaGetLastError(); set_error("cudaMemsetAsync failed"); return fail(RAFI_ERR_CUDA);
   }
   for (auto& e : c->ev)
     if (cudaEventCreate(&e) != cudaSuccess) { cudaGetLastError(); set_error("cudaEventCreate"); return fail(RAFI_ERR_CUDA); }
+  for (auto& pr : c->ev_emit)
+    for (auto& e : pr)
+      if (cudaEventCreate(&e) != cudaSuccess) { cudaGetLastError(); set_error("cudaEventCreate"); return fail(RAFI_ERR_CUDA); }
   if ((rc = alloc_all(c))) return fail(rc);
   if ((rc = exchange_peer_pointers(c))) return fail(rc);
   if ((rc = resolve_exchange(c))) return fail(rc);
@@ -342,8 +347,8 @@ static int enqueue_fused(Ctx* c, unsigned long long* G_dev, bool T) {
 
 // Host refresh after device work: count matrix + counters -> host bookkeeping.
 static int refresh_host(Ctx* c, uint64_t* G) {
-  RAFI_CK_CUDA(cudaMemcpyAsync(c->Chost, c->Cdev, sizeof(uint64_t) * c->R * c->R, cudaMemcpyDeviceToHost, c->stream));
-  RAFI_CK_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl, sizeof(CtrlDev) * c->L, cudaMemcpyDeviceToHost, c->stream));
+  // control blocks and count matrix are one allocation: one copy back
+  RAFI_CK_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl, ctrl_c_bytes(c), cudaMemcpyDeviceToHost, c->stream));
   RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
   c->host_stale = false;
   if (book_keep(c, G)) {
@@ -354,20 +359,57 @@ static int refresh_host(Ctx* c, uint64_t* G) {
   return RAFI_OK;
 }
 
+// Phase timings are read lazily -- at the next forward or stats read, off the
+// critical path -- and summed over every timed forward / bulk emit since
+// RAFI_OPT_TIMING was set.
+static void collect_timing(Ctx* c) {
+  if (!c->timing_unread) return;
+  c->timing_unread = false;
+  cudaEventSynchronize(c->ev[6]);
+  rafi_stats& s = c->st;
+  if (c->unread_fused) {
+    s.ms_hist = ev_ms(c->ev[0], c->ev[1]);
+    s.ms_scan = ev_ms(c->ev[1], c->ev[2]);
+    s.ms_count_exchange = ev_ms(c->ev[2], c->ev[3]);
+    s.ms_scatter = ev_ms(c->ev[3], c->ev[4]);
+    s.ms_payload_exchange = ev_ms(c->ev[4], c->ev[5]);  // the completion barrier
+    s.ms_wrapup = ev_ms(c->ev[5], c->ev[6]);
+  } else {
+    s.ms_hist = ev_ms(c->ev[0], c->ev[1]);
+    s.ms_scan = ev_ms(c->ev[1], c->ev[2]);
+    s.ms_scatter = ev_ms(c->ev[2], c->ev[3]);
+    s.ms_count_exchange = ev_ms(c->ev[3], c->ev[4]);
+    s.ms_payload_exchange = ev_ms(c->ev[7], c->ev[5]);
+    s.ms_wrapup = ev_ms(c->ev[5], c->ev[6]);
+  }
+  s.ms_total = ev_ms(c->ev[0], c->ev[6]);
+  s.acc_ms_hist += s.ms_hist;
+  s.acc_ms_scan += s.ms_scan;
+  s.acc_ms_scatter += s.ms_scatter;
+  s.acc_ms_count_exchange += s.ms_count_exchange;
+  s.acc_ms_payload_exchange += s.ms_payload_exchange;
+  s.acc_ms_wrapup += s.ms_wrapup;
+  s.acc_ms_total += s.ms_total;
+  s.acc_forwards += 1;
+  while (c->emit_head != c->emit_mark) {  // emits enqueued before that forward: complete
+    s.acc_ms_emit += ev_ms(c->ev_emit[c->emit_head][0], c->ev_emit[c->emit_head][1]);
+    s.acc_emits += 1;
+    c->emit_head = (c->emit_head + 1) % Ctx::kEmitEv;
+  }
+}
+
+static void mark_timing(Ctx* c, bool fused) {
+  c->timing_unread = true;
+  c->unread_fused = fused;
+  c->emit_mark = c->emit_tail;
+}
+
 static int64_t forward_fused(Ctx* c) {
   const bool T = c->timing;
   RAFI_CK(enqueue_fused(c, nullptr, T));
   uint64_t G = 0;
   RAFI_CK(refresh_host(c, &G));
-  if (T) {
-    c->st.ms_hist = ev_ms(c->ev[0], c->ev[1]);
-    c->st.ms_scan = ev_ms(c->ev[1], c->ev[2]);
-    c->st.ms_count_exchange = ev_ms(c->ev[2], c->ev[3]);
-    c->st.ms_scatter = ev_ms(c->ev[3], c->ev[4]);
-    c->st.ms_payload_exchange = ev_ms(c->ev[4], c->ev[5]);  // the completion barrier
-    c->st.ms_wrapup = ev_ms(c->ev[5], c->ev[6]);
-    c->st.ms_total = ev_ms(c->ev[0], c->ev[6]);
-  }
+  if (T) mark_timing(c, true);
   c->last_fused = true;
   c->round += 1;
   c->last_G = (int64_t)G;  // a8
@@ -393,8 +435,7 @@ static int64_t forward_staged(Ctx* c) {
   if (c->nprocs > 1)
     RAFI_CK_NCCL(ncclAllGather(c->Cdev + (size_t)c->proc * L * R, c->Cdev, (size_t)L * R, ncclUint64, c->comm,
                                c->stream));
-  RAFI_CK_CUDA(cudaMemcpyAsync(c->Chost, c->Cdev, sizeof(uint64_t) * R * R, cudaMemcpyDeviceToHost, c->stream));
-  RAFI_CK_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl, sizeof(CtrlDev) * L, cudaMemcpyDeviceToHost, c->stream));
+  RAFI_CK_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl, ctrl_c_bytes(c), cudaMemcpyDeviceToHost, c->stream));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[4], c->stream));
   RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
   // plan and the collective overflow decision (Z3)
@@ -473,14 +514,7 @@ static int64_t forward_staged(Ctx* c) {
   RAFI_CK(launch_wrapup(c));
   if (T) {
     RAFI_CK_CUDA(cudaEventRecord(c->ev[6], c->stream));
-    RAFI_CK_CUDA(cudaEventSynchronize(c->ev[6]));
-    c->st.ms_hist = ev_ms(c->ev[0], c->ev[1]);
-    c->st.ms_scan = ev_ms(c->ev[1], c->ev[2]);
-    c->st.ms_scatter = ev_ms(c->ev[2], c->ev[3]);
-    c->st.ms_count_exchange = ev_ms(c->ev[3], c->ev[4]);
-    c->st.ms_payload_exchange = ev_ms(c->ev[7], c->ev[5]);
-    c->st.ms_wrapup = ev_ms(c->ev[5], c->ev[6]);
-    c->st.ms_total = ev_ms(c->ev[0], c->ev[6]);
+    mark_timing(c, false);
   }
   c->last_cur = c->cur;
   c->last_fused = false;
@@ -493,6 +527,7 @@ static int64_t forward_staged(Ctx* c) {
 static int64_t forward(Ctx* c) {
   if (c->broken) { set_error("context unusable after an earlier collective error"); return RAFI_ERR_STATE; }
   RAFI_CK_CUDA(cudaSetDevice(c->device));
+  collect_timing(c);  // the previous forward's events, before they are re-recorded
   return c->exchange_eff == RAFI_EXCHANGE_FUSED ? forward_fused(c) : forward_staged(c);
 }
 
@@ -649,7 +684,15 @@ int rafi_emit_bulk(rafi_ctx* ctx, int local, const void* items, const int32_t* d
     if (!dev_items) { RAFI_CK_CUDA(cudaMemcpyAsync(si, items, ib, cudaMemcpyHostToDevice, c->stream)); it = si; }
     if (!dev_dests) { RAFI_CK_CUDA(cudaMemcpyAsync(sd, dests, (size_t)n * 4, cudaMemcpyHostToDevice, c->stream)); ds = sd; }
   }
-  return launch_emit_bulk(c, local, it, ds, n);
+  const int slot = c->emit_tail, next = (slot + 1) % Ctx::kEmitEv;
+  const bool timed = c->timing && next != c->emit_head;  // ring full: this emit goes untimed
+  if (timed) RAFI_CK_CUDA(cudaEventRecord(c->ev_emit[slot][0], c->stream));
+  RAFI_CK(launch_emit_bulk(c, local, it, ds, n));
+  if (timed) {
+    RAFI_CK_CUDA(cudaEventRecord(c->ev_emit[slot][1], c->stream));
+    c->emit_tail = next;
+  }
+  return RAFI_OK;
 }
 
 int64_t rafi_forward(rafi_ctx* ctx) {
@@ -784,6 +827,7 @@ int rafi_get_matrix(const rafi_ctx* ctx, uint64_t* Cm) {
 int rafi_get_stats(const rafi_ctx* ctx, int local, rafi_stats* out) {
   const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
   if (bad_local(c, local) || !out) return RAFI_ERR_INVALID_ARG;
+  collect_timing(const_cast<Ctx*>(c));  // lazily read the last timed forward (logically const)
   *out = c->st;
   const LocalRank& r = c->lr[local];
   out->round = c->round;
@@ -813,7 +857,14 @@ int rafi_set_option(rafi_ctx* ctx, int key, long long v) {
       if (rc != RAFI_OK) { c->exchange = old; resolve_exchange(c); }
       return rc;
     }
-    case RAFI_OPT_TIMING: c->timing = v != 0; return RAFI_OK;
+    case RAFI_OPT_TIMING:
+      c->timing = v != 0;
+      c->st.acc_ms_emit = c->st.acc_ms_hist = c->st.acc_ms_scan = c->st.acc_ms_scatter = 0;
+      c->st.acc_ms_count_exchange = c->st.acc_ms_payload_exchange = c->st.acc_ms_wrapup = c->st.acc_ms_total = 0;
+      c->st.acc_forwards = c->st.acc_emits = 0;
+      c->emit_head = c->emit_tail = c->emit_mark = 0;
+      c->timing_unread = false;
+      return RAFI_OK;
     case RAFI_OPT_TILE: {
       // only between rounds with an empty outgoing queue; re-sizes H/O
       if (v != 0 && (v < 256 || v > 4096 || (v & (v - 1)) != 0)) return RAFI_ERR_INVALID_ARG;  // 256 * 2^k

@@ -129,12 +129,18 @@ struct Ctx {
   size_t stage_bytes = 0;
 
   cudaEvent_t ev[8] = {};
+  static constexpr int kEmitEv = 32;     // ring of (start, end) event pairs for timed bulk emits
+  cudaEvent_t ev_emit[kEmitEv][2] = {};
+  int emit_head = 0, emit_tail = 0, emit_mark = 0;  // unread pairs [head, mark) are complete
+  bool timing_unread = false, unread_fused = false;  // last forward's events not read yet
   rafi_stats st{};
   uint64_t launches = 0;
   uint64_t fwd_launches = 0;
 };
 
 inline RankDev* rank_table(Ctx* c) { return c->rank_dev; }
+// bytes of the control blocks [L] followed by the count matrix [R*R] (one allocation)
+inline size_t ctrl_c_bytes(const Ctx* c) { return sizeof(CtrlDev) * c->L + sizeof(uint64_t) * c->R * c->R; }
 
 // kernels.cu
 uint32_t choose_tile(uint64_t item_bytes);

@@ -26,14 +26,9 @@
 
 namespace rafi_impl {
 
-// Scatter tuning (build-time; see paper_2605_30294_b200/build.py variants):
-// resident CTAs per SM, shared-memory budget per CTA (KiB), units in flight.
-#ifndef RAFI_SCATTER_MINB
-#define RAFI_SCATTER_MINB 2
-#endif
-#ifndef RAFI_SCATTER_SMEM_KB
-#define RAFI_SCATTER_SMEM_KB 110u
-#endif
+// Scatter tuning: units in flight per thread (build-time; see
+// paper_2605_30294_b200/build.py variants).  Resident CTAs per SM and the
+// per-CTA shared-memory budget depend on the item size (scatter_minb).
 #ifndef RAFI_SCATTER_ILP
 #define RAFI_SCATTER_ILP 4
 #endif
@@ -162,20 +157,21 @@ __device__ __forceinline__ uint32_t warp_sum(uint32_t x) {
   return x;
 }
 
-constexpr int kHistTilesPerWarp = 4;
-constexpr int kHistTilesPerCta = kWarps * kHistTilesPerWarp;  // 32 tiles = one "block" of the scan
-constexpr int kHistVec = 8;  // 16-byte dest loads in flight per lane
+constexpr int kHistTilesPerWarp = 1;
+constexpr int kHistTilesPerCta = kWarps * kHistTilesPerWarp;  // 8 tiles = one "block" of the scan
+constexpr int kHistVec = 4;  // 16-byte dest loads in flight per lane (one batch covers a 512-item tile)
 
 // Per-tile per-destination counts (the counting half of the paper's radix
 // sort by destination), one warp per tile, 16-byte loads with
-// 8 in flight per lane.  CTA (b, l) covers tiles 32b..32b+31 of local rank l
-// and also does the first level of the tile scan: for every destination d it
-// writes O[l][d][t] = items with dest d in tiles 32b..t-1 of the block, and
+// 4 in flight per lane, many small CTAs resident per SM.  CTA (b, l) covers
+// tiles 8b..8b+7 of local rank l and also does the first level of the tile
+// scan: for every destination d it writes O[l][d][t] = items with dest d in
+// tiles 8b..t-1 of the block, and
 // the block aggregate H[l][d][b] (scanned by k_scan).  RMAX > 0: register
 // counters for R <= RMAX reduced with warp shuffles; RMAX == 0: shared
 // counters fed by __match_any_sync aggregation.
 template <int RMAX>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 6)
 k_hist(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, int R, uint64_t cap, uint32_t T) {
   extern __shared__ uint32_t tc[];  // [kHistTilesPerCta][R] tile counts
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -322,7 +318,7 @@ __device__ __forceinline__ bool last_block(unsigned* done) {
 
 // One CTA per (destination d, local rank l): in place, H[l][d][b] := items
 // with dest d in blocks 0..b-1 (second scan level; the tile offset is then
-// O[l][d][t] + H[l][d][t/32]), and the row total send_count[d] -> count matrix
+// O[l][d][t] + H[l][d][t/8]), and the row total send_count[d] -> count matrix
 // C[g][d] (the paper's segment tally, kept on device).  The
 // per-destination base (send offset, or the receiver's recv offset under
 // FUSED) is added by k_plan / k_scatter.
@@ -470,8 +466,8 @@ __host__ __device__ inline ScatterLayout scatter_layout(uint32_t T, uint64_t B, 
 //   Item index = O[l][d][t] (prefix over earlier tiles) + rank within the tile
 //   + dst_off[l][d], the per-destination base from k_plan: send_off_me[d]
 //   (staged) or recv_off_d[me] (FUSED).
-template <typename U, bool kStageItems, int kK>
-__global__ void __launch_bounds__(kThreads, RAFI_SCATTER_MINB)
+template <typename U, bool kStageItems, int kK, int kMinB>
+__global__ void __launch_bounds__(kThreads, kMinB)
 k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint8_t* const* __restrict__ dst_table,
           const uint64_t* __restrict__ dst_off, const int* __restrict__ ovf, int L, int R, uint64_t cap, uint32_t T,
           int cur, uint32_t B, uint32_t UPI, FastDiv divU, ScatterLayout lay, unsigned* __restrict__ wrap_done,
@@ -714,10 +710,17 @@ static uint32_t unit_for(uint64_t B, uintptr_t align_bits) {
   return 1;
 }
 
+// Items up to 96 B: four 54-KiB CTAs per SM (more warps to hide the
+// dependent shared-memory/index latency of many small units); larger items:
+// two 110-KiB CTAs (longer tiles).  Measured with the cfg5 size sweep
+// (profiles/r01_scatter_variants.md).
+static int scatter_minb(uint64_t B) { return B <= 96 ? 4 : 2; }
+static uint32_t scatter_budget(uint64_t B) { return scatter_minb(B) == 4 ? 54u * 1024u : 110u * 1024u; }
+
 uint32_t choose_tile(uint64_t item_bytes) {
   // two pipeline stages (items + dests) plus 2 B/item of indices in ~110 KiB,
   // so two CTAs fit on an SM
-  const uint64_t t = (RAFI_SCATTER_SMEM_KB * 1024u) / (2 * item_bytes + 10);
+  const uint64_t t = scatter_budget(item_bytes) / (2 * item_bytes + 10);
   uint32_t k = 1;  // items per thread: a power of two (the scatter is templated on it)
   while (k < (uint32_t)kMaxK && (uint64_t)kThreads * k * 2 <= t) k *= 2;
   return kThreads * k;
@@ -788,7 +791,7 @@ int launch_scan(Ctx* c, int plan_mode, unsigned long long* G_out) {
   return RAFI_OK;
 }
 
-template <typename U, int kK>
+template <typename U, int kK, int kMinB>
 static int launch_scatter_k(Ctx* c, bool fused, bool wrap, uint32_t UPI, int grid) {
   const FastDiv dv(UPI);
   const bool si = stage_items(c->tile, c->B);
@@ -798,7 +801,7 @@ static int launch_scatter_k(Ctx* c, bool fused, bool wrap, uint32_t UPI, int gri
   const int* ovf = fused ? c->ovf_dev : nullptr;
   static int set_true = 0, set_false = 0;  // per instantiation: the largest smem opt-in already granted
   if (si) {
-    auto k = k_scatter<U, true, kK>;
+    auto k = k_scatter<U, true, kK, kMinB>;
     if ((int)lay.total > set_true) {
       RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
       set_true = (int)lay.total;
@@ -807,7 +810,7 @@ static int launch_scatter_k(Ctx* c, bool fused, bool wrap, uint32_t UPI, int gri
                                                c->cur, (uint32_t)c->B, UPI, dv, lay, wrap ? c->done_dev + 1 : nullptr,
                                                c->ctrl, c->plan_dev);
   } else {
-    auto k = k_scatter<U, false, kK>;
+    auto k = k_scatter<U, false, kK, kMinB>;
     if ((int)lay.total > set_false) {
       RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
       set_false = (int)lay.total;
@@ -820,23 +823,30 @@ static int launch_scatter_k(Ctx* c, bool fused, bool wrap, uint32_t UPI, int gri
   return RAFI_OK;
 }
 
-template <typename U>
-static int launch_scatter_t(Ctx* c, bool fused, bool wrap, uint32_t UPI, int grid) {
+template <typename U, int kMinB>
+static int launch_scatter_m(Ctx* c, bool fused, bool wrap, uint32_t UPI, int grid) {
   switch (c->tile / kThreads) {
-    case 1: return launch_scatter_k<U, 1>(c, fused, wrap, UPI, grid);
-    case 2: return launch_scatter_k<U, 2>(c, fused, wrap, UPI, grid);
-    case 4: return launch_scatter_k<U, 4>(c, fused, wrap, UPI, grid);
-    case 8: return launch_scatter_k<U, 8>(c, fused, wrap, UPI, grid);
-    case 16: return launch_scatter_k<U, 16>(c, fused, wrap, UPI, grid);
+    case 1: return launch_scatter_k<U, 1, kMinB>(c, fused, wrap, UPI, grid);
+    case 2: return launch_scatter_k<U, 2, kMinB>(c, fused, wrap, UPI, grid);
+    case 4: return launch_scatter_k<U, 4, kMinB>(c, fused, wrap, UPI, grid);
+    case 8: return launch_scatter_k<U, 8, kMinB>(c, fused, wrap, UPI, grid);
+    case 16: return launch_scatter_k<U, 16, kMinB>(c, fused, wrap, UPI, grid);
     default: set_error("tile must be 256 * 2^k"); return RAFI_ERR_INVALID_ARG;
   }
+}
+
+template <typename U>
+static int launch_scatter_t(Ctx* c, bool fused, bool wrap, uint32_t UPI, int grid) {
+  return scatter_minb(c->B) == 4 ? launch_scatter_m<U, 4>(c, fused, wrap, UPI, grid)
+                                 : launch_scatter_m<U, 2>(c, fused, wrap, UPI, grid);
 }
 
 int launch_scatter(Ctx* c, bool fused, bool wrap) {
   const uint32_t unit = unit_for(c->B, 0);
   const uint32_t UPI = (uint32_t)(c->B / unit);
   const size_t smem = scatter_smem_bytes(c->tile, c->B, c->R);
-  const int per_sm = smem <= (size_t)RAFI_SCATTER_SMEM_KB * 1024 ? RAFI_SCATTER_MINB : 1;
+  const int fit = (int)((227u * 1024u) / (smem + 1024u));  // CTAs whose shared memory fits on an SM
+  const int per_sm = std::max(1, std::min(scatter_minb(c->B), fit));
   const int grid = persistent_grid(c, per_sm);
   int rc;
   switch (unit) {

@@ -57,6 +57,10 @@ class Stats(C.Structure):
         ("ms_count_exchange", C.c_float), ("ms_payload_exchange", C.c_float), ("ms_wrapup", C.c_float),
         ("ms_total", C.c_float), ("ms_reserved", C.c_float),
         ("kernel_launches", C.c_uint64), ("forward_launches", C.c_uint64),
+        ("acc_ms_emit", C.c_double), ("acc_ms_hist", C.c_double), ("acc_ms_scan", C.c_double),
+        ("acc_ms_scatter", C.c_double), ("acc_ms_count_exchange", C.c_double),
+        ("acc_ms_payload_exchange", C.c_double), ("acc_ms_wrapup", C.c_double), ("acc_ms_total", C.c_double),
+        ("acc_forwards", C.c_uint64), ("acc_emits", C.c_uint64),
     ]
 
     def as_dict(self):

@@ -77,3 +77,74 @@ def test_multigpu_snapshot_parity(world, exchange, B, pattern):
         pytest.skip("needs %d GPUs" % world)
     import torch.multiprocessing as mp
     mp.spawn(_worker, args=(world, _free_port(), B, 30011, pattern, exchange, 3), nprocs=world, join=True)
+
+
+def _worker_hybrid(rank, world, port, L, B, n, graph):
+    """P processes x L logical ranks each (R = P*L), FUSED exchange over
+    local HBM and NVLink peer mappings; optionally the forward captured in a
+    CUDA graph (NCCL collectives inside the capture, device-side G)."""
+    import torch.distributed as dist
+
+    import oracle
+    import synth
+    from paper_2605_30294_b200 import rafi
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    obj = [rafi.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    comm = rafi.nccl_comm_init(world, rank, obj[0], rank)
+    R = world * L
+    cap = 2 * n
+    s = torch.cuda.Stream()
+    ctx = rafi.Context(B, cap, comm=comm, stream=s, local_ranks=L)
+    assert ctx.num_ranks == R and ctx.get_option(rafi.OPT_EXCHANGE) == rafi.EXCHANGE_FUSED
+    G_dev = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ex = None
+    for rnd in range(3):
+        for l in range(L):
+            g = rank * L + l
+            it = synth.make_items(g, rnd, n, max(B, 16))[:, :B].copy()
+            ds = synth.make_dests("uniform", 11 + rnd, g, rnd, n, R)
+            ctx.emit_bulk(it, ds, n, local=l)
+        snaps = []
+        for l in range(L):
+            snaps.append(ctx.read_outgoing(l))
+        allsnaps = [None] * world
+        dist.all_gather_object(allsnaps, snaps)
+        w = oracle.World(R, cap, B)
+        for p, sn in enumerate(allsnaps):
+            for l, (items, dests, ctr, inv) in enumerate(sn):
+                w.load_snapshot(p * L + l, items, dests, ctr, inv)
+        G_o = w.forward()
+        if graph:
+            if ex is None:
+                ctx.capture_begin()
+                ctx.forward_async(G_dev)
+                ex = ctx.capture_end()
+            ctx.graph_launch(ex)
+            s.synchronize()
+            G = int(G_dev.item())
+            ctx.sync_host()
+        else:
+            G = ctx.forward_rc()
+        assert G == G_o, (rank, rnd, G, G_o)
+        assert np.array_equal(ctx.matrix(), w.C())
+        for l in range(L):
+            assert np.array_equal(ctx.read_incoming(l), w.incoming(rank * L + l)), (rank, l)
+    if ex is not None:
+        rafi.Context.graph_destroy(ex)
+    ctx.close()
+    rafi.nccl_comm_destroy(comm)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("graph", [False, True])
+@pytest.mark.parametrize("world,L", [(2, 2), (2, 4), (4, 2)])
+def test_multigpu_hybrid_local_ranks(world, L, graph):
+    if torch.cuda.device_count() < world:
+        pytest.skip("needs %d GPUs" % world)
+    import torch.multiprocessing as mp
+    mp.spawn(_worker_hybrid, args=(world, _free_port(), L, 44, 20011, graph), nprocs=world, join=True)
