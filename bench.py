@@ -344,23 +344,27 @@ def main():
         ctx.set_option(rafi.OPT_TIMING, 0)
         items_p = torch.from_numpy(items_h).pin_memory()
         dests_p = torch.from_numpy(dests_h).pin_memory()
-        out_p = torch.empty((cap, B), dtype=torch.uint8).pin_memory()
+        # two pinned result buffers: step k's read-back (copy-out stream) overlaps
+        # step k+1's host-to-device copy (copy-in stream) over full-duplex PCIe
+        outs = [torch.empty((cap, B), dtype=torch.uint8).pin_memory() for _ in range(2)]
         Ke = max(3, min(K, 5))
-        for _ in range(2):
+        for k in range(2):
             ctx.emit_bulk(items_p, dests_p, n)
             ctx.forward()
-            ctx.read_incoming(out=out_p[: ctx.num_incoming()].numpy())
+            ctx.read_incoming_async(outs[k % 2][: ctx.num_incoming()])
+        ctx.read_wait()
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         d2h = 0
         e0.record(stream)
-        for _ in range(Ke):
+        for k in range(Ke):
             ctx.emit_bulk(items_p, dests_p, n)             # H2D inside the call (host pointers)
             ctx.forward()
             m = ctx.num_incoming()
-            ctx.read_incoming(out=out_p[:m].numpy())       # D2H of the result
+            ctx.read_incoming_async(outs[k % 2][:m])       # D2H of the result
             d2h += m * B
+        ctx.read_wait()                                    # every result is in host memory
         e1.record(stream)
         barrier()
         ms_e = max_over_ranks(e0.elapsed_time(e1))

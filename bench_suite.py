@@ -268,8 +268,11 @@ def run_cfg4(env, args):
 
 # ----------------------------------------------------------------------------- cfg5 / sweep
 
-def fwd_rate(env, B, n, steps=5, warmup=2, pattern="uniform"):
-    """emit_bulk + forward of n items/rank, R = world (one rank per GPU)."""
+def fwd_rate(env, B, n, steps=5, warmup=2, pattern="uniform", graph=False):
+    """emit_bulk + forward of n items/rank, R = world (one rank per GPU).
+    With graph=True the step is also captured as a CUDA graph of
+    [emit_bulk + rafi_forward_async] and replayed (device-side G, no host
+    synchronisation per step): the per-step latency without host overhead."""
     import synth
     torch = env.torch
     N = env.world
@@ -279,31 +282,49 @@ def fwd_rate(env, B, n, steps=5, warmup=2, pattern="uniform"):
     items = torch.randint(0, 256, (n, B), dtype=torch.uint8, device=env.dev, generator=gen)
     ds = synth.make_dests(pattern, synth.CONFIG_SEEDS[5], env.rank, 0, n, N)
     dests = torch.from_numpy(ds).to(env.dev)
-    ctx = env.ctx(B, n + n // 8 + 4096)
+    side = torch.cuda.Stream(device=env.dev)
+    ctx = env.rafi.Context(B, n + n // 8 + 4096, comm=env.comm, stream=side, device=env.local)
+    saved, env.stream = env.stream, side
     for _ in range(warmup):
         ctx.emit_bulk(items, dests, n)
         ctx.forward()
     ctx.set_option(env.rafi.OPT_TIMING, 1)
-    sc, px = [], []
 
     def loop():
         for _ in range(steps):
             ctx.emit_bulk(items, dests, n)
             ctx.forward()
-            st = ctx.stats()
-            sc.append(st["ms_scatter"])
-            px.append(st["bytes_sent_remote"])
 
     ms, _ = env.timed(loop)
-    scat = sum(sc) / len(sc)
-    remote = sum(px) / len(px)
+    st = ctx.stats()
+    scat = st["acc_ms_scatter"] / max(st["acc_forwards"], 1)
+    remote = st["bytes_sent_remote"]
+    out = {"items_per_rank": n, "item_bytes": B, "ms_per_step": ms / steps,
+           "value": N * n * steps / (ms / 1e3), "unit": "items/s",
+           "scatter_ms": scat, "scatter_hbm_gbs": n * (2 * B + 4) / (scat / 1e3) / 1e9,
+           "nvlink_gbs_per_gpu": (remote / (scat / 1e3) / 1e9) if N > 1 else None}
+    if graph:
+        ctx.set_option(env.rafi.OPT_TIMING, 0)
+        G_dev = torch.zeros(1, dtype=torch.int64, device=env.dev)
+        ctx.capture_begin()
+        ctx.emit_bulk(items, dests, n)
+        ctx.forward_async(G_dev)
+        ex = ctx.capture_end()
+        for _ in range(3):
+            ctx.graph_launch(ex)
+        K = 50
+        msg, _ = env.timed(lambda: [ctx.graph_launch(ex) for _ in range(K)])
+        side.synchronize()
+        assert int(G_dev.item()) == N * n
+        ctx.sync_host()
+        env.rafi.Context.graph_destroy(ex)
+        out["graph_ms_per_step"] = msg / K
+        out["graph_value"] = N * n * K / (msg / 1e3)
+    env.stream = saved
     ctx.close()
     del items, dests
     torch.cuda.empty_cache()
-    return {"items_per_rank": n, "item_bytes": B, "ms_per_step": ms / steps,
-            "value": N * n * steps / (ms / 1e3), "unit": "items/s",
-            "scatter_ms": scat, "scatter_hbm_gbs": n * (2 * B + 4) / (scat / 1e3) / 1e9,
-            "nvlink_gbs_per_gpu": (remote / (scat / 1e3) / 1e9) if N > 1 else None}
+    return out
 
 
 def run_cfg5(env, args):
@@ -316,7 +337,7 @@ def run_cfg5(env, args):
 
 def run_sweep(env, args):
     for e in range(10, 25, 2):
-        r = fwd_rate(env, 44, 1 << e, steps=10 if e < 20 else 5)
+        r = fwd_rate(env, 44, 1 << e, steps=10 if e < 20 else 5, graph=True)
         r["workload"] = "sweep: 2^%d x 44-B items/rank, uniform over R=%d" % (e, env.world)
         env.emit(r)
 

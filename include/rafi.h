@@ -159,8 +159,11 @@ uint64_t rafi_num_incoming(const rafi_ctx* ctx, int local);
  * context stream).  Invalid destinations are rejected and counted; emits past
  * capacity are dropped and counted.  Within one call accepted items keep their
  * relative order in the queue except across 2048-item blocks, whose order
- * follows the atomic counter.  Asynchronous w.r.t. the host for device
- * pointers. */
+ * follows the atomic counter.  Asynchronous w.r.t. the host for device and
+ * pinned host pointers: host inputs are copied on a separate copy-in stream
+ * into one of two staging buffers (so the copy of the next batch overlaps
+ * this batch's forward and read-back); the caller must keep a host buffer
+ * unchanged until the context stream has passed this call. */
 int rafi_emit_bulk(rafi_ctx* ctx, int local, const void* items, const int32_t* dests, uint64_t n);
 
 /* ---- forwarding -------------------------------------------------------------- */
@@ -216,6 +219,17 @@ uint64_t rafi_item_bytes(const rafi_ctx* ctx);
 /* Copies incoming items [first, first+count) of local rank `local` to dst
  * (host or device pointer). */
 int rafi_read_incoming(const rafi_ctx* ctx, int local, void* dst, uint64_t first, uint64_t count);
+
+/* Asynchronous rafi_read_incoming (dst should be pinned host memory or
+ * device memory): the copy runs on the context's copy-out stream after the
+ * work already enqueued on the context stream, and overlaps later work -- in
+ * particular the next rafi_emit_bulk's host-to-device copy, which runs on a
+ * separate copy-in stream.  The next forward waits for it before rewriting
+ * the incoming queue.  dst must stay valid until rafi_read_wait returns. */
+int rafi_read_incoming_async(rafi_ctx* ctx, int local, void* dst, uint64_t first, uint64_t count);
+
+/* Blocks until every rafi_read_incoming_async of the context has landed. */
+int rafi_read_wait(rafi_ctx* ctx);
 
 /* Snapshot of the outgoing queue before forwarding: *ctr and *invalid receive
  * the raw counters; items_dst / dests_dst (may be NULL) receive

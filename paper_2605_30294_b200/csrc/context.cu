@@ -193,6 +193,14 @@ static void destroy_ctx(Ctx* c) {
   cudaFree(c->rank_dev); cudaFree(c->ctrl); cudaFree(c->runs_dev); cudaFree(c->plan_dev);
   cudaFree(c->off_dev); cudaFree(c->ovf_dev); cudaFree(c->in_table_dev); cudaFree(c->done_dev);
   cudaFree(c->stage);
+  if (c->io_in) {
+    cudaStreamSynchronize(c->io_in); cudaStreamSynchronize(c->io_out);
+    cudaStreamDestroy(c->io_in); cudaStreamDestroy(c->io_out);
+    for (int s = 0; s < 2; ++s) {
+      cudaFree(c->stage2[s]); cudaEventDestroy(c->ev_stage_ready[s]); cudaEventDestroy(c->ev_stage_free[s]);
+    }
+    cudaEventDestroy(c->ev_in_ready); cudaEventDestroy(c->ev_out_done);
+  }
   cudaFreeHost(c->ctrl_host); cudaFreeHost(c->runs_host); cudaFreeHost(c->plan_host);
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);
   for (auto& pr : c->ev_emit)
@@ -528,7 +536,26 @@ static int64_t forward(Ctx* c) {
   if (c->broken) { set_error("context unusable after an earlier collective error"); return RAFI_ERR_STATE; }
   RAFI_CK_CUDA(cudaSetDevice(c->device));
   collect_timing(c);  // the previous forward's events, before they are re-recorded
+  if (c->out_pending) {  // an asynchronous read of the incoming queue must land before it is rewritten
+    RAFI_CK_CUDA(cudaStreamWaitEvent(c->stream, c->ev_out_done, 0));
+    c->out_pending = false;
+  }
   return c->exchange_eff == RAFI_EXCHANGE_FUSED ? forward_fused(c) : forward_staged(c);
+}
+
+// Copy streams for host I/O (rafi_emit_bulk from host memory, asynchronous
+// read-back), created on first use.
+static int ensure_io(Ctx* c) {
+  if (c->io_in) return RAFI_OK;
+  RAFI_CK_CUDA(cudaStreamCreateWithFlags(&c->io_in, cudaStreamNonBlocking));
+  RAFI_CK_CUDA(cudaStreamCreateWithFlags(&c->io_out, cudaStreamNonBlocking));
+  for (int s = 0; s < 2; ++s) {
+    RAFI_CK_CUDA(cudaEventCreateWithFlags(&c->ev_stage_ready[s], cudaEventDisableTiming));
+    RAFI_CK_CUDA(cudaEventCreateWithFlags(&c->ev_stage_free[s], cudaEventDisableTiming));
+  }
+  RAFI_CK_CUDA(cudaEventCreateWithFlags(&c->ev_in_ready, cudaEventDisableTiming));
+  RAFI_CK_CUDA(cudaEventCreateWithFlags(&c->ev_out_done, cudaEventDisableTiming));
+  return RAFI_OK;
 }
 
 static bool bad_local(const Ctx* c, int local) { return !c || local < 0 || local >= c->L; }
@@ -592,6 +619,7 @@ int rafi_resize(rafi_ctx* ctx, size_t capacity) {
   if (c->broken) return RAFI_ERR_STATE;
   if (capacity >= (1ull << 32)) { set_error("capacity must be < 2^32"); return RAFI_ERR_INVALID_ARG; }
   RAFI_CK_CUDA(cudaSetDevice(c->device));
+  if (c->io_out) RAFI_CK_CUDA(cudaStreamSynchronize(c->io_out));  // pending async reads of the old queues
   RAFI_CK_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl, sizeof(CtrlDev) * c->L, cudaMemcpyDeviceToHost, c->stream));
   RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
   for (int l = 0; l < c->L; ++l)
@@ -670,19 +698,29 @@ int rafi_emit_bulk(rafi_ctx* ctx, int local, const void* items, const int32_t* d
     return c->cls_dev[k];
   };
   const bool dev_items = classify(0, items), dev_dests = classify(1, dests);
+  int sslot = -1;
   if (!dev_items || !dev_dests) {
+    // host inputs: copied on the copy-in stream into one of two staging
+    // buffers, so the copy of batch k+1 overlaps the device work (and the
+    // asynchronous read-back) of batch k
+    RAFI_CK(ensure_io(c));
+    sslot = c->stage_slot ^= 1;
     const size_t ib = (size_t)n * c->B, need = ((ib + 255) & ~(size_t)255) + (size_t)n * 4;
-    if (need > c->stage_bytes) {
+    if (need > c->stage_cap[sslot]) {
       RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
-      cudaFree(c->stage);
-      c->stage = nullptr; c->stage_bytes = 0;
-      RAFI_CK(alloc_dev((void**)&c->stage, need));
-      c->stage_bytes = need;
+      RAFI_CK_CUDA(cudaStreamSynchronize(c->io_in));
+      cudaFree(c->stage2[sslot]);
+      c->stage2[sslot] = nullptr; c->stage_cap[sslot] = 0; c->stage_used[sslot] = false;
+      RAFI_CK(alloc_dev((void**)&c->stage2[sslot], need));
+      c->stage_cap[sslot] = need;
     }
-    uint8_t* si = c->stage;
-    int32_t* sd = reinterpret_cast<int32_t*>(c->stage + ((ib + 255) & ~(size_t)255));
-    if (!dev_items) { RAFI_CK_CUDA(cudaMemcpyAsync(si, items, ib, cudaMemcpyHostToDevice, c->stream)); it = si; }
-    if (!dev_dests) { RAFI_CK_CUDA(cudaMemcpyAsync(sd, dests, (size_t)n * 4, cudaMemcpyHostToDevice, c->stream)); ds = sd; }
+    if (c->stage_used[sslot]) RAFI_CK_CUDA(cudaStreamWaitEvent(c->io_in, c->ev_stage_free[sslot], 0));
+    uint8_t* si = c->stage2[sslot];
+    int32_t* sd = reinterpret_cast<int32_t*>(si + ((ib + 255) & ~(size_t)255));
+    if (!dev_items) { RAFI_CK_CUDA(cudaMemcpyAsync(si, items, ib, cudaMemcpyHostToDevice, c->io_in)); it = si; }
+    if (!dev_dests) { RAFI_CK_CUDA(cudaMemcpyAsync(sd, dests, (size_t)n * 4, cudaMemcpyHostToDevice, c->io_in)); ds = sd; }
+    RAFI_CK_CUDA(cudaEventRecord(c->ev_stage_ready[sslot], c->io_in));
+    RAFI_CK_CUDA(cudaStreamWaitEvent(c->stream, c->ev_stage_ready[sslot], 0));
   }
   const int slot = c->emit_tail, next = (slot + 1) % Ctx::kEmitEv;
   const bool timed = c->timing && next != c->emit_head;  // ring full: this emit goes untimed
@@ -692,6 +730,33 @@ int rafi_emit_bulk(rafi_ctx* ctx, int local, const void* items, const int32_t* d
     RAFI_CK_CUDA(cudaEventRecord(c->ev_emit[slot][1], c->stream));
     c->emit_tail = next;
   }
+  if (sslot >= 0) {  // the staging slot is free again once the emit kernel has read it
+    RAFI_CK_CUDA(cudaEventRecord(c->ev_stage_free[sslot], c->stream));
+    c->stage_used[sslot] = true;
+  }
+  return RAFI_OK;
+}
+
+int rafi_read_incoming_async(rafi_ctx* ctx, int local, void* dst, uint64_t first, uint64_t count) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (bad_local(c, local) || (count && !dst)) return RAFI_ERR_INVALID_ARG;
+  const LocalRank& r = c->lr[local];
+  if (first > r.num_in || count > r.num_in - first) return RAFI_ERR_INVALID_ARG;
+  if (!count) return RAFI_OK;
+  RAFI_CK_CUDA(cudaSetDevice(c->device));
+  RAFI_CK(ensure_io(c));
+  RAFI_CK_CUDA(cudaEventRecord(c->ev_in_ready, c->stream));  // incoming queue final in stream order
+  RAFI_CK_CUDA(cudaStreamWaitEvent(c->io_out, c->ev_in_ready, 0));
+  RAFI_CK_CUDA(cudaMemcpyAsync(dst, r.in + first * c->B, count * c->B, cudaMemcpyDefault, c->io_out));
+  RAFI_CK_CUDA(cudaEventRecord(c->ev_out_done, c->io_out));
+  c->out_pending = true;
+  return RAFI_OK;
+}
+
+int rafi_read_wait(rafi_ctx* ctx) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return RAFI_ERR_INVALID_ARG;
+  if (c->io_out) RAFI_CK_CUDA(cudaStreamSynchronize(c->io_out));
   return RAFI_OK;
 }
 

@@ -124,9 +124,17 @@ struct Ctx {
 
   const void* cls_ptr[2] = {nullptr, nullptr};  // rafi_emit_bulk pointer-type cache
   bool cls_dev[2] = {false, false};
-  // host staging for rafi_emit_bulk from host memory
-  uint8_t* stage = nullptr;
+  // host I/O: staging for rafi_emit_bulk from host memory (double-buffered,
+  // filled on io_in) and asynchronous read-back (io_out)
+  uint8_t* stage = nullptr;   // (legacy single buffer, unused)
   size_t stage_bytes = 0;
+  cudaStream_t io_in = nullptr, io_out = nullptr;
+  uint8_t* stage2[2] = {nullptr, nullptr};
+  size_t stage_cap[2] = {0, 0};
+  bool stage_used[2] = {false, false};
+  int stage_slot = 1;
+  cudaEvent_t ev_stage_ready[2] = {}, ev_stage_free[2] = {}, ev_in_ready = nullptr, ev_out_done = nullptr;
+  bool out_pending = false;
 
   cudaEvent_t ev[8] = {};
   static constexpr int kEmitEv = 32;     // ring of (start, end) event pairs for timed bulk emits

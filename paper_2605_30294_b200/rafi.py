@@ -86,6 +86,8 @@ SIGNATURES = {
     "rafi_read_outgoing": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64),
                                      C.POINTER(C.c_uint64)]),
     "rafi_read_binned": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64]),
+    "rafi_read_incoming_async": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_uint64]),
+    "rafi_read_wait": (C.c_int, [C.c_void_p]),
     "rafi_get_matrix": (C.c_int, [C.c_void_p, C.c_void_p]),
     "rafi_get_stats": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(Stats)]),
     "rafi_set_option": (C.c_int, [C.c_void_p, C.c_int, C.c_longlong]),
@@ -359,6 +361,16 @@ class Context:
             out = np.empty((count, self.item_bytes), np.uint8)
         _check(lib().rafi_read_incoming(self._h, local, _ptr(out), first, count), "rafi_read_incoming")
         return out
+
+    def read_incoming_async(self, out, local=0, first=0, count=None):
+        """Enqueue the read-back of the incoming queue into `out` (pinned host or device)."""
+        if count is None:
+            count = self.num_incoming(local) - first
+        _check(lib().rafi_read_incoming_async(self._h, local, _ptr(out), first, count), "rafi_read_incoming_async")
+        return out
+
+    def read_wait(self):
+        _check(lib().rafi_read_wait(self._h), "rafi_read_wait")
 
     def read_outgoing(self, local=0, with_items=True):
         ctr, inv = C.c_uint64(), C.c_uint64()

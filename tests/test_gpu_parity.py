@@ -252,3 +252,31 @@ def test_full_size_cfg2_shape(L, n, exchange):
         for l in range(L):
             ctx.drv_emit_synthetic(synth.PATTERNS["uniform"], synth.CONFIG_SEEDS[2], 0, n, local=l)
         p1_forward(ctx, L, B)
+
+
+def test_host_io_overlap_rounds():
+    """rafi_emit_bulk from pinned host memory (copy-in stream, double-buffered
+    staging) and rafi_read_incoming_async (copy-out stream) over several
+    rounds with no host waits in between: each read must capture its own
+    round (the next forward waits for it), matching the oracle."""
+    B, L, n, rounds = 48, 2, 30000, 4
+    pins = [torch.empty((2 * n, B), dtype=torch.uint8).pin_memory() for _ in range(rounds)]
+    host_in = []
+    sizes, exp = [], []
+    with _ctx(B, 2 * n, L) as ctx:
+        for rnd in range(rounds):
+            inputs = make_inputs(L, n - 1000 * rnd, B, "uniform", 5 + rnd, rnd=rnd)
+            w = oracle_sequential(L, 2 * n, B, inputs)
+            w.forward()
+            exp.append(w.incoming(1))
+            for l, (it, ds) in enumerate(inputs):
+                hi, hd = torch.from_numpy(it).pin_memory(), torch.from_numpy(ds).pin_memory()
+                host_in.append((hi, hd))  # keep alive until the copies ran
+                ctx.emit_bulk(hi, hd, len(ds), local=l)
+            ctx.forward()
+            m = ctx.num_incoming(1)
+            sizes.append(m)
+            ctx.read_incoming_async(pins[rnd][:m], local=1)
+        ctx.read_wait()
+    for rnd in range(rounds):
+        assert np.array_equal(canonical(pins[rnd][: sizes[rnd]].numpy()), canonical(exp[rnd])), rnd
