@@ -203,6 +203,49 @@ def run_nbody(env, args):
     P.close(); V.close(); Q.close()
 
 
+def run_streamlines(env, args):
+    """NEXT-4: streamlines on a sampled ABC-flow field (129^3 vertices), R=8
+    macrocell blocks with one-vertex halos, 1M seeds/rank, 64 RK4 steps."""
+    import numpy as np
+    R = 8
+    L = R // env.world
+    n = args.items or 1024 * 1024
+    torch = env.torch
+    nv = 129
+    c = np.linspace(0.0, 1.0, nv)
+    z, y, x = np.meshgrid(c, c, c, indexing="ij")
+    tp = 2 * np.pi
+    field = np.ascontiguousarray(np.stack((np.sin(tp * z) + 0.43 * np.cos(tp * y), 0.7 * np.sin(tp * x) + np.cos(tp * z),
+                                           0.43 * np.sin(tp * y) + 0.7 * np.cos(tp * x)), axis=-1), dtype=np.float32)
+    h = 0.4 * (1.0 / (nv - 1)) / (2 * float(np.abs(field).max()))
+    rng = np.random.default_rng(0x5EED0004 + env.rank)
+    ctx = env.ctx(16, 2 * n + 4096, L)
+    f = env.rafi.StreamField(ctx, field, grid_dims(R))
+    rpos = torch.zeros((R * n, 3), dtype=torch.float32, device=env.dev)
+    rst = torch.zeros((R * n,), dtype=torch.int32, device=env.dev)
+
+    def run():
+        for l in range(L):
+            f.seed(rng.random((n, 3)).astype(np.float32), (env.rank * L + l) * n, local=l)
+        total, k = 0, 0
+        while True:
+            G = ctx.forward()
+            total += G
+            if G == 0:
+                return total, k
+            k += 1
+            f.step(k, h, 1e-7, 64, rpos, rst)
+
+    run()
+    ms, (total, rounds) = env.timed(run)
+    env.emit({"workload": "streamlines: ABC flow on a 129^3 lattice, R=8 blocks + halo, %d seeds/rank, 64 RK4 steps"
+                          % n, "metric": "forwarded work items/sec (app + forward, all rounds)",
+              "value": total / (ms / 1e3), "unit": "items/s", "rounds": rounds, "forwarded_items": total,
+              "ms_total": ms, "halo_misses": f.halo_misses(), "local_ranks": L})
+    f.close()
+    ctx.close()
+
+
 # ----------------------------------------------------------------------------- cfg3 / cfg4
 
 def run_cfg3(env, args):
@@ -344,13 +387,13 @@ def run_sweep(env, args):
 
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("workload", choices=["cfg1", "cfg3", "cfg4", "cfg5", "sweep", "latency", "nbody"])
+    p.add_argument("workload", choices=["cfg1", "cfg3", "cfg4", "cfg5", "sweep", "latency", "nbody", "streamlines"])
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--items", type=int, default=0)
     args = p.parse_args()
     env = Env(args)
     {"cfg1": run_cfg1, "cfg3": run_cfg3, "cfg4": run_cfg4, "cfg5": run_cfg5, "sweep": run_sweep,
-     "latency": run_latency, "nbody": run_nbody}[args.workload](
+     "latency": run_latency, "nbody": run_nbody, "streamlines": run_streamlines}[args.workload](
         env, args)
     if env.comm:
         env.rafi.nccl_comm_destroy(env.comm)

@@ -99,6 +99,35 @@ int rafi_drv_nbody_refine(rafi_ctx* V, rafi_ctx* Q, const unsigned long long* st
 /* each request is answered with this rank's non-empty octant nodes */
 int rafi_drv_nbody_respond(rafi_ctx* Q, rafi_ctx* V, const unsigned long long* stats_dev);
 
+/* ---- streamlines on a sampled vector field (§5.4; NEXT-4) --
+ * A vertex lattice nx*ny*nz of float3 over [0,1]^3 (x fastest) is split into
+ * gx*gy*gz macrocell blocks of (nx-1)/gx x ... cells; every rank keeps its
+ * block plus a one-vertex halo, so the RK4 stages of a particle it owns
+ * sample exactly the global field as long as h*|v| <= half a cell (the
+ * result is then independent of the partition).  Item (16 B): {u32 id;
+ * float x, y, z}.  Sampling is trilinear, evaluated as
+ * a*(1-f) + b*f per axis (x, then y, then z); owner(p) = macrocell of the
+ * lattice cell floor(p*(n-1)) clamped to the last cell.
+ * step (round rnd): one classical RK4 step per incoming particle; it retires
+ * -- result_pos[id] / result_steps[id] written -- if a stage leaves the
+ * domain (steps = rnd-1, position unchanged), the step moved less than eps,
+ * the new position is outside [0,1)^3, or rnd >= max_steps; otherwise it is
+ * emitted to owner(new position).
+ * create copies the blocks of every local rank from the host field
+ * (nx*ny*nz*3 floats) to the device; the handle is freed by destroy. */
+typedef struct rafi_stream_field rafi_stream_field;
+int rafi_drv_stream_create(rafi_ctx* ctx, const float* field_host, int nx, int ny, int nz, int gx, int gy, int gz,
+                           rafi_stream_field** out);
+/* emits n seeds (positions seeds_host[3n], ids id0..id0+n-1) from local rank
+ * `local` to their owners */
+int rafi_drv_stream_seed(rafi_stream_field* f, int local, const float* seeds_host, uint64_t n, uint32_t id0);
+int rafi_drv_stream_step(rafi_stream_field* f, uint32_t rnd, float h, float eps, uint32_t max_steps,
+                         float* result_pos, uint32_t* result_steps);
+int rafi_drv_stream_destroy(rafi_stream_field* f);
+/* number of stage samples that fell outside a rank's block + halo (the
+ * h*|v| <= half-cell condition broken); blocking */
+int rafi_drv_stream_halo_misses(rafi_stream_field* f, int* count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,7 +19,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "rafi_oracle.c")
-_SRCS = [_SRC, os.path.join(_HERE, "proxies.c"), os.path.join(_HERE, "nbody.c")]
+_SRCS = [_SRC, os.path.join(_HERE, "proxies.c"), os.path.join(_HERE, "nbody.c"), os.path.join(_HERE, "streamlines.c")]
 _LIB = os.path.join(_HERE, "liborafi.so")
 
 OK = 0
@@ -94,6 +94,11 @@ def lib():
             "orc_nbody_root": (None, [P, i32, vp]),
             "orc_nbody_refine": (None, [P, P, i32, vp, C.c_float]),
             "orc_nbody_respond": (None, [P, P, i32, vp]),
+            # streamlines.c (CPU twin of the streamline driver, global-field sampling)
+            "orc_sl_owner": (i32, [vp, i32, i32, i32, i32, i32, i32]),
+            "orc_sl_seed": (None, [P, i32, vp, i32, i32, i32, i32, i32, i32, vp, u64, C.c_uint32]),
+            "orc_sl_step": (None, [P, i32, vp, i32, i32, i32, i32, i32, i32, C.c_uint32, C.c_float, C.c_float,
+                                   C.c_uint32, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -265,6 +270,33 @@ class NBody:
     def respond(self):
         for r in range(self.R):
             lib().orc_nbody_respond(self.Q._w, self.V._w, r, self.stats[r].ctypes.data)
+
+
+class Streamlines:
+    """R simulated ranks advecting particles on a sampled field (oracle/streamlines.c)."""
+
+    def __init__(self, R, cap, field: np.ndarray, grid):
+        self.R, self.grid = R, tuple(grid)
+        self.field = np.ascontiguousarray(field, dtype=np.float32)
+        self.nz, self.ny, self.nx = self.field.shape[:3]
+        self.w = World(R, cap, 16)
+
+    def _dims(self):
+        return (self.nx, self.ny, self.nz) + self.grid
+
+    def seed(self, r, seeds, id0):
+        seeds = np.ascontiguousarray(seeds, dtype=np.float32)
+        lib().orc_sl_seed(self.w._w, r, self.field.ctypes.data, *self._dims(), seeds.ctypes.data, seeds.shape[0], id0)
+
+    def step(self, rnd, h, eps, max_steps, rpos, rsteps):
+        assert rpos.dtype == np.float32 and rsteps.dtype == np.uint32
+        for r in range(self.R):
+            lib().orc_sl_step(self.w._w, r, self.field.ctypes.data, *self._dims(), rnd, h, eps, max_steps,
+                              rpos.ctypes.data, rsteps.ctypes.data)
+
+    def owner(self, p):
+        q = np.ascontiguousarray(p, dtype=np.float32)
+        return int(lib().orc_sl_owner(q.ctypes.data, *self._dims()))
 
 
 def morton_owner(x, y, z, R) -> int:

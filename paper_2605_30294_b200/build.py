@@ -90,6 +90,7 @@ def build(force: bool = False, verbose: bool = False, defines=None, out: str | N
 VARIANTS = {  # scatter tuning experiments: name -> defines (build with --variants)
     "ilp2": ["RAFI_SCATTER_ILP=2"],
     "ilp8": ["RAFI_SCATTER_ILP=8"],
+    "debug": ["RAFI_DEBUG_BOUNDS=1"],  # device-side bounds checks (scripts/sanitize_cases.py)
 }
 
 

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "internal.h"
 #include "rafi_device.cuh"
@@ -665,4 +666,213 @@ extern "C" int rafi_drv_nbody_respond(rafi_ctx* qctx, rafi_ctx* vctx, const unsi
       return rc;
   }
   return RAFI_OK;
+}
+
+// ------------------------------------------------------------------ streamlines (NEXT-4)
+// Particle advection on a sampled vector field: per-rank
+// field blocks with a one-vertex halo, trilinear sampling, RK4,
+// owner by macrocell.  + - * / only, no contraction.
+
+namespace {
+
+struct SGrid {
+  int nx, ny, nz, gx, gy, gz, mx, my, mz;  // vertices, macrocell grid, cells per macrocell
+};
+
+struct SBlock {
+  const float* v;  // local vertices (x fastest), float3 each
+  int lo[3];       // first stored vertex
+  int ld[3];       // stored vertices per axis
+};
+
+__device__ __forceinline__ int s_cell(float p, int n) {
+  int i = (int)(p * (float)(n - 1));
+  return i > n - 2 ? n - 2 : (i < 0 ? 0 : i);
+}
+
+__device__ __forceinline__ int s_owner(const SGrid& g, float x, float y, float z) {
+  return ((s_cell(z, g.nz) / g.mz) * g.gy + s_cell(y, g.ny) / g.my) * g.gx + s_cell(x, g.nx) / g.mx;
+}
+
+__device__ __forceinline__ bool s_in_closed(float x, float y, float z) {
+  return x >= 0.0f && x <= 1.0f && y >= 0.0f && y <= 1.0f && z >= 0.0f && z <= 1.0f;
+}
+
+// trilinear sample; false if the stage point left the domain or the block+halo
+__device__ bool s_sample(const SGrid& g, const SBlock& b, float x, float y, float z, float* out, int* halo_miss) {
+  if (!s_in_closed(x, y, z)) return false;
+  const float ux = x * (float)(g.nx - 1), uy = y * (float)(g.ny - 1), uz = z * (float)(g.nz - 1);
+  const int i = s_cell(x, g.nx), j = s_cell(y, g.ny), k = s_cell(z, g.nz);
+  const float fx = ux - (float)i, fy = uy - (float)j, fz = uz - (float)k;
+  const int li = i - b.lo[0], lj = j - b.lo[1], lk = k - b.lo[2];
+  if (li < 0 || lj < 0 || lk < 0 || li > b.ld[0] - 2 || lj > b.ld[1] - 2 || lk > b.ld[2] - 2) {
+    atomicAdd(halo_miss, 1);
+    return false;
+  }
+  const float gx0 = 1.0f - fx, gy0 = 1.0f - fy, gz0 = 1.0f - fz;
+  const int sx = 3, sy = 3 * b.ld[0], sz = 3 * b.ld[0] * b.ld[1];
+  const float* c = b.v + (size_t)lk * sz + (size_t)lj * sy + (size_t)li * sx;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const float c00 = c[a] * gx0 + c[sx + a] * fx;
+    const float c10 = c[sy + a] * gx0 + c[sy + sx + a] * fx;
+    const float c01 = c[sz + a] * gx0 + c[sz + sx + a] * fx;
+    const float c11 = c[sz + sy + a] * gx0 + c[sz + sy + sx + a] * fx;
+    const float c0 = c00 * gy0 + c10 * fy, c1 = c01 * gy0 + c11 * fy;
+    out[a] = c0 * gz0 + c1 * fz;
+  }
+  return true;
+}
+
+__global__ void k_stream_seed(rafi_device_view v, SGrid g, const float* seeds, uint64_t n, uint32_t id0) {
+  rafi::Queue<Particle> q(v);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    Particle p;
+    p.id = id0 + (uint32_t)i;
+    p.x = seeds[3 * i];
+    p.y = seeds[3 * i + 1];
+    p.z = seeds[3 * i + 2];
+    if (!inside(p.x, p.y, p.z)) continue;  // a seed outside the domain has an empty streamline
+    q.emitOutgoing(p, s_owner(g, p.x, p.y, p.z));
+  }
+}
+
+__global__ void k_stream_step(rafi_device_view v, SGrid g, SBlock b, uint32_t rnd, float h, float eps,
+                              uint32_t max_steps, float* rpos, uint32_t* rsteps, int* halo_miss) {
+  rafi::Queue<Particle> q(v);
+  const unsigned long long n = q.numIncoming();
+  const float hh = 0.5f * h, h6 = h / 6.0f;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    Particle p = q.getIncoming(i);
+    float k1[3], k2[3], k3[3], k4[3];
+    bool ok = s_sample(g, b, p.x, p.y, p.z, k1, halo_miss);
+    ok = ok && s_sample(g, b, p.x + hh * k1[0], p.y + hh * k1[1], p.z + hh * k1[2], k2, halo_miss);
+    ok = ok && s_sample(g, b, p.x + hh * k2[0], p.y + hh * k2[1], p.z + hh * k2[2], k3, halo_miss);
+    ok = ok && s_sample(g, b, p.x + h * k3[0], p.y + h * k3[1], p.z + h * k3[2], k4, halo_miss);
+    if (!ok) {  // a stage left the domain: terminated before this step
+      rpos[3 * p.id] = p.x; rpos[3 * p.id + 1] = p.y; rpos[3 * p.id + 2] = p.z;
+      rsteps[p.id] = rnd - 1;
+      continue;
+    }
+    const float nx = p.x + h6 * (((k1[0] + 2.0f * k2[0]) + 2.0f * k3[0]) + k4[0]);
+    const float ny = p.y + h6 * (((k1[1] + 2.0f * k2[1]) + 2.0f * k3[1]) + k4[1]);
+    const float nz = p.z + h6 * (((k1[2] + 2.0f * k2[2]) + 2.0f * k3[2]) + k4[2]);
+    const float dx = nx - p.x, dy = ny - p.y, dz = nz - p.z;
+    p.x = nx; p.y = ny; p.z = nz;
+    if (dx * dx + dy * dy + dz * dz < eps * eps || !inside(nx, ny, nz) || rnd >= max_steps) {
+      rpos[3 * p.id] = nx; rpos[3 * p.id + 1] = ny; rpos[3 * p.id + 2] = nz;
+      rsteps[p.id] = rnd;
+      continue;
+    }
+    q.emitOutgoing(p, s_owner(g, nx, ny, nz));
+  }
+}
+
+}  // namespace
+
+struct rafi_stream_field {
+  rafi_impl::Ctx* c = nullptr;
+  SGrid g{};
+  std::vector<SBlock> blocks;  // per local rank (device pointers)
+  int* halo_miss = nullptr;    // device counter
+};
+
+extern "C" int rafi_drv_stream_create(rafi_ctx* ctx, const float* field, int nx, int ny, int nz, int gx, int gy,
+                                      int gz, rafi_stream_field** out) {
+  auto* c = reinterpret_cast<rafi_impl::Ctx*>(ctx);
+  if (!c || !field || !out || nx < 2 || ny < 2 || nz < 2) return RAFI_ERR_INVALID_ARG;
+  if (c->B != sizeof(Particle)) return RAFI_ERR_INVALID_ARG;
+  int rc = check_grid(c, gx, gy, gz);
+  if (rc) return rc;
+  if ((nx - 1) % gx || (ny - 1) % gy || (nz - 1) % gz) {
+    rafi_impl::set_error("stream field: cells per axis must divide evenly into the macrocell grid");
+    return RAFI_ERR_INVALID_ARG;
+  }
+  if (cudaSetDevice(c->device) != cudaSuccess) return RAFI_ERR_CUDA;
+  auto* f = new rafi_stream_field();
+  f->c = c;
+  f->g = SGrid{nx, ny, nz, gx, gy, gz, (nx - 1) / gx, (ny - 1) / gy, (nz - 1) / gz};
+  const int n[3] = {nx, ny, nz}, m[3] = {f->g.mx, f->g.my, f->g.mz};
+  for (int l = 0; l < c->L; ++l) {
+    const int r = c->proc * c->L + l;
+    const int cc[3] = {r % gx, (r / gx) % gy, r / (gx * gy)};
+    SBlock b{};
+    for (int a = 0; a < 3; ++a) {
+      b.lo[a] = cc[a] * m[a] - 1 < 0 ? 0 : cc[a] * m[a] - 1;
+      const int hi = (cc[a] + 1) * m[a] + 1 > n[a] - 1 ? n[a] - 1 : (cc[a] + 1) * m[a] + 1;
+      b.ld[a] = hi - b.lo[a] + 1;
+    }
+    std::vector<float> host((size_t)b.ld[0] * b.ld[1] * b.ld[2] * 3);
+    for (int k = 0; k < b.ld[2]; ++k)
+      for (int j = 0; j < b.ld[1]; ++j)
+        for (int i = 0; i < b.ld[0]; ++i)
+          for (int a = 0; a < 3; ++a)
+            host[(((size_t)k * b.ld[1] + j) * b.ld[0] + i) * 3 + a] =
+                field[((((size_t)(k + b.lo[2]) * ny) + (j + b.lo[1])) * nx + (i + b.lo[0])) * 3 + a];
+    float* d = nullptr;
+    if (cudaMalloc(&d, host.size() * sizeof(float)) != cudaSuccess ||
+        cudaMemcpy(d, host.data(), host.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaGetLastError();
+      rafi_drv_stream_destroy(f);
+      return RAFI_ERR_CUDA;
+    }
+    b.v = d;
+    f->blocks.push_back(b);
+  }
+  if (cudaMalloc(&f->halo_miss, sizeof(int)) != cudaSuccess || cudaMemset(f->halo_miss, 0, sizeof(int)) != cudaSuccess) {
+    cudaGetLastError();
+    rafi_drv_stream_destroy(f);
+    return RAFI_ERR_CUDA;
+  }
+  *out = f;
+  return RAFI_OK;
+}
+
+extern "C" int rafi_drv_stream_seed(rafi_stream_field* f, int local, const float* seeds, uint64_t n, uint32_t id0) {
+  if (!f || local < 0 || local >= f->c->L || (n && !seeds)) return RAFI_ERR_INVALID_ARG;
+  if (!n) return RAFI_OK;
+  rafi_device_view v;
+  int rc = rafi_get_device_view(reinterpret_cast<rafi_ctx*>(f->c), local, &v);
+  if (rc) return rc;
+  float* d = nullptr;
+  if (cudaMalloc(&d, 3 * n * sizeof(float)) != cudaSuccess) { cudaGetLastError(); return RAFI_ERR_NOMEM; }
+  if (cudaMemcpyAsync(d, seeds, 3 * n * sizeof(float), cudaMemcpyDefault, f->c->stream) != cudaSuccess) {
+    cudaGetLastError(); cudaFree(d); return RAFI_ERR_CUDA;
+  }
+  rc = launch_grid(f->c, n, k_stream_seed, v, f->g, (const float*)d, n, id0);
+  cudaStreamSynchronize(f->c->stream);
+  cudaFree(d);
+  return rc;
+}
+
+extern "C" int rafi_drv_stream_step(rafi_stream_field* f, uint32_t rnd, float h, float eps, uint32_t max_steps,
+                                    float* rpos, uint32_t* rsteps) {
+  if (!f || !rpos || !rsteps) return RAFI_ERR_INVALID_ARG;
+  auto* c = f->c;
+  if (cudaSetDevice(c->device) != cudaSuccess) return RAFI_ERR_CUDA;
+  for (int l = 0; l < c->L; ++l) {
+    rafi_device_view v;
+    int rc = rafi_get_device_view(reinterpret_cast<rafi_ctx*>(c), l, &v);
+    if (rc) return rc;
+    if ((rc = launch_grid(c, launch_count(c, v), k_stream_step, v, f->g, f->blocks[l], rnd, h, eps, max_steps, rpos,
+                          rsteps, f->halo_miss)))
+      return rc;
+  }
+  return RAFI_OK;
+}
+
+extern "C" int rafi_drv_stream_destroy(rafi_stream_field* f) {
+  if (!f) return RAFI_OK;
+  cudaSetDevice(f->c->device);
+  cudaStreamSynchronize(f->c->stream);
+  for (auto& b : f->blocks) cudaFree(const_cast<float*>(b.v));
+  cudaFree(f->halo_miss);
+  delete f;
+  return RAFI_OK;
+}
+
+extern "C" int rafi_drv_stream_halo_misses(rafi_stream_field* f, int* count) {
+  if (!f || !count) return RAFI_ERR_INVALID_ARG;
+  cudaStreamSynchronize(f->c->stream);
+  return cudaMemcpy(count, f->halo_miss, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess ? RAFI_OK : RAFI_ERR_CUDA;
 }

@@ -33,6 +33,23 @@ namespace rafi_impl {
 #define RAFI_SCATTER_ILP 4
 #endif
 
+// Debug builds (build.py --variants "debug"): device-side bounds checks that
+// trap with a message (compute-sanitizer is not available on the GPU pool).
+#ifdef RAFI_DEBUG_BOUNDS
+#define RAFI_DCHECK(cond, what)                                                        \
+  do {                                                                                 \
+    if (!(cond)) {                                                                     \
+      printf("RAFI_DCHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                        \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define RAFI_DCHECK(cond, what) \
+  do {                          \
+  } while (0)
+#endif
+
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxK = 16;          // items per thread per tile (tile <= 4096)
@@ -240,7 +257,10 @@ k_hist(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, int R, 
     uint32_t acc = 0;
     for (int ti = 0; ti < kHistTilesPerCta; ++ti) {
       const uint64_t t = tb + ti;
-      if (t < tiles) O[(uint64_t)d * tiles + t] = acc;
+      if (t < tiles) {
+        RAFI_DCHECK((uint64_t)d * tiles + t < (uint64_t)R * ((cap + T - 1) / T), "O index");
+        O[(uint64_t)d * tiles + t] = acc;
+      }
       acc += tc[ti * R + d];
     }
     rk[l].H[(uint64_t)d * nblk + blockIdx.x] = acc;
@@ -571,8 +591,11 @@ k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint
     }
     // per-run destination base, shifted so that position p of run d lands at
     // base_d + p*B (runs are contiguous in both the tile order and the output)
-    for (int d = tid; d < R; d += kThreads)
+    for (int d = tid; d < R; d += kThreads) {
+      RAFI_DCHECK((uint64_t)rstart[d] + ((d + 1 < R ? tcnt[d + 1] : nt) - tcnt[d]) <= cap,
+                  "destination run beyond the destination queue");
       dbase[d] += (uintptr_t)(((int64_t)rstart[d] - (int64_t)tcnt[d]) * (int64_t)B);
+    }
     __syncthreads();
     // phase 4: coalesced write of every destination run
     const U* srcU = kStageItems ? reinterpret_cast<const U*>(st) : reinterpret_cast<const U*>(rk[l].out + t0 * B);
@@ -606,7 +629,12 @@ k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint
         }
 #pragma unroll
         for (int j = 0; j < kU; ++j)
-          if (x0 + j * kThreads < units) dd[j][(uint64_t)p[j] * UPI + u[j]] = v[j];
+          if (x0 + j * kThreads < units) {
+            RAFI_DCHECK((uintptr_t)&dd[j][(uint64_t)p[j] * UPI + u[j]] >=
+                            (uintptr_t)(dst_table ? dst_table[0] : rk[l].binned[cur]) ||
+                            dst_table, "scatter store below the send batch");
+            dd[j][(uint64_t)p[j] * UPI + u[j]] = v[j];
+          }
       }
     } else {
       int d = 0;

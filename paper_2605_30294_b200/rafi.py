@@ -113,6 +113,13 @@ SIGNATURES = {
     "rafi_drv_nbody_root": (C.c_int, [C.c_void_p, C.c_void_p]),
     "rafi_drv_nbody_refine": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_float]),
     "rafi_drv_nbody_respond": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "rafi_drv_stream_create": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                         C.c_int, C.POINTER(C.c_void_p)]),
+    "rafi_drv_stream_seed": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_uint32]),
+    "rafi_drv_stream_step": (C.c_int, [C.c_void_p, C.c_uint32, C.c_float, C.c_float, C.c_uint32, C.c_void_p,
+                                       C.c_void_p]),
+    "rafi_drv_stream_destroy": (C.c_int, [C.c_void_p]),
+    "rafi_drv_stream_halo_misses": (C.c_int, [C.c_void_p, C.POINTER(C.c_int)]),
     "rafi_forward_async": (C.c_int, [C.c_void_p, C.c_void_p]),
     "rafi_sync_host": (C.c_int, [C.c_void_p]),
     "rafi_capture_begin": (C.c_int, [C.c_void_p]),
@@ -206,6 +213,44 @@ def plan(C_matrix: np.ndarray, capacity: int, d: int):
                            C.byref(tot), C.byref(G), C.byref(ovf)), "rafi_plan")
     return {"recv_count": rc_, "recv_off": ro, "src_off": so, "total": tot.value, "G": G.value,
             "overflow": bool(ovf.value)}
+
+
+class StreamField:
+    """Streamline proxy state (include/rafi_drivers.h, NEXT-4): per-rank field
+    blocks with a one-vertex halo on the device."""
+
+    def __init__(self, ctx: "Context", field: np.ndarray, grid):
+        field = np.ascontiguousarray(field, dtype=np.float32)
+        nz, ny, nx, three = field.shape
+        assert three == 3
+        h = C.c_void_p()
+        _check(lib().rafi_drv_stream_create(ctx.handle, field.ctypes.data, nx, ny, nz, *grid, C.byref(h)),
+               "rafi_drv_stream_create")
+        self._h = h.value
+
+    def seed(self, seeds: np.ndarray, id0: int, local: int = 0):
+        seeds = np.ascontiguousarray(seeds, dtype=np.float32)
+        _check(lib().rafi_drv_stream_seed(self._h, local, seeds.ctypes.data, seeds.shape[0], id0), "rafi_drv_stream_seed")
+
+    def step(self, rnd, h, eps, max_steps, result_pos, result_steps):
+        _check(lib().rafi_drv_stream_step(self._h, rnd, h, eps, max_steps, _ptr(result_pos), _ptr(result_steps)),
+               "rafi_drv_stream_step")
+
+    def halo_misses(self) -> int:
+        v = C.c_int()
+        _check(lib().rafi_drv_stream_halo_misses(self._h, C.byref(v)), "rafi_drv_stream_halo_misses")
+        return v.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().rafi_drv_stream_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Context:
