@@ -47,6 +47,7 @@ def parse():
     p.add_argument("--item-bytes", type=int, default=DEF_B)
     p.add_argument("--pattern", default="uniform")
     p.add_argument("--exchange", default="auto", choices=["auto", "nccl", "peer", "fused"])
+    p.add_argument("--scatter", default="auto", choices=["auto", "threads", "bulk", "aligned"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle cpu_baseline sample")
@@ -240,6 +241,11 @@ def main():
         ctx.set_option(rafi.OPT_EXCHANGE, {"nccl": rafi.EXCHANGE_NCCL, "peer": rafi.EXCHANGE_PEER,
                                            "fused": rafi.EXCHANGE_FUSED}[args.exchange])
     exchange = {1: "nccl", 2: "peer", 3: "fused"}[ctx.get_option(rafi.OPT_EXCHANGE)]
+    if args.scatter != "auto":
+        ctx.set_option(rafi.OPT_SCATTER, {"threads": rafi.SCATTER_THREADS, "bulk": rafi.SCATTER_BULK,
+                                          "aligned": rafi.SCATTER_ALIGNED}[args.scatter])
+    scatter = {1: "threads", 2: "bulk", 3: "aligned"}[ctx.get_option(rafi.OPT_SCATTER)]
+    ctx_tile = ctx.get_option(rafi.OPT_TILE)
 
     # resident inputs (generated on the host by the shared generator, uploaded once)
     items_h = synth.make_items(rank, 0, n, max(B, 16))[:, :B].copy()
@@ -385,7 +391,7 @@ def main():
         "data": "synthetic (synth/ SplitMix64 recipe; resident in HBM)", "config": workload_config(args, N),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clk, "phases_ms": ph, "kernels": kern, "exchange": exch, "exchange_transport": exchange,
-        "per_gpu_items_per_s": value / N,
+        "scatter_write": scatter, "tile": ctx_tile, "per_gpu_items_per_s": value / N,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

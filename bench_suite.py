@@ -50,9 +50,20 @@ class Env:
         (self.torch, self.dist, self.rafi, self.world, self.rank, self.local, self.dev,
          self.comm) = setup(args)
         self.stream = self.torch.cuda.current_stream()
+        self.scatter = {"auto": 0, "threads": 1, "bulk": 2, "aligned": 3}[getattr(args, "scatter", "auto")]
+        self.tile = getattr(args, "tile", 0)
+
+    def configure(self, ctx):
+        """Apply the --scatter choice (RAFI_OPT_SCATTER) to a new context."""
+        if self.scatter:
+            ctx.set_option(self.rafi.OPT_SCATTER, self.scatter)
+        if self.tile:
+            ctx.set_option(self.rafi.OPT_TILE, self.tile)
+        return ctx
 
     def ctx(self, B, cap, L=1):
-        return self.rafi.Context(B, cap, comm=self.comm, stream=self.stream, local_ranks=L, device=self.local)
+        return self.configure(self.rafi.Context(B, cap, comm=self.comm, stream=self.stream, local_ranks=L,
+                                                device=self.local))
 
     def sync(self):
         self.torch.cuda.synchronize()
@@ -326,7 +337,7 @@ def fwd_rate(env, B, n, steps=5, warmup=2, pattern="uniform", graph=False):
     ds = synth.make_dests(pattern, synth.CONFIG_SEEDS[5], env.rank, 0, n, N)
     dests = torch.from_numpy(ds).to(env.dev)
     side = torch.cuda.Stream(device=env.dev)
-    ctx = env.rafi.Context(B, n + n // 8 + 4096, comm=env.comm, stream=side, device=env.local)
+    ctx = env.configure(env.rafi.Context(B, n + n // 8 + 4096, comm=env.comm, stream=side, device=env.local))
     saved, env.stream = env.stream, side
     for _ in range(warmup):
         ctx.emit_bulk(items, dests, n)
@@ -344,7 +355,8 @@ def fwd_rate(env, B, n, steps=5, warmup=2, pattern="uniform", graph=False):
     remote = st["bytes_sent_remote"]
     out = {"items_per_rank": n, "item_bytes": B, "ms_per_step": ms / steps,
            "value": N * n * steps / (ms / 1e3), "unit": "items/s",
-           "scatter_ms": scat, "scatter_hbm_gbs": n * (2 * B + 4) / (scat / 1e3) / 1e9,
+           "scatter": {1: "threads", 2: "bulk", 3: "aligned"}[ctx.get_option(env.rafi.OPT_SCATTER)],
+           "tile": ctx.get_option(env.rafi.OPT_TILE), "scatter_ms": scat, "scatter_hbm_gbs": n * (2 * B + 4) / (scat / 1e3) / 1e9,
            "nvlink_gbs_per_gpu": (remote / (scat / 1e3) / 1e9) if N > 1 else None}
     if graph:
         ctx.set_option(env.rafi.OPT_TIMING, 0)
@@ -372,8 +384,13 @@ def fwd_rate(env, B, n, steps=5, warmup=2, pattern="uniform", graph=False):
 
 def run_cfg5(env, args):
     n = args.items or 32 * 1024 * 1024
-    for B in (16, 24, 32, 40, 44, 48, 64, 96, 128):
-        r = fwd_rate(env, B, n)
+    sizes = [int(x) for x in args.sizes.split(",")] if args.sizes else [16, 24, 32, 40, 44, 48, 64, 96, 128]
+    for B in sizes:
+        try:
+            r = fwd_rate(env, B, n)
+        except env.rafi.RafiError as e:  # e.g. a --tile that does not fit this item size
+            env.emit({"item_bytes": B, "skipped": str(e)})
+            continue
         r["workload"] = "cfg5: uniform all-to-all over R=%d, %d items/rank, %d-B items" % (env.world, n, B)
         env.emit(r)
 
@@ -390,6 +407,9 @@ def main():
     p.add_argument("workload", choices=["cfg1", "cfg3", "cfg4", "cfg5", "sweep", "latency", "nbody", "streamlines"])
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--items", type=int, default=0)
+    p.add_argument("--scatter", default="auto", choices=["auto", "threads", "bulk", "aligned"])
+    p.add_argument("--tile", type=int, default=0, help="RAFI_OPT_TILE (0 = automatic)")
+    p.add_argument("--sizes", default="", help="cfg5: comma-separated item sizes (default: the full sweep)")
     args = p.parse_args()
     env = Env(args)
     {"cfg1": run_cfg1, "cfg3": run_cfg3, "cfg4": run_cfg4, "cfg5": run_cfg5, "sweep": run_sweep,

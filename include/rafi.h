@@ -115,6 +115,20 @@ typedef struct {
                                       accumulated sums in rafi_stats; default 0 */
 #define RAFI_OPT_TILE 3            /* binning tile in items (256 * 2^k, k <= 4); 0 = auto from item size */
 #define RAFI_OPT_SELF_DIRECT 4     /* reserved (self run placement); 0 */
+#define RAFI_OPT_SCATTER 5         /* how the binning scatter writes destination runs:
+                                      RAFI_SCATTER_* (default AUTO).  Same result bytes either way.
+                                      Only between rounds; re-chooses the tile unless RAFI_OPT_TILE
+                                      pinned it.  RAFI_ERR_UNSUPPORTED if BULK/ALIGNED is asked for an
+                                      item size that is not a multiple of 4 or a tile that does not fit */
+
+#define RAFI_SCATTER_AUTO 0        /* BULK when supported, else THREADS */
+#define RAFI_SCATTER_THREADS 1     /* threads store every unit of every run (16/8/4/2/1-B coalesced stores) */
+#define RAFI_SCATTER_BULK 2        /* runs are permuted in shared memory and written by TMA bulk stores
+                                      (cp.async.bulk shared->global, local or NVLink peer); threads write
+                                      only the unaligned < 16-B heads and tails; item_bytes % 4 == 0 */
+#define RAFI_SCATTER_ALIGNED 3     /* runs are permuted in shared memory, placed congruent to their global
+                                      address mod 16, and written by threads as 16-B-aligned vector
+                                      stores whatever the item size; item_bytes % 4 == 0 */
 
 #define RAFI_EXCHANGE_AUTO 0       /* FUSED when every rank's queues are addressable, else NCCL */
 #define RAFI_EXCHANGE_NCCL 1       /* stage the sorted batch, grouped ncclSend/ncclRecv (one local rank per process) */

@@ -176,6 +176,41 @@ static int resolve_exchange(Ctx* c) {
   return RAFI_OK;
 }
 
+// Effective scatter write path (RAFI_OPT_SCATTER).
+static constexpr size_t kMaxSmem = 227u * 1024u;  // opt-in shared memory per CTA on sm_100a
+static bool is_perm(int mode) { return mode == RAFI_SCATTER_BULK || mode == RAFI_SCATTER_ALIGNED; }
+
+static int resolve_scatter(Ctx* c) {
+  int x = c->scatter;
+  if (x == RAFI_SCATTER_AUTO) x = RAFI_SCATTER_THREADS;
+  if (is_perm(x) && !(perm_supported(c->B) && perm_smem_bytes(x, 256, c->B, c->R) <= kMaxSmem)) {
+    set_error("permuting scatter needs item_bytes % 4 == 0 and a 256-item tile that fits in shared memory");
+    return RAFI_ERR_UNSUPPORTED;
+  }
+  c->scatter_eff = x;
+  return RAFI_OK;
+}
+
+static uint32_t auto_tile(const Ctx* c) {
+  return is_perm(c->scatter_eff) ? choose_tile_perm(c->scatter_eff, c->B, c->R) : choose_tile(c->B);
+}
+
+// Binning tile (between rounds); grows H/O when the tile count grows.
+static int set_tile(Ctx* c, uint32_t t) {
+  if ((uint64_t)(c->cap + t - 1) / t > c->max_tiles) {
+    for (auto& r : c->lr) {
+      cudaFree(r.H); cudaFree(r.O); r.H = r.O = nullptr;
+      const size_t hb = (size_t)((c->cap + t - 1) / t) * c->R * 4 + kPad;
+      RAFI_CK(alloc_dev((void**)&r.H, hb));
+      RAFI_CK(alloc_dev((void**)&r.O, hb));
+    }
+    c->max_tiles = (c->cap + t - 1) / t;
+    RAFI_CK(upload_rank_table(c));
+  }
+  c->tile = t;
+  return RAFI_OK;
+}
+
 static int alloc_all(Ctx* c) {
   c->max_tiles = (c->cap + c->tile - 1) / c->tile;
   c->lr.assign(c->L, LocalRank{});
@@ -243,7 +278,8 @@ static int create(Ctx** out, const rafi_create_params* p) {
   c->R = c->nprocs * c->L;
   c->B = p->item_bytes;
   c->cap = p->capacity;
-  c->tile = choose_tile(c->B);
+  if ((rc = resolve_scatter(c))) return fail(rc);
+  c->tile = auto_tile(c);
   if ((rc = alloc_dev((void**)&c->rank_dev, sizeof(RankDev) * c->L))) return fail(rc);
   if ((rc = alloc_dev((void**)&c->ctrl, ctrl_c_bytes(c)))) return fail(rc);
   c->Cdev = reinterpret_cast<uint64_t*>(c->ctrl + c->L);  // count matrix right after the control blocks
@@ -933,19 +969,22 @@ int rafi_set_option(rafi_ctx* ctx, int key, long long v) {
     case RAFI_OPT_TILE: {
       // only between rounds with an empty outgoing queue; re-sizes H/O
       if (v != 0 && (v < 256 || v > 4096 || (v & (v - 1)) != 0)) return RAFI_ERR_INVALID_ARG;  // 256 * 2^k
-      const uint32_t t = v ? (uint32_t)v : choose_tile(c->B);
-      if ((uint64_t)(c->cap + t - 1) / t > c->max_tiles) {
-        // need larger H/O
-        for (auto& r : c->lr) {
-          cudaFree(r.H); cudaFree(r.O); r.H = r.O = nullptr;
-          const size_t hb = (size_t)((c->cap + t - 1) / t) * c->R * 4 + kPad;
-          RAFI_CK(alloc_dev((void**)&r.H, hb));
-          RAFI_CK(alloc_dev((void**)&r.O, hb));
-        }
-        c->max_tiles = (c->cap + t - 1) / t;
-              RAFI_CK(upload_rank_table(c));
+      const uint32_t t = v ? (uint32_t)v : auto_tile(c);
+      if (is_perm(c->scatter_eff) && perm_smem_bytes(c->scatter_eff, t, c->B, c->R) > kMaxSmem) {
+        set_error("tile too large for the permuting scatter's shared memory");
+        return RAFI_ERR_UNSUPPORTED;
       }
-      c->tile = t;
+      RAFI_CK(set_tile(c, t));
+      c->tile_user = v != 0;
+      return RAFI_OK;
+    }
+    case RAFI_OPT_SCATTER: {
+      if (v < RAFI_SCATTER_AUTO || v > RAFI_SCATTER_ALIGNED) return RAFI_ERR_INVALID_ARG;
+      const int old = c->scatter;
+      c->scatter = (int)v;
+      int rc = resolve_scatter(c);
+      if (rc != RAFI_OK) { c->scatter = old; resolve_scatter(c); return rc; }
+      if (!c->tile_user) RAFI_CK(set_tile(c, auto_tile(c)));
       return RAFI_OK;
     }
     case RAFI_OPT_SELF_DIRECT: return v == 0 ? RAFI_OK : RAFI_ERR_UNSUPPORTED;
@@ -960,6 +999,7 @@ int rafi_get_option(const rafi_ctx* ctx, int key, long long* v) {
     case RAFI_OPT_EXCHANGE: *v = c->exchange_eff; return RAFI_OK;
     case RAFI_OPT_TIMING: *v = c->timing; return RAFI_OK;
     case RAFI_OPT_TILE: *v = c->tile; return RAFI_OK;
+    case RAFI_OPT_SCATTER: *v = c->scatter_eff; return RAFI_OK;
     case RAFI_OPT_SELF_DIRECT: *v = 0; return RAFI_OK;
     default: return RAFI_ERR_INVALID_ARG;
   }

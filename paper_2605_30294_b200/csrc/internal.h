@@ -92,6 +92,9 @@ struct Ctx {
   uint64_t max_tiles = 0;     // ceil(cap / tile)
   int exchange = RAFI_EXCHANGE_AUTO;
   int exchange_eff = RAFI_EXCHANGE_FUSED;
+  int scatter = RAFI_SCATTER_AUTO;     // requested scatter write path (RAFI_OPT_SCATTER)
+  int scatter_eff = RAFI_SCATTER_THREADS;
+  bool tile_user = false;              // RAFI_OPT_TILE pinned the tile
   bool timing = false;
   bool broken = false;
   uint64_t round = 0;
@@ -152,6 +155,9 @@ inline size_t ctrl_c_bytes(const Ctx* c) { return sizeof(CtrlDev) * c->L + sizeo
 
 // kernels.cu
 uint32_t choose_tile(uint64_t item_bytes);
+uint32_t choose_tile_perm(int mode, uint64_t item_bytes, int R);
+bool perm_supported(uint64_t item_bytes);
+size_t perm_smem_bytes(int mode, uint32_t tile, uint64_t item_bytes, int R);
 int launch_emit_bulk(Ctx* c, int local, const uint8_t* items, const int32_t* dests, uint64_t n);
 int launch_hist(Ctx* c);
 int launch_scan(Ctx* c, int plan_mode, unsigned long long* G_out = nullptr);

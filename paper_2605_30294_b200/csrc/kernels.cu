@@ -469,6 +469,30 @@ __host__ __device__ inline ScatterLayout scatter_layout(uint32_t T, uint64_t B, 
   return s;
 }
 
+// Phase 1 of both scatter kernels: warp w ranks items w*32*kK .. +32*kK-1 of
+// the tile (slot order).  dk[k] = destination of item w*32*kK + 32k + lane
+// (R past the tile end), rk_[k] = its rank among the warp's earlier items
+// with the same destination (stability); wcnt[w][d] ends as
+// the warp's count of destination d (zeroed by the caller).
+template <int kK>
+__device__ __forceinline__ void rank_chunk(const int32_t* __restrict__ dest_s, uint32_t nt, int R,
+                                           uint32_t* __restrict__ wcnt, int (&dk)[kK], uint32_t (&rk_)[kK]) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < kK; ++k) {
+    const uint32_t il = w * 32 * kK + k * 32 + lane;
+    const int d = il < nt ? dest_s[il] : R;
+    const unsigned m = __match_any_sync(kFull, d);
+    uint32_t c = 0;
+    if (d < R) c = wcnt[w * R + d];
+    __syncwarp();
+    if (d < R && lane == __ffs(m) - 1) wcnt[w * R + d] = c + __popc(m);
+    __syncwarp();
+    dk[k] = d;
+    rk_[k] = c + __popc(m & lanemask_lt());
+  }
+}
+
 // Stable scatter of each tile into one contiguous run per destination.
 //   * Tile loads (items + dests) are 1-D TMA bulk copies into a two-stage
 //     shared-memory ring guarded by mbarriers: tile i+1 (and i+2) stream in
@@ -551,21 +575,7 @@ k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint
     // phase 1: stable rank among same-destination items of the warp's chunk
     int dk[kK];
     uint32_t rk_[kK];
-#pragma unroll
-    for (int k = 0; k < kK; ++k) {
-      {
-        const uint32_t il = w * 32 * K + k * 32 + lane;
-        const int d = il < nt ? dest_s[il] : R;
-        const unsigned m = __match_any_sync(kFull, d);
-        uint32_t c = 0;
-        if (d < R) c = wcnt[w * R + d];
-        __syncwarp();
-        if (d < R && lane == __ffs(m) - 1) wcnt[w * R + d] = c + __popc(m);
-        __syncwarp();
-        dk[k] = d;
-        rk_[k] = c + __popc(m & lanemask_lt());
-      }
-    }
+    rank_chunk<kK>(dest_s, nt, R, wcnt, dk, rk_);
     __syncthreads();
     // phase 2: warp bases per destination; tile-local run starts
     for (int d = tid; d < R; d += kThreads) {
@@ -655,6 +665,270 @@ k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint
   if (dst_table) __threadfence_system();  // pushes to peer memory complete before the kernel does
   // wrap-up epilogue by the last block: every block has finished
   // reading the emit counters, so they can be reset for the next round
+  if (wrap_done && last_block(wrap_done)) {
+    for (int l2 = threadIdx.x; l2 < L; l2 += blockDim.x) {
+      ctrl_w[l2].ctr = 0;
+      ctrl_w[l2].invalid = 0;
+      ctrl_w[l2].num_in = wrap_num_in[l2];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- a4 scatter, bulk-store variant
+
+// 1-D bulk copy shared -> global through the TMA unit (UBLKCP.G.S), tracked in
+// the issuing thread's bulk async-group.  dst may be a CUDA-IPC peer mapping.
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// Shared-memory layout of k_scatter_perm (host mirror: bulk_layout()).
+struct BulkLayout {
+  uint32_t stage_items;   // bytes of one stage's items, 16-aligned
+  uint32_t stage_stride;  // items + dests, 128-aligned
+  uint32_t obuf_stride;   // one destination-major output tile: T*B + alignment slack per run
+  uint32_t nobuf;         // output tiles: 2 (store of tile i overlaps tile i+1) or 1 (large items)
+  uint32_t off_obuf, off_mbar, off_wcnt, off_wbase, off_tcnt, off_ooff, off_dbase, total;
+};
+
+__host__ __device__ inline BulkLayout bulk_layout(uint32_t T, uint64_t B, int R, uint32_t nobuf) {
+  BulkLayout s;
+  s.nobuf = nobuf;
+  auto al = [](uint64_t x, uint64_t a) { return (uint32_t)((x + a - 1) / a * a); };
+  s.stage_items = al((uint64_t)T * B, 16);
+  s.stage_stride = al((uint64_t)s.stage_items + 4ull * T, 128);
+  s.obuf_stride = al((uint64_t)T * B + 32ull * R + 16, 128);  // <= 30 B of slack per run
+  uint32_t o = 2 * s.stage_stride;
+  s.off_obuf = o; o += nobuf * s.obuf_stride;
+  s.off_mbar = o; o += 16;
+  s.off_wcnt = o; o += 4 * kWarps * R;
+  s.off_wbase = o; o += 4 * kWarps * R;
+  s.off_tcnt = o; o += 4 * R;
+  s.off_ooff = o; o = al(o + 4ull * R, 8);
+  s.off_dbase = o; o += 8 * R;
+  s.total = al(o, 16);
+  return s;
+}
+
+// Same result as k_scatter (every item read once, written once,
+// destination-major and stable in slot order), different data movement:
+//   * tile loads: TMA bulk copies into a two-stage mbarrier ring (as k_scatter);
+//   * ranking: rank_chunk (as k_scatter);
+//   * permutation: each thread moves its own items (consecutive items, so
+//     conflict-free reads) into a destination-major output tile in shared
+//     memory.  Run d starts at an offset congruent to its global byte address
+//     modulo 16, so the body of every run is one 16-byte-aligned span on both
+//     sides whatever the item size;
+//   * stores, kTma (RAFI_SCATTER_BULK): one elected thread issues a TMA bulk
+//     store (cp.async.bulk shared -> global) per run body, straight into the
+//     destination queue (the local send batch, the local incoming queue, or a
+//     peer's incoming queue over NVLink under FUSED), double-buffered output
+//     tiles when they fit; threads write the unaligned heads and tails (< 16 B);
+//   * stores, !kTma (RAFI_SCATTER_ALIGNED): all threads write the output tile
+//     as consecutive 16-byte-aligned vector stores (4 in flight per thread),
+//     so a 44-B item costs 2.75 vector stores instead of 11 word stores.
+// The stage is released to the next TMA load as soon as it is permuted.
+template <typename U, int kK, int kMinB, bool kTma>
+__global__ void __launch_bounds__(kThreads, kMinB)
+k_scatter_perm(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint8_t* const* __restrict__ dst_table,
+               const uint64_t* __restrict__ dst_off, const int* __restrict__ ovf, int L, int R, uint64_t cap, uint32_t T,
+               int cur, uint32_t B, uint32_t UPI, BulkLayout lay, unsigned* __restrict__ wrap_done,
+               CtrlDev* __restrict__ ctrl_w, const uint64_t* __restrict__ wrap_num_in) {
+  if (ovf && *ovf) return;  // collective receive overflow: move nothing (Z3)
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + lay.off_mbar);
+  uint32_t* wcnt = reinterpret_cast<uint32_t*>(smem + lay.off_wcnt);
+  uint32_t* wbase = reinterpret_cast<uint32_t*>(smem + lay.off_wbase);
+  uint32_t* tcnt = reinterpret_cast<uint32_t*>(smem + lay.off_tcnt);
+  uint32_t* ooff = reinterpret_cast<uint32_t*>(smem + lay.off_ooff);
+  uintptr_t* dbase = reinterpret_cast<uintptr_t*>(smem + lay.off_dbase);
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+
+  auto issue = [&](uint32_t it) {  // thread 0: start loading iteration it's tile into stage it&1
+    const uint64_t g = blockIdx.x + (uint64_t)it * gridDim.x;
+    int l;
+    uint64_t t, n, tiles;
+    if (!tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) return;
+    const uint64_t t0 = t * T;
+    const uint32_t nt = (uint32_t)umin64(T, n - t0);
+    uint8_t* st = smem + (it & 1) * lay.stage_stride;
+    const uint32_t bi = (nt * B + 15) & ~15u;
+    const uint32_t bd = (nt * 4 + 15) & ~15u;
+    mbar_expect_tx(&mbar[it & 1], bi + bd);
+    bulk_g2s(st, rk[l].out + t0 * B, bi, &mbar[it & 1]);
+    bulk_g2s(st + lay.stage_items, rk[l].dest + t0, bd, &mbar[it & 1]);
+  };
+
+  // byte address of item 0 of destination d's run of iteration it's tile:
+  // destination base + (tile prefix O + block prefix H + per-destination
+  // base) * B; 0 past the last tile
+  auto run_addr = [&](uint32_t it, int d) -> uintptr_t {
+    const uint64_t g = blockIdx.x + (uint64_t)it * gridDim.x;
+    int l;
+    uint64_t t, n, tiles;
+    if (!tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) return 0;
+    const uint64_t nblk = (tiles + kHistTilesPerCta - 1) / kHistTilesPerCta;
+    const uint64_t first = (uint64_t)rk[l].O[(uint64_t)d * tiles + t] +
+                           rk[l].H[(uint64_t)d * nblk + t / kHistTilesPerCta] + dst_off[(uint64_t)l * R + d];
+    return (uintptr_t)(dst_table ? dst_table[d] : rk[l].binned[cur]) + (uintptr_t)(first * B);
+  };
+
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) { issue(0); issue(1); }
+  uintptr_t pf_addr = (R <= kThreads && tid < R) ? run_addr(0, tid) : 0;
+
+  for (uint32_t it = 0;; ++it) {
+    const uint64_t g = blockIdx.x + (uint64_t)it * gridDim.x;
+    int l;
+    uint64_t t, n, tiles;
+    if (!tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) break;
+    const uint64_t t0 = t * T;
+    const uint32_t nt = (uint32_t)umin64(T, n - t0);
+    const uint8_t* st = smem + (it & 1) * lay.stage_stride;
+    uint8_t* ob = smem + lay.off_obuf + (lay.nobuf == 2 ? (it & 1) : 0u) * lay.obuf_stride;
+    const int32_t* dest_s = reinterpret_cast<const int32_t*>(st + lay.stage_items);
+    for (int x = tid; x < kWarps * R; x += kThreads) wcnt[x] = 0;
+    if (R <= kThreads) {  // the addresses were loaded one tile ahead
+      if (tid < R) {
+        dbase[tid] = pf_addr;
+        pf_addr = run_addr(it + 1, tid);
+      }
+    } else {
+      for (int d = tid; d < R; d += kThreads) dbase[d] = run_addr(it, d);
+    }
+    mbar_wait(&mbar[it & 1], (it >> 1) & 1);
+    __syncthreads();
+    int dk[kK];
+    uint32_t rk_[kK];
+    rank_chunk<kK>(dest_s, nt, R, wcnt, dk, rk_);
+    __syncthreads();
+    // warp bases per destination, tile count per destination
+    for (int d = tid; d < R; d += kThreads) {
+      uint32_t run = 0;
+      for (int i = 0; i < kWarps; ++i) { wbase[i * R + d] = run; run += wcnt[i * R + d]; }
+      tcnt[d] = run;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      // output-tile offsets: run d at the next offset congruent to its global
+      // address mod 16 (tcnt stays the per-destination count)
+      uint32_t o = 0;
+      for (int d = 0; d < R; ++d) {
+        o = ((o + 15) & ~15u) + (uint32_t)(dbase[d] & 15);
+        ooff[d] = o;
+        o += tcnt[d] * B;
+      }
+      // this output buffer's stores (two tiles ago, or the last tile's with one buffer) have read it
+      if (kTma) {
+        if (lay.nobuf == 2) bulk_wait_read<1>(); else bulk_wait_read<0>();
+      }
+    }
+    __syncthreads();
+    // permutation: item il (slot order) -> position rank in run d of the output
+    // tile.  Lane j starts at unit j mod UPI of its item and wraps around, so
+    // the lanes of one shared-memory wavefront hit different banks even when
+    // B is a multiple of 128 (items at the same bank offset).
+    const U* srcU = reinterpret_cast<const U*>(st);
+    const uint32_t u0 = lane % UPI;
+#pragma unroll
+    for (int k = 0; k < kK; ++k) {
+      const int d = dk[k];
+      if (d < R) {
+        const uint32_t il = w * 32 * kK + k * 32 + lane;
+        U* dstU = reinterpret_cast<U*>(ob + ooff[d] + (wbase[w * R + d] + rk_[k]) * B);
+        const U* s = srcU + (uint64_t)il * UPI;
+        uint32_t u = u0;
+        for (uint32_t j = 0; j < UPI; j += 4) {
+          U v[4];
+          uint32_t uu[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uu[q] = u;
+            if (j + q < UPI) v[q] = s[u];
+            u = u + 1 == UPI ? 0u : u + 1;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (j + q < UPI) dstU[uu[q]] = v[q];
+        }
+      }
+    }
+    if constexpr (kTma) {
+      fence_proxy_async();  // this thread's generic smem writes -> visible to the bulk stores
+      __syncthreads();
+      if (tid == 0) {
+        issue(it + 2);  // the stage is consumed: refill it
+        for (int d = 0; d < R; ++d) {
+          const uint64_t len = (uint64_t)tcnt[d] * B;
+          const uintptr_t a = dbase[d], e = a + len;
+          const uintptr_t b0 = (a + 15) & ~(uintptr_t)15, b1 = e & ~(uintptr_t)15;
+          if (b1 > b0) bulk_s2g(reinterpret_cast<void*>(b0), ob + ooff[d] + (b0 - a), (uint32_t)(b1 - b0));
+        }
+        bulk_commit();
+      }
+      // heads and tails (< 16 B each, or the whole run when it has no aligned body)
+      for (int d = tid; d < R; d += kThreads) {
+        const uint64_t len = (uint64_t)tcnt[d] * B;
+        if (!len) continue;
+        const uintptr_t a = dbase[d], e = a + len;
+        uintptr_t b0 = (a + 15) & ~(uintptr_t)15, b1 = e & ~(uintptr_t)15;
+        if (b1 <= b0) b0 = b1 = e;  // no body: threads write the whole run
+        const uint8_t* o = ob + ooff[d];
+        for (uintptr_t x = a; x < b0; x += sizeof(U))
+          *reinterpret_cast<U*>(x) = *reinterpret_cast<const U*>(o + (x - a));
+        for (uintptr_t x = b1; x < e; x += sizeof(U))
+          *reinterpret_cast<U*>(x) = *reinterpret_cast<const U*>(o + (x - a));
+      }
+    } else {
+      __syncthreads();
+      if (tid == 0) {
+        fence_proxy_async();  // order the generic-proxy reads of the stage before the async refill
+        issue(it + 2);
+      }
+      // every thread stores consecutive 16-byte chunks of the output tile; a
+      // chunk inside run d lands at a 16-byte-aligned global address (runs are
+      // placed congruent mod 16), chunks at a run's ends are written in
+      // item-unit pieces; the run a thread is in only moves forward
+      const uint32_t oend = ooff[R - 1] + tcnt[R - 1] * B;
+      int d = 0;
+      uint32_t rs = ooff[0], re = rs + tcnt[0] * B;
+      constexpr uint32_t kStep = kThreads * 16;
+      for (uint32_t c0 = tid * 16; c0 < oend; c0 += 4 * kStep) {
+        uint4 v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (c0 + q * kStep < oend) v[q] = *reinterpret_cast<const uint4*>(ob + c0 + q * kStep);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t c = c0 + q * kStep;
+          if (c < oend) {
+            while (c >= re) { ++d; rs = ooff[d]; re = rs + tcnt[d] * B; }
+            uint8_t* gp = reinterpret_cast<uint8_t*>(dbase[d]);
+            if (c >= rs && c + 16 <= re) {
+              *reinterpret_cast<uint4*>(gp + (c - rs)) = v[q];
+            } else {
+              const uint32_t x1 = c + 16 < re ? c + 16 : re;
+              for (uint32_t x = c > rs ? c : rs; x < x1; x += sizeof(U))
+                *reinterpret_cast<U*>(gp + (x - rs)) = *reinterpret_cast<const U*>(ob + x);
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();  // tcnt / ooff / dbase / the output tile are rewritten by the next tile
+  }
+  if (kTma && tid == 0) bulk_wait_all();  // every bulk store has completed its writes
+  if (dst_table) __threadfence_system();
   if (wrap_done && last_block(wrap_done)) {
     for (int l2 = threadIdx.x; l2 < L; l2 += blockDim.x) {
       ctrl_w[l2].ctr = 0;
@@ -869,7 +1143,90 @@ static int launch_scatter_t(Ctx* c, bool fused, bool wrap, uint32_t UPI, int gri
                                  : launch_scatter_m<U, 2>(c, fused, wrap, UPI, grid);
 }
 
+// ---- permuting scatter (RAFI_SCATTER_BULK: TMA bulk stores; RAFI_SCATTER_ALIGNED: 16-B thread stores)
+
+bool perm_supported(uint64_t B) { return B % 4 == 0; }
+
+// Output tiles: BULK keeps two (the store of tile i overlaps tile i+1) when
+// that still leaves room for two CTAs per SM; ALIGNED stores synchronously
+// and needs one.
+static uint32_t perm_nobuf(int mode, uint32_t T, uint64_t B, int R) {
+  if (mode != RAFI_SCATTER_BULK) return 1u;
+  return bulk_layout(T, B, R, 2).total <= 112u * 1024u ? 2u : 1u;
+}
+
+size_t perm_smem_bytes(int mode, uint32_t T, uint64_t B, int R) {
+  return bulk_layout(T, B, R, perm_nobuf(mode, T, B, R)).total;
+}
+
+// Largest tile (256 * 2^k) whose layout fits four CTAs per SM, else two, else one.
+uint32_t choose_tile_perm(int mode, uint64_t B, int R) {
+  for (uint32_t budget : {56u * 1024u, 112u * 1024u, 227u * 1024u}) {
+    uint32_t best = 0;
+    for (uint32_t T = kThreads; T <= kThreads * kMaxK; T *= 2)
+      if (perm_smem_bytes(mode, T, B, R) <= budget) best = T;
+    if (best) return best;
+  }
+  return kThreads;
+}
+
+template <typename U, int kK, int kMinB, bool kTma>
+static int launch_perm_k(Ctx* c, bool fused, bool wrap, uint32_t UPI, int grid) {
+  const BulkLayout lay = bulk_layout(c->tile, c->B, c->R, perm_nobuf(c->scatter_eff, c->tile, c->B, c->R));
+  static int granted = 0;  // per instantiation: the largest smem opt-in already granted
+  auto k = k_scatter_perm<U, kK, kMinB, kTma>;
+  if ((int)lay.total > granted) {
+    RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
+    granted = (int)lay.total;
+  }
+  k<<<grid, kThreads, lay.total, c->stream>>>(rank_table(c), c->ctrl, fused ? c->in_table_dev : nullptr, c->off_dev,
+                                             fused ? c->ovf_dev : nullptr, c->L, c->R, c->cap, c->tile, c->cur,
+                                             (uint32_t)c->B, UPI, lay, wrap ? c->done_dev + 1 : nullptr, c->ctrl,
+                                             c->plan_dev);
+  RAFI_CK_CUDA(cudaGetLastError());
+  return RAFI_OK;
+}
+
+template <typename U, int kMinB, bool kTma>
+static int launch_perm_m(Ctx* c, bool fused, bool wrap, uint32_t UPI, int grid) {
+  switch (c->tile / kThreads) {
+    case 1: return launch_perm_k<U, 1, kMinB, kTma>(c, fused, wrap, UPI, grid);
+    case 2: return launch_perm_k<U, 2, kMinB, kTma>(c, fused, wrap, UPI, grid);
+    case 4: return launch_perm_k<U, 4, kMinB, kTma>(c, fused, wrap, UPI, grid);
+    case 8: return launch_perm_k<U, 8, kMinB, kTma>(c, fused, wrap, UPI, grid);
+    case 16: return launch_perm_k<U, 16, kMinB, kTma>(c, fused, wrap, UPI, grid);
+    default: set_error("tile must be 256 * 2^k"); return RAFI_ERR_INVALID_ARG;
+  }
+}
+
+template <typename U, bool kTma>
+static int launch_perm_t(Ctx* c, bool fused, bool wrap, uint32_t UPI, int grid, int per_sm) {
+  return per_sm >= 4 ? launch_perm_m<U, 4, kTma>(c, fused, wrap, UPI, grid)
+                     : launch_perm_m<U, 2, kTma>(c, fused, wrap, UPI, grid);
+}
+
+template <bool kTma>
+static int launch_scatter_perm(Ctx* c, bool fused, bool wrap) {
+  const uint32_t unit = unit_for(c->B, 0);
+  const uint32_t UPI = (uint32_t)(c->B / unit);
+  const size_t smem = perm_smem_bytes(c->scatter_eff, c->tile, c->B, c->R);
+  const int fit = (int)((228u * 1024u) / (smem + 1024u));
+  const int per_sm = std::max(1, std::min(4, fit));
+  const int grid = persistent_grid(c, per_sm);
+  int rc;
+  switch (unit) {
+    case 16: rc = launch_perm_t<uint4, kTma>(c, fused, wrap, UPI, grid, per_sm); break;
+    case 8: rc = launch_perm_t<uint2, kTma>(c, fused, wrap, UPI, grid, per_sm); break;
+    case 4: rc = launch_perm_t<uint32_t, kTma>(c, fused, wrap, UPI, grid, per_sm); break;
+    default: set_error("permuting scatter needs item_bytes % 4 == 0"); return RAFI_ERR_UNSUPPORTED;
+  }
+  if (rc == RAFI_OK) { c->launches += 1; c->fwd_launches += 1; }
+  return rc;
+}
+
 int launch_scatter(Ctx* c, bool fused, bool wrap) {
+  if (c->scatter_eff == RAFI_SCATTER_BULK) return launch_scatter_perm<true>(c, fused, wrap);
+  if (c->scatter_eff == RAFI_SCATTER_ALIGNED) return launch_scatter_perm<false>(c, fused, wrap);
   const uint32_t unit = unit_for(c->B, 0);
   const uint32_t UPI = (uint32_t)(c->B / unit);
   const size_t smem = scatter_smem_bytes(c->tile, c->B, c->R);

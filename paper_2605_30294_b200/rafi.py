@@ -29,6 +29,8 @@ OPT_EXCHANGE = 1
 OPT_TIMING = 2
 OPT_TILE = 3
 OPT_SELF_DIRECT = 4
+OPT_SCATTER = 5
+SCATTER_AUTO, SCATTER_THREADS, SCATTER_BULK, SCATTER_ALIGNED = 0, 1, 2, 3
 EXCHANGE_AUTO, EXCHANGE_NCCL, EXCHANGE_PEER, EXCHANGE_FUSED = 0, 1, 2, 3
 
 

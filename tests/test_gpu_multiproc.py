@@ -23,7 +23,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, B, n, pattern, exchange, rounds):
+def _worker(rank, world, port, B, n, pattern, exchange, rounds, scatter=1):
     import torch.distributed as dist
 
     import oracle
@@ -41,6 +41,8 @@ def _worker(rank, world, port, B, n, pattern, exchange, rounds):
     ctx = rafi.Context(B, cap, comm=comm, stream=torch.cuda.current_stream())
     ctx.set_option(rafi.OPT_EXCHANGE, exchange)
     assert ctx.get_option(rafi.OPT_EXCHANGE) == exchange
+    ctx.set_option(rafi.OPT_SCATTER, scatter)
+    assert ctx.get_option(rafi.OPT_SCATTER) == scatter
     assert ctx.num_ranks == world and ctx.rank_of(0) == rank
     for rnd in range(rounds):
         m = n if rnd % 2 == 0 else n // 3
@@ -69,17 +71,18 @@ def _worker(rank, world, port, B, n, pattern, exchange, rounds):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("scatter", [1, 2, 3])  # THREADS, BULK (TMA bulk stores, to NVLink peers), ALIGNED
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("exchange", [1, 2, 3])  # NCCL, PEER, FUSED
 @pytest.mark.parametrize("B,pattern", [(48, "uniform"), (44, "skewed"), (16, "all_to_one")])
-def test_multigpu_snapshot_parity(world, exchange, B, pattern):
+def test_multigpu_snapshot_parity(world, exchange, B, pattern, scatter):
     if torch.cuda.device_count() < world:
         pytest.skip("needs %d GPUs" % world)
     import torch.multiprocessing as mp
-    mp.spawn(_worker, args=(world, _free_port(), B, 30011, pattern, exchange, 3), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), B, 30011, pattern, exchange, 3, scatter), nprocs=world, join=True)
 
 
-def _worker_hybrid(rank, world, port, L, B, n, graph):
+def _worker_hybrid(rank, world, port, L, B, n, graph, scatter=1):
     """P processes x L logical ranks each (R = P*L), FUSED exchange over
     local HBM and NVLink peer mappings; optionally the forward captured in a
     CUDA graph (NCCL collectives inside the capture, device-side G)."""
@@ -101,6 +104,7 @@ def _worker_hybrid(rank, world, port, L, B, n, graph):
     s = torch.cuda.Stream()
     ctx = rafi.Context(B, cap, comm=comm, stream=s, local_ranks=L)
     assert ctx.num_ranks == R and ctx.get_option(rafi.OPT_EXCHANGE) == rafi.EXCHANGE_FUSED
+    ctx.set_option(rafi.OPT_SCATTER, scatter)
     G_dev = torch.zeros(1, dtype=torch.int64, device="cuda")
     ex = None
     for rnd in range(3):
@@ -141,10 +145,12 @@ def _worker_hybrid(rank, world, port, L, B, n, graph):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("scatter", [1, 2, 3])
 @pytest.mark.parametrize("graph", [False, True])
 @pytest.mark.parametrize("world,L", [(2, 2), (2, 4), (4, 2)])
-def test_multigpu_hybrid_local_ranks(world, L, graph):
+def test_multigpu_hybrid_local_ranks(world, L, graph, scatter):
     if torch.cuda.device_count() < world:
         pytest.skip("needs %d GPUs" % world)
     import torch.multiprocessing as mp
-    mp.spawn(_worker_hybrid, args=(world, _free_port(), L, 44, 20011, graph), nprocs=world, join=True)
+    mp.spawn(_worker_hybrid, args=(world, _free_port(), L, 44, 20011, graph, scatter), nprocs=world,
+             join=True)

@@ -81,15 +81,21 @@ CASES = [
 
 
 EXCHANGES = {"fused": 3, "peer": 2}
+SCATTERS = {"threads": rafi.SCATTER_THREADS, "bulk": rafi.SCATTER_BULK, "aligned": rafi.SCATTER_ALIGNED}
 
 
+@pytest.mark.parametrize("scatter", sorted(SCATTERS))
 @pytest.mark.parametrize("exchange", sorted(EXCHANGES))
 @pytest.mark.parametrize("B,L,n,pattern", CASES)
-def test_forward_snapshot_parity(B, L, n, pattern, exchange):
+def test_forward_snapshot_parity(B, L, n, pattern, exchange, scatter):
+    if scatter != "threads" and (B % 4 or B > 256):
+        pytest.skip("bulk scatter needs item_bytes % 4 == 0 and a 256-item tile in shared memory")
     inputs = make_inputs(L, n, B, pattern, 1234 + B, invalid_frac=0.01)
     cap = max(n * L, 1)
     with _ctx(B, cap, L) as ctx:
         ctx.set_option(rafi.OPT_EXCHANGE, EXCHANGES[exchange])
+        ctx.set_option(rafi.OPT_SCATTER, SCATTERS[scatter])
+        assert ctx.get_option(rafi.OPT_SCATTER) == SCATTERS[scatter]
         _emit_all(ctx, inputs)
         p1_forward(ctx, L, B)
         # a second round on the same context (counters reset, buffers reused)
@@ -106,6 +112,36 @@ def test_tile_sizes(tile):
         ctx.set_option(rafi.OPT_TILE, tile)
         _emit_all(ctx, inputs)
         p1_forward(ctx, L, B)
+
+
+@pytest.mark.parametrize("B,tile", [(16, 256), (16, 1024), (16, 2048), (48, 256), (48, 512), (44, 1024),
+                                    (128, 256), (4, 4096), (36, 512), (256, 256), (200, 256), (64, 1024)])
+@pytest.mark.parametrize("mode", ["bulk", "aligned"])
+def test_perm_tile_sizes(B, tile, mode):
+    """The permuting scatters at every tile that fits, ragged last tiles and
+    runs whose global start is not 16-byte aligned (B % 16 != 0)."""
+    L, n = 4, 20011
+    inputs = make_inputs(L, n, B, "uniform", 6 + B)
+    with _ctx(B, n * L, L) as ctx:
+        ctx.set_option(rafi.OPT_SCATTER, SCATTERS[mode])
+        ctx.set_option(rafi.OPT_TILE, tile)
+        _emit_all(ctx, inputs)
+        p1_forward(ctx, L, B)
+
+
+def test_bulk_unsupported():
+    """BULK is refused (not silently replaced) where it cannot run."""
+    with _ctx(6, 1000, 1) as ctx:
+        with pytest.raises(rafi.RafiError):
+            ctx.set_option(rafi.OPT_SCATTER, rafi.SCATTER_BULK)
+        assert ctx.get_option(rafi.OPT_SCATTER) == rafi.SCATTER_THREADS
+    with _ctx(520, 1000, 1) as ctx:
+        with pytest.raises(rafi.RafiError):  # 2 stages + 1 output tile of 256 x 520 B > 227 KiB
+            ctx.set_option(rafi.OPT_SCATTER, rafi.SCATTER_BULK)
+    with _ctx(48, 100000, 1) as ctx:
+        ctx.set_option(rafi.OPT_SCATTER, rafi.SCATTER_BULK)
+        with pytest.raises(rafi.RafiError):
+            ctx.set_option(rafi.OPT_TILE, 4096)  # 2 stages + 1 output tile of 4096 x 48 B > 227 KiB
 
 
 @pytest.mark.parametrize("B,L,n,pattern", [(16, 1, 3000, "uniform"), (32, 2, 4096, "uniform"),
