@@ -46,7 +46,7 @@ def parse():
     p.add_argument("--items", type=int, default=DEF_N, help="items per rank per step")
     p.add_argument("--item-bytes", type=int, default=DEF_B)
     p.add_argument("--pattern", default="uniform")
-    p.add_argument("--exchange", default="auto", choices=["auto", "nccl", "peer", "fused"])
+    p.add_argument("--exchange", default="auto", choices=["auto", "nccl", "peer", "fused", "ce"])
     p.add_argument("--scatter", default="auto", choices=["auto", "threads", "bulk", "aligned"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -61,6 +61,15 @@ def load_peaks():
         return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def nvlink_ceilings(N):
+    """NVLink ceilings measured on this pool by tools/p2p_bw (profiles/nvlink_ceilings.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "nvlink_ceilings.json")) as f:
+            return json.load(f).get(str(N))
+    except Exception:
+        return None
 
 
 def workload_config(args, N):
@@ -239,8 +248,8 @@ def main():
     ctx = rafi.Context(B, cap, comm=comm, stream=stream, device=local)
     if args.exchange != "auto":
         ctx.set_option(rafi.OPT_EXCHANGE, {"nccl": rafi.EXCHANGE_NCCL, "peer": rafi.EXCHANGE_PEER,
-                                           "fused": rafi.EXCHANGE_FUSED}[args.exchange])
-    exchange = {1: "nccl", 2: "peer", 3: "fused"}[ctx.get_option(rafi.OPT_EXCHANGE)]
+                                           "fused": rafi.EXCHANGE_FUSED, "ce": rafi.EXCHANGE_CE}[args.exchange])
+    exchange = {1: "nccl", 2: "peer", 3: "fused", 4: "ce"}[ctx.get_option(rafi.OPT_EXCHANGE)]
     if args.scatter != "auto":
         ctx.set_option(rafi.OPT_SCATTER, {"threads": rafi.SCATTER_THREADS, "bulk": rafi.SCATTER_BULK,
                                           "aligned": rafi.SCATTER_ALIGNED}[args.scatter])
@@ -336,13 +345,25 @@ def main():
                 "unit": "GB/s", "frac": kern[dom]["frac"], "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": kern[dom]["bytes"]}
     exch = None
-    xfer_ms = ph["scatter"] if exchange == "fused" else ph["payload_exchange"]
+    xfer_ms = {"fused": ph["scatter"], "ce": ph["scatter"] + ph["payload_exchange"]}.get(exchange,
+                                                                                      ph["payload_exchange"])
     if N > 1 and xfer_ms > 0:
-        # remote payload bytes this GPU sends per step / time of the kernel that moves them
-        # (FUSED: the scatter pushes over NVLink; staged: the copy kernel / NCCL send-recv)
+        # remote payload bytes this GPU sends per step / time of the phase that moves them
+        # (FUSED: the scatter pushes over NVLink; CE: scatter passes + the copy-engine tail;
+        # staged: the copy kernel / NCCL send-recv)
         gbs = (remote / K) / (xfer_ms / 1e3) / 1e9
+        ceil = nvlink_ceilings(N)
         exch = {"gbs_per_gpu": gbs, "frac_of_900": gbs / 900.0, "frac_of_770_measured_p2p": gbs / 770.0,
-                "transport": exchange, "remote_bytes_per_step": remote / K, "kernel_ms": xfer_ms}
+                "transport": exchange, "remote_bytes_per_step": remote / K, "kernel_ms": xfer_ms,
+                "ceilings_gbs": ceil}
+        if exchange in ("fused", "ce") and xfer_ms >= max(v["ms"] for v in kern.values()):
+            # the step's dominant phase moves bytes over NVLink: that is its roofline
+            # (peak: the profiling guide's measured 770 GB/s peer copy per direction)
+            roofline = {"bound": "nvlink", "kernel": "scatter" if exchange == "fused" else "scatter+ce_copies",
+                        "achieved": gbs, "peak": 770.0, "unit": "GB/s", "frac": gbs / 770.0,
+                        "traffic": None, "peak_source": "B200_PROFILING.md: measured peer copy 770 GB/s per "
+                        "direction (nominal 900); this box's ceilings from tools/p2p_bw in ceilings_gbs",
+                        "algorithmic_bytes_per_launch": remote / K}
 
     # ---- end to end through the C ABI with host buffers
     e2e = None

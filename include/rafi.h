@@ -115,6 +115,8 @@ typedef struct {
                                       accumulated sums in rafi_stats; default 0 */
 #define RAFI_OPT_TILE 3            /* binning tile in items (256 * 2^k, k <= 4); 0 = auto from item size */
 #define RAFI_OPT_SELF_DIRECT 4     /* reserved (self run placement); 0 */
+#define RAFI_OPT_CE_PASSES 6       /* RAFI_EXCHANGE_CE: scatter passes per forward, 1..16 (0 = automatic:
+                                      about 2M items per pass, at most 8) */
 #define RAFI_OPT_SCATTER 5         /* how the binning scatter writes destination runs:
                                       RAFI_SCATTER_* (default AUTO).  Same result bytes either way.
                                       Only between rounds; re-chooses the tile unless RAFI_OPT_TILE
@@ -137,6 +139,13 @@ typedef struct {
 #define RAFI_EXCHANGE_FUSED 3      /* the scatter writes every destination run straight into the destination
                                       rank's incoming queue (local HBM or NVLink peer memory); the count
                                       matrix is all-gathered first; no send batch, no separate copy */
+#define RAFI_EXCHANGE_CE 4         /* copy-engine pipeline: counts all-gathered first; the scatter runs in
+                                      passes over the batch, writing the self run straight into the own
+                                      incoming queue and peer runs into the send batch; after each pass the
+                                      DMA copy engines move that pass's runs into the peers' incoming queues
+                                      (cudaMemcpyAsync over CUDA-IPC pointers, one stream per peer) while the
+                                      SMs scatter the next pass.  Several processes, one local rank each,
+                                      every rank's queues mapped; not capturable (rafi_forward_async) */
 
 /* ---- lifecycle ------------------------------------------------------------ */
 

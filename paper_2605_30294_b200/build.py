@@ -87,6 +87,24 @@ def build(force: bool = False, verbose: bool = False, defines=None, out: str | N
     return lib_path
 
 
+TOOLS = os.path.join(os.path.dirname(PKG), "tools")
+
+
+def build_tools() -> list:
+    """Measurement tools (not the product): tools/p2p_bw, the NVLink ceilings."""
+    out = []
+    for src in sorted(glob.glob(os.path.join(TOOLS, "*.cu"))):
+        exe = src[:-3]
+        if os.path.exists(exe) and os.path.getmtime(exe) >= os.path.getmtime(src):
+            out.append(exe)
+            continue
+        r = subprocess.run([NVCC] + ARCH + ["-O3", "-lineinfo", "-o", exe, src], capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("nvcc failed for %s:\n%s\n%s" % (src, r.stdout, r.stderr))
+        out.append(exe)
+    return out
+
+
 VARIANTS = {  # scatter tuning experiments: name -> defines (build with --variants)
     "ilp2": ["RAFI_SCATTER_ILP=2"],
     "ilp8": ["RAFI_SCATTER_ILP=8"],

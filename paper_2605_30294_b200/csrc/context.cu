@@ -161,6 +161,46 @@ static int exchange_peer_pointers(Ctx* c) {
   return rc;
 }
 
+static void free_ce(Ctx* c) {
+  for (size_t i = 0; i < c->ce_streams.size(); ++i) {
+    if (c->ce_streams[i]) { cudaStreamSynchronize(c->ce_streams[i]); cudaStreamDestroy(c->ce_streams[i]); }
+    if (c->ce_done[i]) cudaEventDestroy(c->ce_done[i]);
+  }
+  c->ce_streams.clear(); c->ce_done.clear();
+  for (auto& e : c->ce_pass)
+    if (e) { cudaEventDestroy(e); e = nullptr; }
+  cudaFree(c->ce_table_dev); cudaFree(c->bounds_dev);
+  cudaFreeHost(c->bounds_host); cudaFreeHost(c->off_host);
+  c->ce_table_dev = nullptr; c->bounds_dev = c->bounds_host = nullptr; c->off_host = nullptr;
+}
+
+// RAFI_EXCHANGE_CE resources: the destination table (own incoming queue for
+// the self run, the send batch for every peer), pass bounds, copy streams.
+static int ensure_ce(Ctx* c) {
+  if (c->ce_table_dev) return RAFI_OK;
+  const int R = c->R, me = c->proc;
+  RAFI_CK(alloc_dev((void**)&c->ce_table_dev, sizeof(uint8_t*) * R));
+  RAFI_CK(alloc_dev((void**)&c->bounds_dev, sizeof(uint32_t) * (Ctx::kMaxPasses + 1) * R));
+  if (cudaMallocHost((void**)&c->bounds_host, sizeof(uint32_t) * (Ctx::kMaxPasses + 1) * R) != cudaSuccess ||
+      cudaMallocHost((void**)&c->off_host, sizeof(uint64_t) * R) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("cudaMallocHost failed");
+    return RAFI_ERR_NOMEM;
+  }
+  std::vector<uint8_t*> t(R);
+  for (int d = 0; d < R; ++d) t[d] = d == me ? c->lr[0].in : c->lr[0].binned[0];
+  RAFI_CK_CUDA(cudaMemcpy(c->ce_table_dev, t.data(), sizeof(uint8_t*) * R, cudaMemcpyHostToDevice));
+  c->ce_streams.assign(R, nullptr);
+  c->ce_done.assign(R, nullptr);
+  for (int d = 0; d < R; ++d) {
+    if (d == me) continue;
+    RAFI_CK_CUDA(cudaStreamCreateWithFlags(&c->ce_streams[d], cudaStreamNonBlocking));
+    RAFI_CK_CUDA(cudaEventCreateWithFlags(&c->ce_done[d], cudaEventDisableTiming));
+  }
+  for (auto& e : c->ce_pass) RAFI_CK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return RAFI_OK;
+}
+
 static int resolve_exchange(Ctx* c) {
   int x = c->exchange;
   if (x == RAFI_EXCHANGE_AUTO) x = (c->nprocs == 1 || c->peer_ok) ? RAFI_EXCHANGE_FUSED : RAFI_EXCHANGE_NCCL;
@@ -172,6 +212,11 @@ static int resolve_exchange(Ctx* c) {
     set_error("NCCL exchange supports one local rank per process");
     return RAFI_ERR_UNSUPPORTED;
   }
+  if (x == RAFI_EXCHANGE_CE && (c->nprocs < 2 || c->L != 1 || !c->peer_ok)) {
+    set_error("CE exchange needs several processes, one local rank each, with every rank's queues mapped");
+    return RAFI_ERR_UNSUPPORTED;
+  }
+  if (x == RAFI_EXCHANGE_CE) RAFI_CK(ensure_ce(c));
   c->exchange_eff = x;
   return RAFI_OK;
 }
@@ -182,7 +227,14 @@ static bool is_perm(int mode) { return mode == RAFI_SCATTER_BULK || mode == RAFI
 
 static int resolve_scatter(Ctx* c) {
   int x = c->scatter;
-  if (x == RAFI_SCATTER_AUTO) x = RAFI_SCATTER_THREADS;
+  if (x == RAFI_SCATTER_AUTO) {
+    // BULK where the scatter pushes runs to NVLink peers (measured faster there:
+    // DESIGN.md section 6); THREADS for local HBM (faster at every item size)
+    const bool remote_push = c->nprocs > 1 && c->exchange_eff == RAFI_EXCHANGE_FUSED;
+    x = remote_push && perm_supported(c->B) && perm_smem_bytes(RAFI_SCATTER_BULK, 256, c->B, c->R) <= kMaxSmem
+            ? RAFI_SCATTER_BULK
+            : RAFI_SCATTER_THREADS;
+  }
   if (is_perm(x) && !(perm_supported(c->B) && perm_smem_bytes(x, 256, c->B, c->R) <= kMaxSmem)) {
     set_error("permuting scatter needs item_bytes % 4 == 0 and a 256-item tile that fits in shared memory");
     return RAFI_ERR_UNSUPPORTED;
@@ -211,6 +263,13 @@ static int set_tile(Ctx* c, uint32_t t) {
   return RAFI_OK;
 }
 
+// Re-resolve the scatter path (AUTO depends on the exchange) and its tile.
+static int refresh_scatter(Ctx* c) {
+  RAFI_CK(resolve_scatter(c));
+  if (!c->tile_user) RAFI_CK(set_tile(c, auto_tile(c)));
+  return RAFI_OK;
+}
+
 static int alloc_all(Ctx* c) {
   c->max_tiles = (c->cap + c->tile - 1) / c->tile;
   c->lr.assign(c->L, LocalRank{});
@@ -223,6 +282,7 @@ static void destroy_ctx(Ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  free_ce(c);
   close_ipc(c);
   for (auto& r : c->lr) free_rank(r);
   cudaFree(c->rank_dev); cudaFree(c->ctrl); cudaFree(c->runs_dev); cudaFree(c->plan_dev);
@@ -311,6 +371,7 @@ static int create(Ctx** out, const rafi_create_params* p) {
   if ((rc = alloc_all(c))) return fail(rc);
   if ((rc = exchange_peer_pointers(c))) return fail(rc);
   if ((rc = resolve_exchange(c))) return fail(rc);
+  if ((rc = refresh_scatter(c))) return fail(rc);
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) { cudaGetLastError(); set_error("sync"); return fail(RAFI_ERR_CUDA); }
   *out = c;
   return RAFI_OK;
@@ -568,6 +629,97 @@ static int64_t forward_staged(Ctx* c) {
   return (int64_t)G;
 }
 
+// CE forward: the payload moves on the DMA copy engines, pipelined with the
+// scatter (PAPER:492 names asynchronous streams as the way to overlap).
+//   hist -> scan -> [all-gather counts] -> pass bounds -> D2H, host plan ->
+//   for each pass k: scatter pass k (self run -> own incoming queue, peer runs
+//   -> send batch) ; copy streams: pass k's peer runs -> peers' incoming queues
+//   -> join copies -> [completion all-reduce]
+// Item order is the FUSED/staged order: source-major, slot order within a
+// source (pass k's run of (me, d) precedes pass k+1's in the receiver).
+static int64_t forward_ce(Ctx* c) {
+  const int R = c->R, me = c->proc;
+  const uint64_t B = c->B;
+  const bool T = c->timing;
+  c->fwd_launches = 0;
+  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[0], c->stream));
+  RAFI_CK(launch_hist(c));
+  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[1], c->stream));
+  RAFI_CK(launch_scan(c, 0));
+  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[2], c->stream));
+  RAFI_CK_NCCL(ncclAllGather(c->Cdev + (size_t)me * R, c->Cdev, (size_t)R, ncclUint64, c->comm, c->stream));
+  // passes: this round's item count is not on the host yet, so the previous
+  // round's sizes it (any K gives the same bytes; K only sets the overlap)
+  int K = c->ce_passes;
+  if (K <= 0) K = (int)std::max<uint64_t>(1, std::min<uint64_t>(8, c->lr[0].n_out >> 21));
+  RAFI_CK(launch_pass_bounds(c, K));
+  RAFI_CK_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl, ctrl_c_bytes(c), cudaMemcpyDeviceToHost, c->stream));
+  RAFI_CK_CUDA(cudaMemcpyAsync(c->bounds_host, c->bounds_dev, sizeof(uint32_t) * (K + 1) * R,
+                               cudaMemcpyDeviceToHost, c->stream));
+  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[3], c->stream));
+  RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
+  c->host_stale = false;
+  uint64_t G = 0;
+  if (book_keep(c, &G)) {  // Z3, decided identically on every rank from the same matrix
+    c->broken = true;
+    set_error("receive overflow: some rank would receive more than its capacity");
+    return RAFI_ERR_RECV_OVERFLOW;
+  }
+  // bases: self run at recv_off_me[me] in the own incoming queue, peer d's run
+  // at send_off[d] in the send batch; each peer's run lands at recv_off_d[me]
+  std::vector<uint64_t> recv_off(R, 0);
+  uint64_t send_off = 0;
+  for (int d = 0; d < R; ++d) {
+    for (int s = 0; s < me; ++s) recv_off[d] += c->Chost[(size_t)s * R + d];
+    c->off_host[d] = d == me ? recv_off[d] : send_off;
+    send_off += c->Chost[(size_t)me * R + d];
+  }
+  c->plan_host[0] = c->lr[0].num_in;
+  RAFI_CK_CUDA(cudaMemcpyAsync(c->off_dev, c->off_host, sizeof(uint64_t) * R, cudaMemcpyHostToDevice, c->stream));
+  RAFI_CK_CUDA(cudaMemcpyAsync(c->plan_dev, c->plan_host, sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
+  const uint64_t n = c->lr[0].n_out;
+  const uint64_t tiles = (n + c->tile - 1) / c->tile;
+  const uint64_t nblk = (tiles + 7) / 8;  // kHistTilesPerCta
+  uint8_t* sb = c->lr[0].binned[0];
+  for (int k = 0; k < K; ++k) {
+    const uint64_t b0 = (uint64_t)k * nblk / K, b1 = (uint64_t)(k + 1) * nblk / K;
+    c->g_lo = std::min(tiles, 8 * b0);
+    c->g_hi = std::min(tiles, 8 * b1);
+    if (c->g_hi > c->g_lo || k == K - 1) {
+      if (c->g_hi <= c->g_lo) { c->g_lo = 0; c->g_hi = 0; }  // empty last pass: wrap-up only
+      int rc = launch_scatter(c, true, k == K - 1);
+      c->g_lo = 0; c->g_hi = ~0ull;
+      RAFI_CK(rc);
+    }
+    RAFI_CK_CUDA(cudaEventRecord(c->ce_pass[k], c->stream));
+    for (int d = 0; d < R; ++d) {
+      if (d == me) continue;
+      const uint64_t lo = c->bounds_host[(size_t)k * R + d], hi = c->bounds_host[(size_t)(k + 1) * R + d];
+      if (hi <= lo) continue;
+      RAFI_CK_CUDA(cudaStreamWaitEvent(c->ce_streams[d], c->ce_pass[k], 0));
+      RAFI_CK_CUDA(cudaMemcpyAsync(c->peer_in[d] + (recv_off[d] + lo) * B, sb + (c->off_host[d] + lo) * B,
+                                   (hi - lo) * B, cudaMemcpyDeviceToDevice, c->ce_streams[d]));
+    }
+  }
+  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[4], c->stream));
+  for (int d = 0; d < R; ++d) {
+    if (d == me) continue;
+    RAFI_CK_CUDA(cudaEventRecord(c->ce_done[d], c->ce_streams[d]));
+    RAFI_CK_CUDA(cudaStreamWaitEvent(c->stream, c->ce_done[d], 0));
+  }
+  // every rank's copies into every queue have completed once the all-reduce has
+  RAFI_CK_NCCL(ncclAllReduce(c->ovf_dev + 1, c->ovf_dev + 1, 1, ncclInt32, ncclMax, c->comm, c->stream));
+  if (T) {
+    RAFI_CK_CUDA(cudaEventRecord(c->ev[5], c->stream));
+    RAFI_CK_CUDA(cudaEventRecord(c->ev[6], c->stream));
+    mark_timing(c, true);
+  }
+  c->last_fused = true;  // no readable send batch for the self run (it went straight to the queue)
+  c->round += 1;
+  c->last_G = (int64_t)G;
+  return (int64_t)G;
+}
+
 static int64_t forward(Ctx* c) {
   if (c->broken) { set_error("context unusable after an earlier collective error"); return RAFI_ERR_STATE; }
   RAFI_CK_CUDA(cudaSetDevice(c->device));
@@ -576,6 +728,7 @@ static int64_t forward(Ctx* c) {
     RAFI_CK_CUDA(cudaStreamWaitEvent(c->stream, c->ev_out_done, 0));
     c->out_pending = false;
   }
+  if (c->exchange_eff == RAFI_EXCHANGE_CE) return forward_ce(c);
   return c->exchange_eff == RAFI_EXCHANGE_FUSED ? forward_fused(c) : forward_staged(c);
 }
 
@@ -689,7 +842,9 @@ int rafi_resize(rafi_ctx* ctx, size_t capacity) {
   RAFI_CK(upload_rank_table(c));
   c->cur = 0;
   RAFI_CK(exchange_peer_pointers(c));
+  free_ce(c);  // its table points at the old queues
   RAFI_CK(resolve_exchange(c));
+  RAFI_CK(refresh_scatter(c));
   return RAFI_OK;
 }
 
@@ -951,12 +1106,12 @@ int rafi_set_option(rafi_ctx* ctx, int key, long long v) {
   if (!c) return RAFI_ERR_INVALID_ARG;
   switch (key) {
     case RAFI_OPT_EXCHANGE: {
-      if (v < RAFI_EXCHANGE_AUTO || v > RAFI_EXCHANGE_FUSED) return RAFI_ERR_INVALID_ARG;
+      if (v < RAFI_EXCHANGE_AUTO || v > RAFI_EXCHANGE_CE) return RAFI_ERR_INVALID_ARG;
       const int old = c->exchange;
       c->exchange = (int)v;
       int rc = resolve_exchange(c);
-      if (rc != RAFI_OK) { c->exchange = old; resolve_exchange(c); }
-      return rc;
+      if (rc != RAFI_OK) { c->exchange = old; resolve_exchange(c); return rc; }
+      return refresh_scatter(c);
     }
     case RAFI_OPT_TIMING:
       c->timing = v != 0;
@@ -988,6 +1143,10 @@ int rafi_set_option(rafi_ctx* ctx, int key, long long v) {
       return RAFI_OK;
     }
     case RAFI_OPT_SELF_DIRECT: return v == 0 ? RAFI_OK : RAFI_ERR_UNSUPPORTED;
+    case RAFI_OPT_CE_PASSES:
+      if (v < 0 || v > Ctx::kMaxPasses) return RAFI_ERR_INVALID_ARG;
+      c->ce_passes = (int)v;
+      return RAFI_OK;
     default: return RAFI_ERR_INVALID_ARG;
   }
 }
@@ -1000,6 +1159,7 @@ int rafi_get_option(const rafi_ctx* ctx, int key, long long* v) {
     case RAFI_OPT_TIMING: *v = c->timing; return RAFI_OK;
     case RAFI_OPT_TILE: *v = c->tile; return RAFI_OK;
     case RAFI_OPT_SCATTER: *v = c->scatter_eff; return RAFI_OK;
+    case RAFI_OPT_CE_PASSES: *v = c->ce_passes; return RAFI_OK;
     case RAFI_OPT_SELF_DIRECT: *v = 0; return RAFI_OK;
     default: return RAFI_ERR_INVALID_ARG;
   }

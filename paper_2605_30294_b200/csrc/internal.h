@@ -139,6 +139,19 @@ struct Ctx {
   cudaEvent_t ev_stage_ready[2] = {}, ev_stage_free[2] = {}, ev_in_ready = nullptr, ev_out_done = nullptr;
   bool out_pending = false;
 
+  // scatter tile range [g_lo, g_hi) (flat over local ranks; the CE exchange scatters in passes)
+  uint64_t g_lo = 0, g_hi = ~0ull;
+  // RAFI_EXCHANGE_CE: destination table (own incoming queue for the self run,
+  // the local send batch for every peer), pass bounds, copy streams
+  static constexpr int kMaxPasses = 16;
+  uint8_t** ce_table_dev = nullptr;   // [R]
+  uint32_t* bounds_dev = nullptr;     // [(kMaxPasses+1) * R] items of dest d before pass k's first block
+  uint32_t* bounds_host = nullptr;    // pinned mirror
+  uint64_t* off_host = nullptr;       // [R] pinned: per-destination bases uploaded to off_dev
+  int ce_passes = 0;                  // RAFI_OPT_CE_PASSES (0 = automatic)
+  std::vector<cudaStream_t> ce_streams;  // [R] one copy stream per peer
+  std::vector<cudaEvent_t> ce_done;      // [R]
+  cudaEvent_t ce_pass[kMaxPasses] = {};
   cudaEvent_t ev[8] = {};
   static constexpr int kEmitEv = 32;     // ring of (start, end) event pairs for timed bulk emits
   cudaEvent_t ev_emit[kEmitEv][2] = {};
@@ -165,6 +178,7 @@ int launch_scatter(Ctx* c, bool fused, bool wrap);
 int launch_plan(Ctx* c, bool fused, unsigned long long* G_out = nullptr);
 int launch_copy(Ctx* c, int nruns_per_dest);
 int launch_wrapup(Ctx* c);
+int launch_pass_bounds(Ctx* c, int K);
 size_t scatter_smem_bytes(uint32_t tile, uint64_t item_bytes, int R);
 
 }  // namespace rafi_impl

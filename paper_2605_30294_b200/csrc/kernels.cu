@@ -174,22 +174,30 @@ __device__ __forceinline__ uint32_t warp_sum(uint32_t x) {
   return x;
 }
 
-constexpr int kHistTilesPerWarp = 1;
-constexpr int kHistTilesPerCta = kWarps * kHistTilesPerWarp;  // 8 tiles = one "block" of the scan
-constexpr int kHistVec = 4;  // 16-byte dest loads in flight per lane (one batch covers a 512-item tile)
+constexpr int kHistTilesPerCta = 8;  // one "block" of the two-level tile scan
+constexpr int kHistVec = 4;          // 16-byte dest loads per lane per tile and batch (a batch covers 512 items)
+
+// Tiles a warp counts concurrently: two for R <= 8 (eight 16-byte loads in
+// flight per lane, four warps per CTA), one otherwise (eight warps per CTA).
+template <int RMAX>
+struct HistShape {
+  static constexpr int kTPW = (RMAX > 0 && RMAX <= 8) ? 2 : 1;
+  static constexpr int kThreadsH = 32 * kHistTilesPerCta / kTPW;
+};
 
 // Per-tile per-destination counts (the counting half of the paper's radix
-// sort by destination), one warp per tile, 16-byte loads with
-// 4 in flight per lane, many small CTAs resident per SM.  CTA (b, l) covers
-// tiles 8b..8b+7 of local rank l and also does the first level of the tile
-// scan: for every destination d it writes O[l][d][t] = items with dest d in
-// tiles 8b..t-1 of the block, and
-// the block aggregate H[l][d][b] (scanned by k_scan).  RMAX > 0: register
-// counters for R <= RMAX reduced with warp shuffles; RMAX == 0: shared
-// counters fed by __match_any_sync aggregation.
+// sort by destination), one warp per one or two tiles, 16-byte
+// loads, many small CTAs resident per SM.  CTA (b, l) covers tiles 8b..8b+7 of
+// local rank l and also does the first level of the tile scan: for every
+// destination d it writes O[l][d][t] = items with dest d in tiles 8b..t-1 of
+// the block, and the block aggregate H[l][d][b] (scanned by k_scan).
+// RMAX > 0: register counters for R <= RMAX reduced with warp shuffles;
+// RMAX == 0: shared counters fed by __match_any_sync aggregation.
 template <int RMAX>
-__global__ void __launch_bounds__(kThreads, 6)
+__global__ void __launch_bounds__(HistShape<RMAX>::kThreadsH, 1024 / HistShape<RMAX>::kThreadsH)
 k_hist(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, int R, uint64_t cap, uint32_t T) {
+  constexpr int TPW = HistShape<RMAX>::kTPW;
+  constexpr int NT = HistShape<RMAX>::kThreadsH;
   extern __shared__ uint32_t tc[];  // [kHistTilesPerCta][R] tile counts
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int l = blockIdx.y;
@@ -198,49 +206,69 @@ k_hist(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, int R, 
   const uint64_t tb = (uint64_t)blockIdx.x * kHistTilesPerCta;
   if (tb >= tiles) return;  // uniform over the CTA
   const uint64_t nblk = (tiles + kHistTilesPerCta - 1) / kHistTilesPerCta;
-  for (int k = 0; k < kHistTilesPerWarp; ++k) {
-    const int ti = w * kHistTilesPerWarp + k;  // tile within the CTA
-    const uint64_t t = tb + ti;
-    uint32_t* mine = tc + ti * R;
-    if (t >= tiles) {
-      for (int d = lane; d < R; d += 32) mine[d] = 0;
-      continue;
-    }
-    const uint64_t t0 = t * T;
-    const uint32_t nt = (uint32_t)umin64(T, n - t0);
-    if (RMAX > 0) {
-      const int4* d4 = reinterpret_cast<const int4*>(rk[l].dest + t0);  // t0*4 is a multiple of 1 KiB
-      uint32_t c[RMAX > 0 ? RMAX : 1];
+  if (RMAX > 0) {
+    // the warp's TPW tiles, batch by batch, all their loads issued before counting
+    // packed counters: byte (d & 7) of word d >> 3 counts destination d; a
+    // lane sees at most T / 32 <= 128 items of a tile, so no byte overflows
+    constexpr int NW = RMAX > 0 ? (RMAX + 7) / 8 : 1;
+    uint64_t c[TPW][NW];
+    uint32_t nq[TPW];
+    const int4* d4[TPW];
 #pragma unroll
-      for (int r = 0; r < RMAX; ++r) c[r] = 0;
-      const uint32_t nq = (nt + 3) / 4;
-      for (uint32_t q0 = 0; q0 < nq; q0 += 32 * kHistVec) {
-        int4 v[kHistVec];
+    for (int k = 0; k < TPW; ++k) {
+      const uint64_t t = tb + w * TPW + k;
+      const uint64_t t0 = t * T;
+      const uint32_t nt = t < tiles ? (uint32_t)umin64(T, n - t0) : 0u;
+      nq[k] = (nt + 3) / 4;
+      d4[k] = reinterpret_cast<const int4*>(rk[l].dest + (t < tiles ? t0 : 0));  // t0*4 is a multiple of 1 KiB
+#pragma unroll
+      for (int x = 0; x < NW; ++x) c[k][x] = 0;
+    }
+    for (uint32_t q0 = 0; q0 < (T + 3) / 4; q0 += 32 * kHistVec) {
+      int4 v[TPW][kHistVec];
+#pragma unroll
+      for (int k = 0; k < TPW; ++k)
 #pragma unroll
         for (int j = 0; j < kHistVec; ++j) {
           const uint32_t q = q0 + j * 32 + lane;
-          v[j] = q < nq ? d4[q] : make_int4(-1, -1, -1, -1);
+          v[k][j] = q < nq[k] ? d4[k][q] : make_int4(-1, -1, -1, -1);
         }
+#pragma unroll
+      for (int k = 0; k < TPW; ++k) {
+        const uint64_t t = tb + w * TPW + k;
+        const uint32_t nt = t < tiles ? (uint32_t)umin64(T, n - t * T) : 0u;
 #pragma unroll
         for (int j = 0; j < kHistVec; ++j) {
           const uint32_t i0 = (q0 + j * 32 + lane) * 4;
-          const int e[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+          const int e[4] = {v[k][j].x, v[k][j].y, v[k][j].z, v[k][j].w};
 #pragma unroll
           for (int m = 0; m < 4; ++m) {
-            const int d = i0 + m < nt ? e[m] : -1;
+            const int d = i0 + m < nt ? e[m] : -1;  // -1 (and any d >= RMAX) matches no word
+            const uint64_t one = 1ull << ((d & 7) * 8);
 #pragma unroll
-            for (int r = 0; r < RMAX; ++r) c[r] += (d == r);
+            for (int x = 0; x < NW; ++x) c[k][x] += (d >> 3) == x ? one : 0ull;
           }
         }
       }
+    }
+#pragma unroll
+    for (int k = 0; k < TPW; ++k) {
+      uint32_t* mine = tc + (w * TPW + k) * R;
 #pragma unroll
       for (int r = 0; r < RMAX; ++r) {
-        const uint32_t x = warp_sum(c[r]);
+        const uint32_t x = warp_sum((uint32_t)(c[k][r >> 3] >> ((r & 7) * 8)) & 0xffu);
         if (lane == (r & 31) && r < R) mine[r] = x;
       }
-    } else {
-      for (int d = lane; d < R; d += 32) mine[d] = 0;
-      __syncwarp();
+    }
+  } else {
+    const int ti = w;  // one tile per warp
+    const uint64_t t = tb + ti;
+    uint32_t* mine = tc + ti * R;
+    for (int d = lane; d < R; d += 32) mine[d] = 0;
+    __syncwarp();
+    if (t < tiles) {
+      const uint64_t t0 = t * T;
+      const uint32_t nt = (uint32_t)umin64(T, n - t0);
       const int32_t* dest = rk[l].dest + t0;
       for (uint32_t i = lane; i < T; i += 32) {  // T is a multiple of 32
         const int d = i < nt ? dest[i] : -1;
@@ -253,7 +281,7 @@ k_hist(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, int R, 
   __syncthreads();
   // first scan level: exclusive prefix over the CTA's tiles, per destination
   uint32_t* O = rk[l].O;
-  for (int d = threadIdx.x; d < R; d += kThreads) {
+  for (int d = threadIdx.x; d < R; d += NT) {
     uint32_t acc = 0;
     for (int ti = 0; ti < kHistTilesPerCta; ++ti) {
       const uint64_t t = tb + ti;
@@ -515,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, kMinB)
 k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint8_t* const* __restrict__ dst_table,
           const uint64_t* __restrict__ dst_off, const int* __restrict__ ovf, int L, int R, uint64_t cap, uint32_t T,
           int cur, uint32_t B, uint32_t UPI, FastDiv divU, ScatterLayout lay, unsigned* __restrict__ wrap_done,
-          CtrlDev* __restrict__ ctrl_w, const uint64_t* __restrict__ wrap_num_in) {
+          CtrlDev* __restrict__ ctrl_w, const uint64_t* __restrict__ wrap_num_in, uint64_t g_lo, uint64_t g_hi) {
   if (ovf && *ovf) return;  // collective receive overflow: move nothing (Z3)
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + lay.off_mbar);
@@ -529,10 +557,10 @@ k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint
   constexpr uint32_t K = kK;  // items per thread per tile (T = 256 * kK)
 
   auto issue = [&](uint32_t it) {  // thread 0: start loading iteration it's tile into stage it&1
-    const uint64_t g = blockIdx.x + (uint64_t)it * gridDim.x;
+    const uint64_t g = g_lo + blockIdx.x + (uint64_t)it * gridDim.x;
     int l;
     uint64_t t, n, tiles;
-    if (!tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) return;
+    if (g >= g_hi || !tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) return;
     const uint64_t t0 = t * T;
     const uint32_t nt = (uint32_t)umin64(T, n - t0);
     uint8_t* st = smem + (it & 1) * lay.stage_stride;
@@ -552,10 +580,10 @@ k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint
   if (tid == 0) { issue(0); issue(1); }
 
   for (uint32_t it = 0;; ++it) {
-    const uint64_t g = blockIdx.x + (uint64_t)it * gridDim.x;
+    const uint64_t g = g_lo + blockIdx.x + (uint64_t)it * gridDim.x;
     int l;
     uint64_t t, n, tiles;
-    if (!tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) break;
+    if (g >= g_hi || !tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) break;
     const uint64_t t0 = t * T;
     const uint32_t nt = (uint32_t)umin64(T, n - t0);
     const uint8_t* st = smem + (it & 1) * lay.stage_stride;
@@ -738,7 +766,7 @@ __global__ void __launch_bounds__(kThreads, kMinB)
 k_scatter_perm(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint8_t* const* __restrict__ dst_table,
                const uint64_t* __restrict__ dst_off, const int* __restrict__ ovf, int L, int R, uint64_t cap, uint32_t T,
                int cur, uint32_t B, uint32_t UPI, BulkLayout lay, unsigned* __restrict__ wrap_done,
-               CtrlDev* __restrict__ ctrl_w, const uint64_t* __restrict__ wrap_num_in) {
+               CtrlDev* __restrict__ ctrl_w, const uint64_t* __restrict__ wrap_num_in, uint64_t g_lo, uint64_t g_hi) {
   if (ovf && *ovf) return;  // collective receive overflow: move nothing (Z3)
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + lay.off_mbar);
@@ -750,10 +778,10 @@ k_scatter_perm(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl,
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
 
   auto issue = [&](uint32_t it) {  // thread 0: start loading iteration it's tile into stage it&1
-    const uint64_t g = blockIdx.x + (uint64_t)it * gridDim.x;
+    const uint64_t g = g_lo + blockIdx.x + (uint64_t)it * gridDim.x;
     int l;
     uint64_t t, n, tiles;
-    if (!tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) return;
+    if (g >= g_hi || !tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) return;
     const uint64_t t0 = t * T;
     const uint32_t nt = (uint32_t)umin64(T, n - t0);
     uint8_t* st = smem + (it & 1) * lay.stage_stride;
@@ -768,10 +796,10 @@ k_scatter_perm(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl,
   // destination base + (tile prefix O + block prefix H + per-destination
   // base) * B; 0 past the last tile
   auto run_addr = [&](uint32_t it, int d) -> uintptr_t {
-    const uint64_t g = blockIdx.x + (uint64_t)it * gridDim.x;
+    const uint64_t g = g_lo + blockIdx.x + (uint64_t)it * gridDim.x;
     int l;
     uint64_t t, n, tiles;
-    if (!tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) return 0;
+    if (g >= g_hi || !tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) return 0;
     const uint64_t nblk = (tiles + kHistTilesPerCta - 1) / kHistTilesPerCta;
     const uint64_t first = (uint64_t)rk[l].O[(uint64_t)d * tiles + t] +
                            rk[l].H[(uint64_t)d * nblk + t / kHistTilesPerCta] + dst_off[(uint64_t)l * R + d];
@@ -788,10 +816,10 @@ k_scatter_perm(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl,
   uintptr_t pf_addr = (R <= kThreads && tid < R) ? run_addr(0, tid) : 0;
 
   for (uint32_t it = 0;; ++it) {
-    const uint64_t g = blockIdx.x + (uint64_t)it * gridDim.x;
+    const uint64_t g = g_lo + blockIdx.x + (uint64_t)it * gridDim.x;
     int l;
     uint64_t t, n, tiles;
-    if (!tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) break;
+    if (g >= g_hi || !tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) break;
     const uint64_t t0 = t * T;
     const uint32_t nt = (uint32_t)umin64(T, n - t0);
     const uint8_t* st = smem + (it & 1) * lay.stage_stride;
@@ -981,6 +1009,34 @@ k_copy(const CopyRun* __restrict__ runs, const RankDev* __restrict__ rk, int R, 
   }
 }
 
+// ---------------------------------------------------------------- a6 CE exchange: pass bounds
+
+// Items of destination d in blocks 0 .. b_k-1 of (single) local rank 0, for the
+// K+1 pass boundaries b_k = k * nblk / K (blocks of kHistTilesPerCta tiles;
+// b_K = nblk gives the row total).  After k_scan, H holds exactly these
+// exclusive block prefixes.  The host derives the same b_k from the item
+// count, so pass k of the scatter covers tiles [8 b_k, 8 b_{k+1}).
+__global__ void k_pass_bounds(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl,
+                              const uint64_t* __restrict__ Cmat, int grank, int R, uint64_t cap, uint32_t T, int K,
+                              uint32_t* __restrict__ out) {
+  const uint64_t n = n_items(ctrl[0], cap);
+  const uint64_t tiles = (n + T - 1) / T;
+  const uint64_t nblk = (tiles + kHistTilesPerCta - 1) / kHistTilesPerCta;
+  for (int x = threadIdx.x; x < (K + 1) * R; x += blockDim.x) {
+    const int k = x / R, d = x % R;
+    const uint64_t b = (uint64_t)k * nblk / K;
+    out[x] = b >= nblk ? (uint32_t)Cmat[(uint64_t)grank * R + d] : rk[0].H[(uint64_t)d * nblk + b];
+  }
+}
+
+int launch_pass_bounds(Ctx* c, int K) {
+  k_pass_bounds<<<1, 256, 0, c->stream>>>(rank_table(c), c->ctrl, c->Cdev, c->proc, c->R, c->cap, c->tile, K,
+                                          c->bounds_dev);
+  RAFI_CK_CUDA(cudaGetLastError());
+  c->launches += 1; c->fwd_launches += 1;
+  return RAFI_OK;
+}
+
 // ---------------------------------------------------------------- a7 wrap-up
 
 __global__ void k_wrapup(CtrlDev* ctrl, const uint64_t* num_in, int L, const int* ovf) {
@@ -1058,7 +1114,7 @@ int launch_emit_bulk(Ctx* c, int local, const uint8_t* items, const int32_t* des
 }
 
 static int persistent_grid(Ctx* c, int per_sm) {
-  const uint64_t max_tiles_all = c->max_tiles * (uint64_t)c->L;
+  const uint64_t max_tiles_all = std::min<uint64_t>(c->max_tiles * (uint64_t)c->L, c->g_hi - c->g_lo);
   return (int)std::max<uint64_t>(1, std::min<uint64_t>(max_tiles_all, (uint64_t)num_sms(c->device) * per_sm));
 }
 
@@ -1069,7 +1125,7 @@ int launch_hist(Ctx* c) {
   do {                                                                                                  \
     if (sm > 48 * 1024)                                                                                 \
       RAFI_CK_CUDA(cudaFuncSetAttribute(k_hist<RM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
-    k_hist<RM><<<grid, kThreads, sm, c->stream>>>(rank_table(c), c->ctrl, c->R, c->cap, c->tile);      \
+    k_hist<RM><<<grid, HistShape<RM>::kThreadsH, sm, c->stream>>>(rank_table(c), c->ctrl, c->R, c->cap, c->tile); \
   } while (0)
   if (c->R <= 1) HIST(1);
   else if (c->R <= 2) HIST(2);
@@ -1098,9 +1154,9 @@ static int launch_scatter_k(Ctx* c, bool fused, bool wrap, uint32_t UPI, int gri
   const FastDiv dv(UPI);
   const bool si = stage_items(c->tile, c->B);
   const ScatterLayout lay = scatter_layout(c->tile, c->B, c->R, si);
-  uint8_t* const* table = fused ? c->in_table_dev : nullptr;
+  uint8_t* const* table = fused ? (c->exchange_eff == RAFI_EXCHANGE_CE ? c->ce_table_dev : c->in_table_dev) : nullptr;
   const uint64_t* off = c->off_dev;
-  const int* ovf = fused ? c->ovf_dev : nullptr;
+  const int* ovf = fused && c->exchange_eff != RAFI_EXCHANGE_CE ? c->ovf_dev : nullptr;
   static int set_true = 0, set_false = 0;  // per instantiation: the largest smem opt-in already granted
   if (si) {
     auto k = k_scatter<U, true, kK, kMinB>;
@@ -1110,7 +1166,7 @@ static int launch_scatter_k(Ctx* c, bool fused, bool wrap, uint32_t UPI, int gri
     }
     k<<<grid, kThreads, lay.total, c->stream>>>(rank_table(c), c->ctrl, table, off, ovf, c->L, c->R, c->cap, c->tile,
                                                c->cur, (uint32_t)c->B, UPI, dv, lay, wrap ? c->done_dev + 1 : nullptr,
-                                               c->ctrl, c->plan_dev);
+                                               c->ctrl, c->plan_dev, c->g_lo, c->g_hi);
   } else {
     auto k = k_scatter<U, false, kK, kMinB>;
     if ((int)lay.total > set_false) {
@@ -1119,7 +1175,7 @@ static int launch_scatter_k(Ctx* c, bool fused, bool wrap, uint32_t UPI, int gri
     }
     k<<<grid, kThreads, lay.total, c->stream>>>(rank_table(c), c->ctrl, table, off, ovf, c->L, c->R, c->cap, c->tile,
                                                c->cur, (uint32_t)c->B, UPI, dv, lay, wrap ? c->done_dev + 1 : nullptr,
-                                               c->ctrl, c->plan_dev);
+                                               c->ctrl, c->plan_dev, c->g_lo, c->g_hi);
   }
   RAFI_CK_CUDA(cudaGetLastError());
   return RAFI_OK;
@@ -1179,10 +1235,12 @@ static int launch_perm_k(Ctx* c, bool fused, bool wrap, uint32_t UPI, int grid) 
     RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
     granted = (int)lay.total;
   }
-  k<<<grid, kThreads, lay.total, c->stream>>>(rank_table(c), c->ctrl, fused ? c->in_table_dev : nullptr, c->off_dev,
-                                             fused ? c->ovf_dev : nullptr, c->L, c->R, c->cap, c->tile, c->cur,
+  const bool ce = c->exchange_eff == RAFI_EXCHANGE_CE;
+  k<<<grid, kThreads, lay.total, c->stream>>>(rank_table(c), c->ctrl,
+                                             fused ? (ce ? c->ce_table_dev : c->in_table_dev) : nullptr, c->off_dev,
+                                             fused && !ce ? c->ovf_dev : nullptr, c->L, c->R, c->cap, c->tile, c->cur,
                                              (uint32_t)c->B, UPI, lay, wrap ? c->done_dev + 1 : nullptr, c->ctrl,
-                                             c->plan_dev);
+                                             c->plan_dev, c->g_lo, c->g_hi);
   RAFI_CK_CUDA(cudaGetLastError());
   return RAFI_OK;
 }

@@ -30,8 +30,9 @@ OPT_TIMING = 2
 OPT_TILE = 3
 OPT_SELF_DIRECT = 4
 OPT_SCATTER = 5
+OPT_CE_PASSES = 6
 SCATTER_AUTO, SCATTER_THREADS, SCATTER_BULK, SCATTER_ALIGNED = 0, 1, 2, 3
-EXCHANGE_AUTO, EXCHANGE_NCCL, EXCHANGE_PEER, EXCHANGE_FUSED = 0, 1, 2, 3
+EXCHANGE_AUTO, EXCHANGE_NCCL, EXCHANGE_PEER, EXCHANGE_FUSED, EXCHANGE_CE = 0, 1, 2, 3, 4
 
 
 class DeviceView(C.Structure):

@@ -15,6 +15,16 @@ if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
     pytest.skip("needs >= 2 CUDA GPUs", allow_module_level=True)
 
 
+def _need(world):
+    """Skip unless `world` GPUs are visible (and, when RAFI_TEST_WORLDS is set,
+    e.g. "2", unless world is one of the listed sizes)."""
+    if torch.cuda.device_count() < world:
+        pytest.skip("needs %d GPUs" % world)
+    only = os.environ.get("RAFI_TEST_WORLDS")
+    if only and str(world) not in only.split(","):
+        pytest.skip("world %d not selected by RAFI_TEST_WORLDS" % world)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -23,7 +33,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, B, n, pattern, exchange, rounds, scatter=1):
+def _worker(rank, world, port, B, n, pattern, exchange, rounds, scatter=1, passes=0):
     import torch.distributed as dist
 
     import oracle
@@ -43,6 +53,7 @@ def _worker(rank, world, port, B, n, pattern, exchange, rounds, scatter=1):
     assert ctx.get_option(rafi.OPT_EXCHANGE) == exchange
     ctx.set_option(rafi.OPT_SCATTER, scatter)
     assert ctx.get_option(rafi.OPT_SCATTER) == scatter
+    ctx.set_option(rafi.OPT_CE_PASSES, passes)
     assert ctx.num_ranks == world and ctx.rank_of(0) == rank
     for rnd in range(rounds):
         m = n if rnd % 2 == 0 else n // 3
@@ -61,7 +72,7 @@ def _worker(rank, world, port, B, n, pattern, exchange, rounds, scatter=1):
         assert np.array_equal(ctx.matrix(), w.C())
         st = ctx.stats()
         assert st["num_in"] == w.num_incoming(rank)
-        if exchange != rafi.EXCHANGE_FUSED:
+        if exchange in (rafi.EXCHANGE_NCCL, rafi.EXCHANGE_PEER):  # staged: the send batch is readable
             assert np.array_equal(ctx.read_binned(0, st["n_out"]), w.binned(rank, st["n_out"]))
         assert np.array_equal(ctx.read_incoming(0), w.incoming(rank))
     # termination: nothing emitted anywhere -> 0 on every rank
@@ -73,13 +84,24 @@ def _worker(rank, world, port, B, n, pattern, exchange, rounds, scatter=1):
 
 @pytest.mark.parametrize("scatter", [1, 2, 3])  # THREADS, BULK (TMA bulk stores, to NVLink peers), ALIGNED
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("exchange", [1, 2, 3])  # NCCL, PEER, FUSED
+@pytest.mark.parametrize("exchange", [1, 2, 3, 4])  # NCCL, PEER, FUSED, CE
 @pytest.mark.parametrize("B,pattern", [(48, "uniform"), (44, "skewed"), (16, "all_to_one")])
 def test_multigpu_snapshot_parity(world, exchange, B, pattern, scatter):
-    if torch.cuda.device_count() < world:
-        pytest.skip("needs %d GPUs" % world)
+    _need(world)
     import torch.multiprocessing as mp
     mp.spawn(_worker, args=(world, _free_port(), B, 30011, pattern, exchange, 3, scatter), nprocs=world, join=True)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("passes", [1, 3, 16])
+@pytest.mark.parametrize("B,n", [(48, 30011), (44, 3000), (16, 200000)])
+def test_multigpu_ce_passes(world, passes, B, n):
+    """CE exchange: any number of scatter passes (more than there are blocks
+    included) gives the bit-exact result; copies of every pass land at the
+    right offsets of the peers' queues."""
+    _need(world)
+    import torch.multiprocessing as mp
+    mp.spawn(_worker, args=(world, _free_port(), B, n, "uniform", 4, 3, 1, passes), nprocs=world, join=True)
 
 
 def _worker_hybrid(rank, world, port, L, B, n, graph, scatter=1):
@@ -149,8 +171,7 @@ def _worker_hybrid(rank, world, port, L, B, n, graph, scatter=1):
 @pytest.mark.parametrize("graph", [False, True])
 @pytest.mark.parametrize("world,L", [(2, 2), (2, 4), (4, 2)])
 def test_multigpu_hybrid_local_ranks(world, L, graph, scatter):
-    if torch.cuda.device_count() < world:
-        pytest.skip("needs %d GPUs" % world)
+    _need(world)
     import torch.multiprocessing as mp
     mp.spawn(_worker_hybrid, args=(world, _free_port(), L, 44, 20011, graph, scatter), nprocs=world,
              join=True)
