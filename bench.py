@@ -47,7 +47,7 @@ def parse():
     p.add_argument("--item-bytes", type=int, default=DEF_B)
     p.add_argument("--pattern", default="uniform")
     p.add_argument("--exchange", default="auto", choices=["auto", "nccl", "peer", "fused", "ce"])
-    p.add_argument("--scatter", default="auto", choices=["auto", "threads", "bulk", "aligned"])
+    p.add_argument("--scatter", default="auto", choices=["auto", "threads", "bulk", "aligned", "units"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle cpu_baseline sample")
@@ -252,8 +252,9 @@ def main():
     exchange = {1: "nccl", 2: "peer", 3: "fused", 4: "ce"}[ctx.get_option(rafi.OPT_EXCHANGE)]
     if args.scatter != "auto":
         ctx.set_option(rafi.OPT_SCATTER, {"threads": rafi.SCATTER_THREADS, "bulk": rafi.SCATTER_BULK,
-                                          "aligned": rafi.SCATTER_ALIGNED}[args.scatter])
-    scatter = {1: "threads", 2: "bulk", 3: "aligned"}[ctx.get_option(rafi.OPT_SCATTER)]
+                                          "aligned": rafi.SCATTER_ALIGNED,
+                                          "units": rafi.SCATTER_UNITS}[args.scatter])
+    scatter = {1: "threads", 2: "bulk", 3: "aligned", 4: "units"}[ctx.get_option(rafi.OPT_SCATTER)]
     ctx_tile = ctx.get_option(rafi.OPT_TILE)
 
     # resident inputs (generated on the host by the shared generator, uploaded once)

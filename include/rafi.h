@@ -124,10 +124,13 @@ typedef struct {
                                       item size that is not a multiple of 4 or a tile that does not fit */
 
 #define RAFI_SCATTER_AUTO 0        /* BULK when supported, else THREADS */
-#define RAFI_SCATTER_THREADS 1     /* threads store every unit of every run (16/8/4/2/1-B coalesced stores) */
+#define RAFI_SCATTER_THREADS 1     /* threads store every run with coalesced stores: 16/8/4/2/1-B item units,
+                                      or, for 4-B units (item_bytes % 8 == 4, >= 16), 16-B-aligned chunks
+                                      gathered from the (at most two) items they cover */
 #define RAFI_SCATTER_BULK 2        /* runs are permuted in shared memory and written by TMA bulk stores
                                       (cp.async.bulk shared->global, local or NVLink peer); threads write
                                       only the unaligned < 16-B heads and tails; item_bytes % 4 == 0 */
+#define RAFI_SCATTER_UNITS 4       /* THREADS with item-unit stores only (no 16-B chunk gathering): comparison */
 #define RAFI_SCATTER_ALIGNED 3     /* runs are permuted in shared memory, placed congruent to their global
                                       address mod 16, and written by threads as 16-B-aligned vector
                                       stores whatever the item size; item_bytes % 4 == 0 */

@@ -1134,7 +1134,7 @@ int rafi_set_option(rafi_ctx* ctx, int key, long long v) {
       return RAFI_OK;
     }
     case RAFI_OPT_SCATTER: {
-      if (v < RAFI_SCATTER_AUTO || v > RAFI_SCATTER_ALIGNED) return RAFI_ERR_INVALID_ARG;
+      if (v < RAFI_SCATTER_AUTO || v > RAFI_SCATTER_UNITS) return RAFI_ERR_INVALID_ARG;
       const int old = c->scatter;
       c->scatter = (int)v;
       int rc = resolve_scatter(c);

@@ -33,6 +33,7 @@ namespace rafi_impl {
 #define RAFI_SCATTER_ILP 4
 #endif
 
+
 // Debug builds (build.py --variants "debug"): device-side bounds checks that
 // trap with a message (compute-sanitizer is not available on the GPU pool).
 #ifdef RAFI_DEBUG_BOUNDS
@@ -538,11 +539,11 @@ __device__ __forceinline__ void rank_chunk(const int32_t* __restrict__ dest_s, u
 //   Item index = O[l][d][t] (prefix over earlier tiles) + rank within the tile
 //   + dst_off[l][d], the per-destination base from k_plan: send_off_me[d]
 //   (staged) or recv_off_d[me] (FUSED).
-template <typename U, bool kStageItems, int kK, int kMinB>
+template <typename U, bool kStageItems, int kK, int kMinB, bool kChunk>
 __global__ void __launch_bounds__(kThreads, kMinB)
 k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint8_t* const* __restrict__ dst_table,
           const uint64_t* __restrict__ dst_off, const int* __restrict__ ovf, int L, int R, uint64_t cap, uint32_t T,
-          int cur, uint32_t B, uint32_t UPI, FastDiv divU, ScatterLayout lay, unsigned* __restrict__ wrap_done,
+          int cur, uint32_t B, uint32_t UPI, FastDiv divU, FastDiv divB, ScatterLayout lay, unsigned* __restrict__ wrap_done,
           CtrlDev* __restrict__ ctrl_w, const uint64_t* __restrict__ wrap_num_in, uint64_t g_lo, uint64_t g_hi) {
   if (ovf && *ovf) return;  // collective receive overflow: move nothing (Z3)
   extern __shared__ __align__(128) uint8_t smem[];
@@ -630,16 +631,68 @@ k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint
     // per-run destination base, shifted so that position p of run d lands at
     // base_d + p*B (runs are contiguous in both the tile order and the output)
     for (int d = tid; d < R; d += kThreads) {
-      RAFI_DCHECK((uint64_t)rstart[d] + ((d + 1 < R ? tcnt[d + 1] : nt) - tcnt[d]) <= cap,
-                  "destination run beyond the destination queue");
-      dbase[d] += (uintptr_t)(((int64_t)rstart[d] - (int64_t)tcnt[d]) * (int64_t)B);
+      const uint32_t cnt = (d + 1 < R ? tcnt[d + 1] : nt) - tcnt[d];
+      RAFI_DCHECK((uint64_t)rstart[d] + cnt <= cap, "destination run beyond the destination queue");
+      const uint32_t r0 = rstart[d];
+      const uintptr_t a = dbase[d] + (uintptr_t)r0 * B;  // first byte of the run
+      dbase[d] = a - (uintptr_t)tcnt[d] * B;
+      // kChunk: rstart is free from here on and holds the number of
+      // 16-byte-aligned chunks the run's bytes touch
+      if (kChunk) rstart[d] = cnt ? (uint32_t)(((a + (uintptr_t)cnt * B + 15) >> 4) - (a >> 4)) : 0u;
     }
     __syncthreads();
     // phase 4: coalesced write of every destination run
     const U* srcU = kStageItems ? reinterpret_cast<const U*>(st) : reinterpret_cast<const U*>(rk[l].out + t0 * B);
     // A thread walks its units in increasing order, so the run it is in only
     // moves forward: one shared-memory read (src_of) per unit besides the data.
-    if (UPI <= 64) {
+    if (kChunk) {
+      // items of 4-byte granularity (20, 28, 36, 44 B ...): a thread writes one
+      // 16-byte-aligned chunk of a run at a time,
+      // gathering its four words from the (at most two) items it overlaps, so a
+      // 44-B item costs 2.75 vector stores instead of 11 word stores
+      // rstart[d] holds run d's chunk count; a thread walks the runs forward,
+      // keeping [c0, c1) = the flat chunk range of the run it is in
+      const uint8_t* src8 = reinterpret_cast<const uint8_t*>(srcU);
+      int d = 0;
+      uint32_t c0 = 0, c1 = rstart[0];
+      for (uint32_t x = tid;; x += kThreads) {
+        while (x >= c1 && d < R) {
+          if (++d < R) { c0 = c1; c1 += rstart[d]; }
+        }
+        if (d >= R) break;
+        const uint32_t p0 = tcnt[d], p1 = d + 1 < R ? tcnt[d + 1] : nt;
+        const uintptr_t rs = dbase[d] + (uintptr_t)p0 * B, re = dbase[d] + (uintptr_t)p1 * B;
+        const uintptr_t g = ((rs >> 4) + (x - c0)) << 4;
+        RAFI_DCHECK(rs % 4 == 0 && g + 16 > rs && g < re, "chunk outside its run");
+        if (g >= rs && g + 16 <= re) {
+          const uint32_t o = (uint32_t)(g - rs), q = divB.div(o), e = o - q * B;
+          RAFI_DCHECK(e < B && q * B + e == o && p0 + q < p1 && (e + 16 <= B || p0 + q + 1 < p1), "chunk items");
+          const uint32_t s0 = (uint32_t)src_of[p0 + q] * B + e;
+          const uint32_t s1 = e + 16 > B ? (uint32_t)src_of[p0 + q + 1] * B + e - B : s0;
+          RAFI_DCHECK(s0 % 4 == 0 && s1 % 4 == 0 && ((uintptr_t)src8 & 3) == 0, "chunk source alignment");
+          uint32_t v[4];
+#ifdef RAFI_CHUNK_DIAG
+          if ((g & 15) || s0 + 16 > T * B + 16 || s1 + 16 > T * B + 16 || ((uintptr_t)src8 & 15)) {
+            printf("DIAG blk %d tid %d it %u d %d x %u p0 %u p1 %u rs %llx re %llx g %llx o %u q %u e %u s0 %u s1 %u src8 %p\n",
+                   (int)blockIdx.x, tid, it, d, x, p0, p1, (unsigned long long)rs, (unsigned long long)re,
+                   (unsigned long long)g, o, q, e, s0, s1, src8);
+            continue;
+          }
+#endif
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            v[j] = *reinterpret_cast<const uint32_t*>(src8 + (e + 4 * j < B ? s0 : s1) + 4 * j);
+          *reinterpret_cast<uint4*>(g) = make_uint4(v[0], v[1], v[2], v[3]);
+        } else {  // the run's first or last chunk: word by word
+          const uintptr_t w0 = g > rs ? g : rs, w1 = g + 16 < re ? g + 16 : re;
+          for (uintptr_t a = w0; a < w1; a += 4) {
+            const uint32_t o = (uint32_t)(a - rs), q = divB.div(o), e = o - q * B;
+            *reinterpret_cast<uint32_t*>(a) =
+                *reinterpret_cast<const uint32_t*>(src8 + (uint32_t)src_of[p0 + q] * B + e);
+          }
+        }
+      }
+    } else if (UPI <= 64) {
       const uint32_t units = nt * UPI;
       int d = 0;
       uint32_t nb = R > 1 ? tcnt[1] : nt;  // first position after run d
@@ -1073,7 +1126,12 @@ static uint32_t unit_for(uint64_t B, uintptr_t align_bits) {
 // two 110-KiB CTAs (longer tiles).  Measured with the cfg5 size sweep
 // (profiles/r01_scatter_variants.md).
 static int scatter_minb(uint64_t B) { return B <= 96 ? 4 : 2; }
-static uint32_t scatter_budget(uint64_t B) { return scatter_minb(B) == 4 ? 54u * 1024u : 110u * 1024u; }
+// Items of 17-24 B: 1024-item tiles at three CTAs/SM beat 512-item tiles at
+// four (cfg5 tile sweep, profiles/r01_suite_n1_tiles_threads.md).
+static uint32_t scatter_budget(uint64_t B) {
+  if (B > 16 && B <= 24) return 62u * 1024u;
+  return scatter_minb(B) == 4 ? 54u * 1024u : 110u * 1024u;
+}
 
 uint32_t choose_tile(uint64_t item_bytes) {
   // two pipeline stages (items + dests) plus 2 B/item of indices in ~110 KiB,
@@ -1149,36 +1207,39 @@ int launch_scan(Ctx* c, int plan_mode, unsigned long long* G_out) {
   return RAFI_OK;
 }
 
-template <typename U, int kK, int kMinB>
-static int launch_scatter_k(Ctx* c, bool fused, bool wrap, uint32_t UPI, int grid) {
-  const FastDiv dv(UPI);
-  const bool si = stage_items(c->tile, c->B);
-  const ScatterLayout lay = scatter_layout(c->tile, c->B, c->R, si);
-  uint8_t* const* table = fused ? (c->exchange_eff == RAFI_EXCHANGE_CE ? c->ce_table_dev : c->in_table_dev) : nullptr;
-  const uint64_t* off = c->off_dev;
-  const int* ovf = fused && c->exchange_eff != RAFI_EXCHANGE_CE ? c->ovf_dev : nullptr;
-  static int set_true = 0, set_false = 0;  // per instantiation: the largest smem opt-in already granted
-  if (si) {
-    auto k = k_scatter<U, true, kK, kMinB>;
-    if ((int)lay.total > set_true) {
-      RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
-      set_true = (int)lay.total;
-    }
-    k<<<grid, kThreads, lay.total, c->stream>>>(rank_table(c), c->ctrl, table, off, ovf, c->L, c->R, c->cap, c->tile,
-                                               c->cur, (uint32_t)c->B, UPI, dv, lay, wrap ? c->done_dev + 1 : nullptr,
-                                               c->ctrl, c->plan_dev, c->g_lo, c->g_hi);
-  } else {
-    auto k = k_scatter<U, false, kK, kMinB>;
-    if ((int)lay.total > set_false) {
-      RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
-      set_false = (int)lay.total;
-    }
-    k<<<grid, kThreads, lay.total, c->stream>>>(rank_table(c), c->ctrl, table, off, ovf, c->L, c->R, c->cap, c->tile,
-                                               c->cur, (uint32_t)c->B, UPI, dv, lay, wrap ? c->done_dev + 1 : nullptr,
-                                               c->ctrl, c->plan_dev, c->g_lo, c->g_hi);
+template <typename U, bool kSI, int kK, int kMinB, bool kChunk>
+static int launch_scatter_kk(Ctx* c, bool fused, bool wrap, uint32_t UPI, int grid, const ScatterLayout& lay) {
+  static int granted = 0;  // per instantiation: the largest smem opt-in already granted
+  auto k = k_scatter<U, kSI, kK, kMinB, kChunk>;
+  if ((int)lay.total > granted) {
+    RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
+    granted = (int)lay.total;
   }
+  uint8_t* const* table = fused ? (c->exchange_eff == RAFI_EXCHANGE_CE ? c->ce_table_dev : c->in_table_dev) : nullptr;
+  const int* ovf = fused && c->exchange_eff != RAFI_EXCHANGE_CE ? c->ovf_dev : nullptr;
+  k<<<grid, kThreads, lay.total, c->stream>>>(rank_table(c), c->ctrl, table, c->off_dev, ovf, c->L, c->R, c->cap,
+                                             c->tile, c->cur, (uint32_t)c->B, UPI, FastDiv(UPI),
+                                             FastDiv((uint32_t)c->B), lay, wrap ? c->done_dev + 1 : nullptr, c->ctrl,
+                                             c->plan_dev, c->g_lo, c->g_hi);
   RAFI_CK_CUDA(cudaGetLastError());
   return RAFI_OK;
+}
+
+// 16-byte chunk gathering (kChunk) for 4-byte units (B % 8 == 4, B >= 16):
+// 44 B goes from 4.43 to 5.41 TB/s.  8-byte units (24, 40 B) stay on unit
+// stores, which measured faster there (profiles/r01_suite_n1_cfg5_chunk.md).
+// RAFI_SCATTER_UNITS keeps unit stores everywhere (comparison).
+template <typename U, int kK, int kMinB>
+static int launch_scatter_k(Ctx* c, bool fused, bool wrap, uint32_t UPI, int grid) {
+  const bool si = stage_items(c->tile, c->B);
+  const ScatterLayout lay = scatter_layout(c->tile, c->B, c->R, si);
+  constexpr bool kCanChunk = sizeof(U) == 4;
+  const bool chunk = kCanChunk && c->B >= 16 && c->B % 16 != 0 && c->scatter_eff != RAFI_SCATTER_UNITS;
+  if (chunk)
+    return si ? launch_scatter_kk<U, true, kK, kMinB, kCanChunk>(c, fused, wrap, UPI, grid, lay)
+              : launch_scatter_kk<U, false, kK, kMinB, kCanChunk>(c, fused, wrap, UPI, grid, lay);
+  return si ? launch_scatter_kk<U, true, kK, kMinB, false>(c, fused, wrap, UPI, grid, lay)
+            : launch_scatter_kk<U, false, kK, kMinB, false>(c, fused, wrap, UPI, grid, lay);
 }
 
 template <typename U, int kMinB>

@@ -31,7 +31,7 @@ OPT_TILE = 3
 OPT_SELF_DIRECT = 4
 OPT_SCATTER = 5
 OPT_CE_PASSES = 6
-SCATTER_AUTO, SCATTER_THREADS, SCATTER_BULK, SCATTER_ALIGNED = 0, 1, 2, 3
+SCATTER_AUTO, SCATTER_THREADS, SCATTER_BULK, SCATTER_ALIGNED, SCATTER_UNITS = 0, 1, 2, 3, 4
 EXCHANGE_AUTO, EXCHANGE_NCCL, EXCHANGE_PEER, EXCHANGE_FUSED, EXCHANGE_CE = 0, 1, 2, 3, 4
 
 

@@ -81,14 +81,15 @@ CASES = [
 
 
 EXCHANGES = {"fused": 3, "peer": 2}
-SCATTERS = {"threads": rafi.SCATTER_THREADS, "bulk": rafi.SCATTER_BULK, "aligned": rafi.SCATTER_ALIGNED}
+SCATTERS = {"threads": rafi.SCATTER_THREADS, "bulk": rafi.SCATTER_BULK, "aligned": rafi.SCATTER_ALIGNED,
+            "units": rafi.SCATTER_UNITS}
 
 
 @pytest.mark.parametrize("scatter", sorted(SCATTERS))
 @pytest.mark.parametrize("exchange", sorted(EXCHANGES))
 @pytest.mark.parametrize("B,L,n,pattern", CASES)
 def test_forward_snapshot_parity(B, L, n, pattern, exchange, scatter):
-    if scatter != "threads" and (B % 4 or B > 256):
+    if scatter in ("bulk", "aligned") and (B % 4 or B > 256):
         pytest.skip("bulk scatter needs item_bytes % 4 == 0 and a 256-item tile in shared memory")
     inputs = make_inputs(L, n, B, pattern, 1234 + B, invalid_frac=0.01)
     cap = max(n * L, 1)
