@@ -47,6 +47,7 @@ def parse():
     p.add_argument("--item-bytes", type=int, default=DEF_B)
     p.add_argument("--pattern", default="uniform")
     p.add_argument("--exchange", default="auto", choices=["auto", "nccl", "peer", "fused", "ce"])
+    p.add_argument("--control", default="auto", choices=["auto", "nccl", "peer"])
     p.add_argument("--scatter", default="auto", choices=["auto", "threads", "bulk", "aligned", "units"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -256,6 +257,9 @@ def main():
                                           "units": rafi.SCATTER_UNITS}[args.scatter])
     scatter = {1: "threads", 2: "bulk", 3: "aligned", 4: "units"}[ctx.get_option(rafi.OPT_SCATTER)]
     ctx_tile = ctx.get_option(rafi.OPT_TILE)
+    if args.control != "auto":
+        ctx.set_option(rafi.OPT_CONTROL, {"nccl": rafi.CONTROL_NCCL, "peer": rafi.CONTROL_PEER}[args.control])
+    control = {1: "nccl", 2: "peer"}[ctx.get_option(rafi.OPT_CONTROL)] if N > 1 else None
 
     # resident inputs (generated on the host by the shared generator, uploaded once)
     items_h = synth.make_items(rank, 0, n, max(B, 16))[:, :B].copy()
@@ -413,7 +417,7 @@ def main():
         "data": "synthetic (synth/ SplitMix64 recipe; resident in HBM)", "config": workload_config(args, N),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clk, "phases_ms": ph, "kernels": kern, "exchange": exch, "exchange_transport": exchange,
-        "scatter_write": scatter, "tile": ctx_tile, "per_gpu_items_per_s": value / N,
+        "scatter_write": scatter, "tile": ctx_tile, "control": control, "per_gpu_items_per_s": value / N,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

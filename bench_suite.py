@@ -52,6 +52,7 @@ class Env:
         self.stream = self.torch.cuda.current_stream()
         self.scatter = {"auto": 0, "threads": 1, "bulk": 2, "aligned": 3, "units": 4}[getattr(args, "scatter", "auto")]
         self.tile = getattr(args, "tile", 0)
+        self.control = {"auto": 0, "nccl": 1, "peer": 2}[getattr(args, "control", "auto")]
 
     def configure(self, ctx):
         """Apply the --scatter choice (RAFI_OPT_SCATTER) to a new context."""
@@ -59,6 +60,8 @@ class Env:
             ctx.set_option(self.rafi.OPT_SCATTER, self.scatter)
         if self.tile:
             ctx.set_option(self.rafi.OPT_TILE, self.tile)
+        if self.control:
+            ctx.set_option(self.rafi.OPT_CONTROL, self.control)
         return ctx
 
     def ctx(self, B, cap, L=1):
@@ -148,7 +151,7 @@ def run_latency(env, args):
     torch = env.torch
     seed = synth.CONFIG_SEEDS[1]
     side = torch.cuda.Stream(device=env.dev)
-    ctx = env.rafi.Context(B, 2 * n, comm=env.comm, stream=side, local_ranks=L, device=env.local)
+    ctx = env.configure(env.rafi.Context(B, 2 * n, comm=env.comm, stream=side, local_ranks=L, device=env.local))
     G_dev = torch.zeros(1, dtype=torch.int64, device=env.dev)
     for l in range(L):
         ctx.drv_emit_synthetic(synth.PATTERNS["uniform"], seed, 0, n, local=l)
@@ -409,6 +412,7 @@ def main():
     p.add_argument("--items", type=int, default=0)
     p.add_argument("--scatter", default="auto", choices=["auto", "threads", "bulk", "aligned", "units"])
     p.add_argument("--tile", type=int, default=0, help="RAFI_OPT_TILE (0 = automatic)")
+    p.add_argument("--control", default="auto", choices=["auto", "nccl", "peer"])
     p.add_argument("--sizes", default="", help="cfg5: comma-separated item sizes (default: the full sweep)")
     args = p.parse_args()
     env = Env(args)

@@ -117,6 +117,8 @@ typedef struct {
 #define RAFI_OPT_SELF_DIRECT 4     /* reserved (self run placement); 0 */
 #define RAFI_OPT_CE_PASSES 6       /* RAFI_EXCHANGE_CE: scatter passes per forward, 1..16 (0 = automatic:
                                       about 2M items per pass, at most 8) */
+#define RAFI_OPT_CONTROL 7         /* count exchange and completion barrier of FUSED/CE forwards:
+                                      RAFI_CONTROL_* (default AUTO) */
 #define RAFI_OPT_SCATTER 5         /* how the binning scatter writes destination runs:
                                       RAFI_SCATTER_* (default AUTO).  Same result bytes either way.
                                       Only between rounds; re-chooses the tile unless RAFI_OPT_TILE
@@ -134,6 +136,13 @@ typedef struct {
 #define RAFI_SCATTER_ALIGNED 3     /* runs are permuted in shared memory, placed congruent to their global
                                       address mod 16, and written by threads as 16-B-aligned vector
                                       stores whatever the item size; item_bytes % 4 == 0 */
+
+#define RAFI_CONTROL_AUTO 0        /* PEER when every rank's queues are mapped, else NCCL */
+#define RAFI_CONTROL_NCCL 1        /* ncclAllGather of the count rows, ncclAllReduce as the completion barrier */
+#define RAFI_CONTROL_PEER 2        /* one small kernel pushes this process's count rows into every peer's
+                                      CUDA-IPC mailbox over NVLink and raises a flag (st.release.sys);
+                                      the completion barrier is a flag per process; both spin on
+                                      ld.acquire.sys (a peer that never arrives traps after 20 s) */
 
 #define RAFI_EXCHANGE_AUTO 0       /* FUSED when every rank's queues are addressable, else NCCL */
 #define RAFI_EXCHANGE_NCCL 1       /* stage the sorted batch, grouped ncclSend/ncclRecv (one local rank per process) */

@@ -43,7 +43,8 @@ static int alloc_dev(void** p, size_t bytes) {
 
 static void free_rank(LocalRank& r) {
   cudaFree(r.out); cudaFree(r.dest); cudaFree(r.binned[0]); cudaFree(r.binned[1]);
-  cudaFree(r.in); cudaFree(r.H); cudaFree(r.O);
+  cudaFree(r.in); cudaFree(r.H); cudaFree(r.O); cudaFree(r.mbox);
+  r.mbox = nullptr;
   r.out = nullptr; r.dest = nullptr; r.binned[0] = r.binned[1] = nullptr; r.in = nullptr;
   r.H = nullptr; r.O = nullptr;
 }
@@ -53,6 +54,7 @@ static void close_ipc(Ctx* c) {
   c->ipc_opened.clear();
   c->peer_binned.clear();
   c->peer_in.clear();
+  c->peer_mbox.clear();
   c->peer_ok = false;
 }
 
@@ -68,6 +70,9 @@ static int alloc_rank(Ctx* c, LocalRank& r, uint64_t cap) {
   const size_t hb = (size_t)std::max<uint64_t>(c->max_tiles, 1) * c->R * 4 + kPad;
   RAFI_CK(alloc_dev((void**)&r.H, hb));
   RAFI_CK(alloc_dev((void**)&r.O, hb));
+  const size_t mb = mbox_words(c->nprocs, c->R) * sizeof(unsigned long long);
+  RAFI_CK(alloc_dev((void**)&r.mbox, mb));
+  RAFI_CK_CUDA(cudaMemset(r.mbox, 0, mb));
   return RAFI_OK;
 }
 
@@ -85,14 +90,20 @@ static int upload_rank_table(Ctx* c) {
 // Every rank learns every rank's binned[0..1] and in pointers: local ones
 // directly, other processes' through CUDA IPC handles all-gathered over NCCL.
 // Collective.  peer_ok is decided identically on all ranks.
-static constexpr int kMapped = 3;  // binned[0], binned[1], in
+static constexpr int kMapped = 4;  // binned[0], binned[1], in, mbox
 
-static uint8_t* mapped_buf(LocalRank& r, int b) { return b < 2 ? (r.binned[b] ? r.binned[b] : r.binned[0]) : r.in; }
+static uint8_t* mapped_buf(LocalRank& r, int b) {
+  return b < 2 ? (r.binned[b] ? r.binned[b] : r.binned[0]) : b == 2 ? r.in : reinterpret_cast<uint8_t*>(r.mbox);
+}
 
 static int upload_in_table(Ctx* c) {
   std::vector<uint8_t*> t(c->R, nullptr);
   for (int g = 0; g < c->R; ++g) t[g] = c->peer_in.empty() ? nullptr : c->peer_in[g];
   RAFI_CK_CUDA(cudaMemcpyAsync(c->in_table_dev, t.data(), sizeof(uint8_t*) * c->R, cudaMemcpyHostToDevice, c->stream));
+  std::vector<unsigned long long*> m(c->nprocs, nullptr);
+  for (int p = 0; p < c->nprocs; ++p) m[p] = c->peer_mbox.empty() ? nullptr : c->peer_mbox[(size_t)p * c->L];
+  RAFI_CK_CUDA(cudaMemcpyAsync(c->mbox_table_dev, m.data(), sizeof(void*) * c->nprocs, cudaMemcpyHostToDevice,
+                               c->stream));
   RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
   return RAFI_OK;
 }
@@ -101,9 +112,11 @@ static int exchange_peer_pointers(Ctx* c) {
   close_ipc(c);
   c->peer_binned.assign((size_t)c->R * 2, nullptr);
   c->peer_in.assign((size_t)c->R, nullptr);
+  c->peer_mbox.assign((size_t)c->R, nullptr);
   auto place = [&](int g, int b, uint8_t* p) {
     if (b < 2) c->peer_binned[(size_t)g * 2 + b] = p;
-    else c->peer_in[g] = p;
+    else if (b == 2) c->peer_in[g] = p;
+    else c->peer_mbox[g] = reinterpret_cast<unsigned long long*>(p);
   };
   for (int l = 0; l < c->L; ++l)
     for (int b = 0; b < kMapped; ++b) place(c->proc * c->L + l, b, mapped_buf(c->lr[l], b));
@@ -156,6 +169,7 @@ static int exchange_peer_pointers(Ctx* c) {
     close_ipc(c);
     c->peer_binned.assign((size_t)c->R * 2, nullptr);
     c->peer_in.assign((size_t)c->R, nullptr);
+    c->peer_mbox.assign((size_t)c->R, nullptr);
   }
   if (rc == RAFI_OK) rc = upload_in_table(c);
   return rc;
@@ -217,6 +231,7 @@ static int resolve_exchange(Ctx* c) {
     return RAFI_ERR_UNSUPPORTED;
   }
   if (x == RAFI_EXCHANGE_CE) RAFI_CK(ensure_ce(c));
+  c->ctl_peer = c->nprocs > 1 && c->peer_ok && c->control != RAFI_CONTROL_NCCL;
   c->exchange_eff = x;
   return RAFI_OK;
 }
@@ -287,6 +302,7 @@ static void destroy_ctx(Ctx* c) {
   for (auto& r : c->lr) free_rank(r);
   cudaFree(c->rank_dev); cudaFree(c->ctrl); cudaFree(c->runs_dev); cudaFree(c->plan_dev);
   cudaFree(c->off_dev); cudaFree(c->ovf_dev); cudaFree(c->in_table_dev); cudaFree(c->done_dev);
+  cudaFree(c->mbox_table_dev);
   cudaFree(c->stage);
   if (c->io_in) {
     cudaStreamSynchronize(c->io_in); cudaStreamSynchronize(c->io_out);
@@ -349,6 +365,7 @@ static int create(Ctx** out, const rafi_create_params* p) {
   if ((rc = alloc_dev((void**)&c->ovf_dev, 2 * sizeof(int)))) return fail(rc);
   if ((rc = alloc_dev((void**)&c->done_dev, 2 * sizeof(unsigned)))) return fail(rc);
   if ((rc = alloc_dev((void**)&c->in_table_dev, sizeof(uint8_t*) * c->R))) return fail(rc);
+  if ((rc = alloc_dev((void**)&c->mbox_table_dev, sizeof(void*) * c->nprocs))) return fail(rc);
   if (cudaMallocHost((void**)&c->ctrl_host, ctrl_c_bytes(c)) != cudaSuccess ||
       cudaMallocHost((void**)&c->runs_host, sizeof(CopyRun) * c->L * c->R) != cudaSuccess ||
       cudaMallocHost((void**)&c->plan_host, sizeof(uint64_t) * c->L) != cudaSuccess) {
@@ -432,8 +449,11 @@ static int enqueue_fused(Ctx* c, unsigned long long* G_dev, bool T) {
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[2], c->stream));
   if (c->nprocs > 1) {
     // a5: the whole R x R matrix on every rank; offsets + overflow on device
-    RAFI_CK_NCCL(ncclAllGather(c->Cdev + (size_t)c->proc * L * R, c->Cdev, (size_t)L * R, ncclUint64, c->comm,
-                               c->stream));
+    if (c->ctl_peer)
+      RAFI_CK(launch_ctl_counts(c));
+    else
+      RAFI_CK_NCCL(ncclAllGather(c->Cdev + (size_t)c->proc * L * R, c->Cdev, (size_t)L * R, ncclUint64, c->comm,
+                                 c->stream));
     RAFI_CK(launch_plan(c, true, G_dev));
   }
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[3], c->stream));
@@ -442,9 +462,13 @@ static int enqueue_fused(Ctx* c, unsigned long long* G_dev, bool T) {
   RAFI_CK(launch_scatter(c, true, true));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[4], c->stream));
   // every push has landed before any rank's next app kernel reads its queue:
-  // the all-reduce completes only after every rank's scatter kernel completed
-  if (c->nprocs > 1)
-    RAFI_CK_NCCL(ncclAllReduce(c->ovf_dev + 1, c->ovf_dev + 1, 1, ncclInt32, ncclMax, c->comm, c->stream));
+  // the barrier completes only after every rank's scatter kernel completed
+  if (c->nprocs > 1) {
+    if (c->ctl_peer)
+      RAFI_CK(launch_ctl_barrier(c));
+    else
+      RAFI_CK_NCCL(ncclAllReduce(c->ovf_dev + 1, c->ovf_dev + 1, 1, ncclInt32, ncclMax, c->comm, c->stream));
+  }
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[5], c->stream));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[6], c->stream));
   return RAFI_OK;
@@ -647,7 +671,10 @@ static int64_t forward_ce(Ctx* c) {
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[1], c->stream));
   RAFI_CK(launch_scan(c, 0));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[2], c->stream));
-  RAFI_CK_NCCL(ncclAllGather(c->Cdev + (size_t)me * R, c->Cdev, (size_t)R, ncclUint64, c->comm, c->stream));
+  if (c->ctl_peer)
+    RAFI_CK(launch_ctl_counts(c));
+  else
+    RAFI_CK_NCCL(ncclAllGather(c->Cdev + (size_t)me * R, c->Cdev, (size_t)R, ncclUint64, c->comm, c->stream));
   // passes: this round's item count is not on the host yet, so the previous
   // round's sizes it (any K gives the same bytes; K only sets the overlap)
   int K = c->ce_passes;
@@ -707,8 +734,11 @@ static int64_t forward_ce(Ctx* c) {
     RAFI_CK_CUDA(cudaEventRecord(c->ce_done[d], c->ce_streams[d]));
     RAFI_CK_CUDA(cudaStreamWaitEvent(c->stream, c->ce_done[d], 0));
   }
-  // every rank's copies into every queue have completed once the all-reduce has
-  RAFI_CK_NCCL(ncclAllReduce(c->ovf_dev + 1, c->ovf_dev + 1, 1, ncclInt32, ncclMax, c->comm, c->stream));
+  // every rank's copies into every queue have completed once the barrier has
+  if (c->ctl_peer)
+    RAFI_CK(launch_ctl_barrier(c));
+  else
+    RAFI_CK_NCCL(ncclAllReduce(c->ovf_dev + 1, c->ovf_dev + 1, 1, ncclInt32, ncclMax, c->comm, c->stream));
   if (T) {
     RAFI_CK_CUDA(cudaEventRecord(c->ev[5], c->stream));
     RAFI_CK_CUDA(cudaEventRecord(c->ev[6], c->stream));
@@ -1143,6 +1173,15 @@ int rafi_set_option(rafi_ctx* ctx, int key, long long v) {
       return RAFI_OK;
     }
     case RAFI_OPT_SELF_DIRECT: return v == 0 ? RAFI_OK : RAFI_ERR_UNSUPPORTED;
+    case RAFI_OPT_CONTROL:
+      if (v < RAFI_CONTROL_AUTO || v > RAFI_CONTROL_PEER) return RAFI_ERR_INVALID_ARG;
+      if (v == RAFI_CONTROL_PEER && c->nprocs > 1 && !c->peer_ok) {
+        set_error("PEER control needs every rank's mailbox mapped (CUDA IPC failed)");
+        return RAFI_ERR_UNSUPPORTED;
+      }
+      c->control = (int)v;
+      c->ctl_peer = c->nprocs > 1 && c->peer_ok && c->control != RAFI_CONTROL_NCCL;
+      return RAFI_OK;
     case RAFI_OPT_CE_PASSES:
       if (v < 0 || v > Ctx::kMaxPasses) return RAFI_ERR_INVALID_ARG;
       c->ce_passes = (int)v;
@@ -1160,6 +1199,7 @@ int rafi_get_option(const rafi_ctx* ctx, int key, long long* v) {
     case RAFI_OPT_TILE: *v = c->tile; return RAFI_OK;
     case RAFI_OPT_SCATTER: *v = c->scatter_eff; return RAFI_OK;
     case RAFI_OPT_CE_PASSES: *v = c->ce_passes; return RAFI_OK;
+    case RAFI_OPT_CONTROL: *v = c->ctl_peer ? RAFI_CONTROL_PEER : RAFI_CONTROL_NCCL; return RAFI_OK;
     case RAFI_OPT_SELF_DIRECT: *v = 0; return RAFI_OK;
     default: return RAFI_ERR_INVALID_ARG;
   }

@@ -67,8 +67,14 @@ struct CopyRun {
   unsigned long long count;  // items
 };
 
+// Peer control mailbox (one per process, CUDA-IPC mapped by every peer), u64
+// words: [0] epoch (local), [8, 8+P) count flags, [8+P, 8+2P) completion
+// flags, [8+2P, 8+2P+R*R) the count matrix as the peers push their rows.
+inline size_t mbox_words(int P, int R) { return 8 + 2 * (size_t)P + (size_t)R * R; }
+
 struct LocalRank {
   uint8_t* out = nullptr;     // outgoing queue (emit target)
+  unsigned long long* mbox = nullptr;  // peer control mailbox (used for local rank 0)
   int32_t* dest = nullptr;    // destination per slot
   uint8_t* binned[2] = {nullptr, nullptr};  // send batches (double-buffered for PEER)
   uint8_t* in = nullptr;      // incoming queue
@@ -118,6 +124,10 @@ struct Ctx {
   unsigned* done_dev = nullptr;       // [2] last-block counters (scan+plan, scatter+wrap-up)
   uint8_t** in_table_dev = nullptr;   // [R] every global rank's incoming queue (local or IPC-mapped)
   std::vector<uint8_t*> peer_in;      // host copy of in_table
+  std::vector<unsigned long long*> peer_mbox;  // [R] every global rank's mailbox (local or IPC-mapped)
+  unsigned long long** mbox_table_dev = nullptr;  // [P] mailbox of each process's local rank 0
+  int control = RAFI_CONTROL_AUTO;     // RAFI_OPT_CONTROL
+  bool ctl_peer = false;               // count exchange + completion barrier over peer mailboxes
   uint64_t* plan_host = nullptr;      // [L] pinned
   // peer pointers to every global rank's binned buffers ([R][2]); local ones
   // are our own allocations, remote ones are CUDA-IPC mappings
@@ -179,6 +189,8 @@ int launch_plan(Ctx* c, bool fused, unsigned long long* G_out = nullptr);
 int launch_copy(Ctx* c, int nruns_per_dest);
 int launch_wrapup(Ctx* c);
 int launch_pass_bounds(Ctx* c, int K);
+int launch_ctl_counts(Ctx* c);
+int launch_ctl_barrier(Ctx* c);
 size_t scatter_smem_bytes(uint32_t tile, uint64_t item_bytes, int R);
 
 }  // namespace rafi_impl

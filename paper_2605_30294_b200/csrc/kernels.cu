@@ -1090,6 +1090,94 @@ int launch_pass_bounds(Ctx* c, int K) {
   return RAFI_OK;
 }
 
+// ---------------------------------------------------------------- a5/a8 peer control
+
+// The count exchange and the completion barrier of a FUSED/CE
+// forward without NCCL: every process owns a mailbox (mbox_words), CUDA-IPC
+// mapped by every peer.  A round's epoch is the local counter mbox[0], bumped
+// in lockstep by every process.
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Wait until *flag >= e; a peer that never arrives is a hang: trap after 20 s.
+__device__ void spin_until(const unsigned long long* flag, unsigned long long e) {
+  const unsigned long long t0 = globaltimer_ns();
+  while (ld_acquire_sys(flag) < e) {
+    __nanosleep(32);
+    if (globaltimer_ns() - t0 > 20000000000ull) {
+      printf("rafi: peer control flag timed out (epoch %llu)\n", e);
+      __trap();
+    }
+  }
+}
+
+// Count exchange: push this process's L count rows into every process's
+// mailbox, raise its count flag there, wait for every process's flag, then
+// copy the whole R x R matrix into Cdev (where k_plan and the host read it).
+__global__ void __launch_bounds__(256) k_ctl_counts(unsigned long long* const* __restrict__ mbox, uint64_t* Cdev,
+                                                    int proc, int P, int L, int R) {
+  __shared__ unsigned long long se;
+  unsigned long long* mine = mbox[proc];
+  const int tid = threadIdx.x;
+  if (tid == 0) { se = mine[0] + 1; mine[0] = se; }
+  __syncthreads();
+  const unsigned long long e = se;
+  const size_t C0 = 8 + 2 * (size_t)P, row0 = (size_t)proc * L * R, n = (size_t)L * R;
+  for (size_t x = tid; x < (size_t)P * n; x += blockDim.x) {
+    const size_t p = x / n, i = x - p * n;
+    mbox[p][C0 + row0 + i] = Cdev[row0 + i];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence_system();
+    for (int p = 0; p < P; ++p) st_release_sys(&mbox[p][8 + proc], e);
+  }
+  for (int p = tid; p < P; p += blockDim.x) spin_until(&mine[8 + p], e);
+  __syncthreads();
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  for (size_t x = tid; x < (size_t)R * R; x += blockDim.x)
+    Cdev[x] = *reinterpret_cast<volatile unsigned long long*>(&mine[C0 + x]);
+}
+
+// Completion barrier: every push of this round (issued by the kernels before
+// this one on the stream) is visible system-wide, then the flag goes up in
+// every mailbox; return once every process's flag is up.
+__global__ void k_ctl_barrier(unsigned long long* const* __restrict__ mbox, int proc, int P) {
+  unsigned long long* mine = mbox[proc];
+  const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&mine[0]);
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int p = 0; p < P; ++p) st_release_sys(&mbox[p][8 + P + proc], e);
+  }
+  for (int p = threadIdx.x; p < P; p += blockDim.x) spin_until(&mine[8 + P + p], e);
+  __syncthreads();
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+
+int launch_ctl_counts(Ctx* c) {
+  k_ctl_counts<<<1, 256, 0, c->stream>>>(c->mbox_table_dev, c->Cdev, c->proc, c->nprocs, c->L, c->R);
+  RAFI_CK_CUDA(cudaGetLastError());
+  c->launches += 1; c->fwd_launches += 1;
+  return RAFI_OK;
+}
+
+int launch_ctl_barrier(Ctx* c) {
+  k_ctl_barrier<<<1, 32, 0, c->stream>>>(c->mbox_table_dev, c->proc, c->nprocs);
+  RAFI_CK_CUDA(cudaGetLastError());
+  c->launches += 1; c->fwd_launches += 1;
+  return RAFI_OK;
+}
+
 // ---------------------------------------------------------------- a7 wrap-up
 
 __global__ void k_wrapup(CtrlDev* ctrl, const uint64_t* num_in, int L, const int* ovf) {

@@ -33,7 +33,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, B, n, pattern, exchange, rounds, scatter=1, passes=0):
+def _worker(rank, world, port, B, n, pattern, exchange, rounds, scatter=1, passes=0, control=0):
     import torch.distributed as dist
 
     import oracle
@@ -54,6 +54,9 @@ def _worker(rank, world, port, B, n, pattern, exchange, rounds, scatter=1, passe
     ctx.set_option(rafi.OPT_SCATTER, scatter)
     assert ctx.get_option(rafi.OPT_SCATTER) == scatter
     ctx.set_option(rafi.OPT_CE_PASSES, passes)
+    ctx.set_option(rafi.OPT_CONTROL, control)
+    if control:
+        assert ctx.get_option(rafi.OPT_CONTROL) == control
     assert ctx.num_ranks == world and ctx.rank_of(0) == rank
     for rnd in range(rounds):
         m = n if rnd % 2 == 0 else n // 3
@@ -102,6 +105,18 @@ def test_multigpu_ce_passes(world, passes, B, n):
     _need(world)
     import torch.multiprocessing as mp
     mp.spawn(_worker, args=(world, _free_port(), B, n, "uniform", 4, 3, 1, passes), nprocs=world, join=True)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("control", [1, 2])  # NCCL collectives, PEER mailboxes over NVLink
+@pytest.mark.parametrize("exchange", [3, 4])  # FUSED, CE
+def test_multigpu_control_modes(world, control, exchange):
+    """Count exchange + completion barrier through NCCL or through the peer
+    mailboxes: same bytes, same G, several rounds (epochs) in a row."""
+    _need(world)
+    import torch.multiprocessing as mp
+    mp.spawn(_worker, args=(world, _free_port(), 48, 20011, "skewed", exchange, 5, 1, 0, control), nprocs=world,
+             join=True)
 
 
 def _worker_hybrid(rank, world, port, L, B, n, graph, scatter=1):
