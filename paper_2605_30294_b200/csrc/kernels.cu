@@ -114,6 +114,16 @@ k_emit_bulk(const uint8_t* __restrict__ items, const int32_t* __restrict__ dests
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const U* itemsU = reinterpret_cast<const U*>(items);
   U* outU = reinterpret_cast<U*>(out);
+  // the next tile's destinations are loaded while this tile's items move
+  int dnext[kEmitK];
+  auto load_dests = [&](uint64_t g) {
+#pragma unroll
+    for (int k = 0; k < kEmitK; ++k) {
+      const uint64_t i = g * kEmitTile + w * 32 * kEmitK + k * 32 + lane;
+      dnext[k] = i < n ? dests[i] : -1;
+    }
+  };
+  load_dests(blockIdx.x);
   for (uint64_t g = blockIdx.x; g * kEmitTile < n; g += gridDim.x) {
     const uint64_t t0 = g * kEmitTile;
     const uint32_t nt = (uint32_t)umin64(kEmitTile, n - t0);
@@ -123,7 +133,7 @@ k_emit_bulk(const uint8_t* __restrict__ items, const int32_t* __restrict__ dests
 #pragma unroll
     for (int k = 0; k < kEmitK; ++k) {
       const uint32_t il = w * 32 * kEmitK + k * 32 + lane;
-      int d = il < nt ? dests[t0 + il] : -1;
+      int d = il < nt ? dnext[k] : -1;
       const bool valid = il < nt && (unsigned)d < (unsigned)R;
       const unsigned b = __ballot_sync(kFull, valid);
       dk[k] = valid ? d : -1;
@@ -152,7 +162,20 @@ k_emit_bulk(const uint8_t* __restrict__ items, const int32_t* __restrict__ dests
     }
     __syncthreads();
     const uint32_t nkeep = base >= cap ? 0u : (uint32_t)umin64(nvalid, cap - base);
-    if (UPI <= 64) {
+    load_dests(g + gridDim.x);
+    if (nvalid == nt) {
+      // every destination valid (the common case): slot order = tile order,
+      // one contiguous span, 4 independent units in flight per thread
+      const U* sp = itemsU + t0 * UPI;
+      U* dp = outU + base * UPI;
+      const uint32_t units = nkeep * UPI;
+      uint32_t x = tid;
+      for (; x + 3 * kThreads < units; x += 4 * kThreads) {
+        const U a = sp[x], b = sp[x + kThreads], c = sp[x + 2 * kThreads], d = sp[x + 3 * kThreads];
+        dp[x] = a; dp[x + kThreads] = b; dp[x + 2 * kThreads] = c; dp[x + 3 * kThreads] = d;
+      }
+      for (; x < units; x += kThreads) dp[x] = sp[x];
+    } else if (UPI <= 64) {
       const uint32_t units = nkeep * UPI;
       for (uint32_t x = tid; x < units; x += kThreads) {
         const uint32_t p = divU.div(x), u = x - p * UPI;
@@ -1112,9 +1135,8 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 // Wait until *flag >= e; a peer that never arrives is a hang: trap after 20 s.
 __device__ void spin_until(const unsigned long long* flag, unsigned long long e) {
   const unsigned long long t0 = globaltimer_ns();
-  while (ld_acquire_sys(flag) < e) {
-    __nanosleep(32);
-    if (globaltimer_ns() - t0 > 20000000000ull) {
+  for (uint32_t i = 1; ld_acquire_sys(flag) < e; ++i) {
+    if ((i & 1023) == 0 && globaltimer_ns() - t0 > 20000000000ull) {
       printf("rafi: peer control flag timed out (epoch %llu)\n", e);
       __trap();
     }

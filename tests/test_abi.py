@@ -112,3 +112,21 @@ def test_plan_overflow_is_global(L):
     for d in range(2):
         assert rafi.plan(Cm, 4, d)["overflow"]     # every rank decides alike (Z3)
     assert not rafi.plan(Cm, 5, 0)["overflow"]
+
+
+def test_binding_constants_match_header():
+    """Every status code and option value the Python binding names equals the
+    #define in include/rafi.h (the binding is marshalling only)."""
+    txt = open(os.path.join(ROOT, "include", "rafi.h")).read()
+    defs = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define RAFI_([A-Z0-9_]+)\s+\(?(-?\d+)\)?", txt)}
+    defs.update({m.group(1): int(m.group(2)) for m in re.finditer(r"\bRAFI_([A-Z0-9_]+)\s*=\s*(-?\d+)", txt)})
+    names = [n for n in dir(rafi) if re.fullmatch(r"(ERR_[A-Z_]+|OPT_[A-Z_]+|EXCHANGE_[A-Z]+|SCATTER_[A-Z]+|"
+                                                 r"CONTROL_[A-Z]+|OK)", n)]
+    assert len(names) >= 25
+    for n in names:
+        assert n in defs, "RAFI_%s missing from rafi.h" % n
+        assert getattr(rafi, n) == defs[n], n
+    for prefix in ("OPT_", "EXCHANGE_", "SCATTER_", "CONTROL_"):
+        for d in defs:
+            if d.startswith(prefix):
+                assert hasattr(rafi, d), "binding lacks %s" % d
