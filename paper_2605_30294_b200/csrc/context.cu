@@ -444,31 +444,31 @@ static int enqueue_fused(Ctx* c, unsigned long long* G_dev, bool T) {
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[0], c->stream));
   RAFI_CK(launch_hist(c));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[1], c->stream));
-  // a3 (+ a5's plan when this process holds every rank: the scan's last block plans)
-  RAFI_CK(launch_scan(c, c->nprocs == 1 ? 2 : 0, G_dev));
+  // a3 (+ a5's plan when this process holds every rank: the scan's last block
+  // plans; with peer control it first exchanges the counts through the
+  // mailboxes, so one kernel does scan + count exchange + plan)
+  const bool peer = c->nprocs > 1 && c->ctl_peer;
+  RAFI_CK(launch_scan(c, (c->nprocs == 1 || peer) ? 2 : 0, G_dev, peer));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[2], c->stream));
-  if (c->nprocs > 1) {
+  if (c->nprocs > 1 && !peer) {
     // a5: the whole R x R matrix on every rank; offsets + overflow on device
-    if (c->ctl_peer)
-      RAFI_CK(launch_ctl_counts(c));
-    else
-      RAFI_CK_NCCL(ncclAllGather(c->Cdev + (size_t)c->proc * L * R, c->Cdev, (size_t)L * R, ncclUint64, c->comm,
-                                 c->stream));
+    RAFI_CK_NCCL(ncclAllGather(c->Cdev + (size_t)c->proc * L * R, c->Cdev, (size_t)L * R, ncclUint64, c->comm,
+                               c->stream));
     RAFI_CK(launch_plan(c, true, G_dev));
   }
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[3], c->stream));
   // a4 + a6: stable scatter, each destination run written into its receiver's
-  // queue; a7 wrap-up by its last block (skipped on overflow)
-  RAFI_CK(launch_scatter(c, true, true));
+  // queue; a7 wrap-up by its last block (skipped on overflow), and with peer
+  // control the completion barrier after it
+  c->scatter_barrier = peer;
+  const int rc = launch_scatter(c, true, true);
+  c->scatter_barrier = false;
+  RAFI_CK(rc);
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[4], c->stream));
   // every push has landed before any rank's next app kernel reads its queue:
-  // the barrier completes only after every rank's scatter kernel completed
-  if (c->nprocs > 1) {
-    if (c->ctl_peer)
-      RAFI_CK(launch_ctl_barrier(c));
-    else
-      RAFI_CK_NCCL(ncclAllReduce(c->ovf_dev + 1, c->ovf_dev + 1, 1, ncclInt32, ncclMax, c->comm, c->stream));
-  }
+  // the all-reduce completes only after every rank's scatter kernel completed
+  if (c->nprocs > 1 && !peer)
+    RAFI_CK_NCCL(ncclAllReduce(c->ovf_dev + 1, c->ovf_dev + 1, 1, ncclInt32, ncclMax, c->comm, c->stream));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[5], c->stream));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[6], c->stream));
   return RAFI_OK;
@@ -669,11 +669,9 @@ static int64_t forward_ce(Ctx* c) {
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[0], c->stream));
   RAFI_CK(launch_hist(c));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[1], c->stream));
-  RAFI_CK(launch_scan(c, 0));
+  RAFI_CK(launch_scan(c, 0, nullptr, c->ctl_peer));  // peer control: counts exchanged by its last block
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[2], c->stream));
-  if (c->ctl_peer)
-    RAFI_CK(launch_ctl_counts(c));
-  else
+  if (!c->ctl_peer)
     RAFI_CK_NCCL(ncclAllGather(c->Cdev + (size_t)me * R, c->Cdev, (size_t)R, ncclUint64, c->comm, c->stream));
   // passes: this round's item count is not on the host yet, so the previous
   // round's sizes it (any K gives the same bytes; K only sets the overlap)

@@ -128,6 +128,7 @@ struct Ctx {
   unsigned long long** mbox_table_dev = nullptr;  // [P] mailbox of each process's local rank 0
   int control = RAFI_CONTROL_AUTO;     // RAFI_OPT_CONTROL
   bool ctl_peer = false;               // count exchange + completion barrier over peer mailboxes
+  bool scatter_barrier = false;        // the next scatter launch ends with the peer completion barrier
   uint64_t* plan_host = nullptr;      // [L] pinned
   // peer pointers to every global rank's binned buffers ([R][2]); local ones
   // are our own allocations, remote ones are CUDA-IPC mappings
@@ -183,7 +184,7 @@ bool perm_supported(uint64_t item_bytes);
 size_t perm_smem_bytes(int mode, uint32_t tile, uint64_t item_bytes, int R);
 int launch_emit_bulk(Ctx* c, int local, const uint8_t* items, const int32_t* dests, uint64_t n);
 int launch_hist(Ctx* c);
-int launch_scan(Ctx* c, int plan_mode, unsigned long long* G_out = nullptr);
+int launch_scan(Ctx* c, int plan_mode, unsigned long long* G_out = nullptr, bool ctl = false);
 int launch_scatter(Ctx* c, bool fused, bool wrap);
 int launch_plan(Ctx* c, bool fused, unsigned long long* G_out = nullptr);
 int launch_copy(Ctx* c, int nruns_per_dest);

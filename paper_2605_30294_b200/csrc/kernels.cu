@@ -386,6 +386,93 @@ __device__ __forceinline__ bool last_block(unsigned* done) {
   return s_last;
 }
 
+// ---------------------------------------------------------------- a5/a8 peer control
+
+// The count exchange (PAPER:126) and the completion barrier of a FUSED/CE
+// forward without NCCL: every process owns a mailbox (mbox_words), CUDA-IPC
+// mapped by every peer.  A round's epoch is the local counter mbox[0], bumped
+// in lockstep by every process.  Writers order their data before a flag with
+// one system-scope fence and relaxed flag stores; readers poll with
+// ld.acquire.sys.
+struct PeerCtl {
+  unsigned long long* const* mbox;  // [P] mailboxes (local or IPC-mapped), nullptr = off
+  int proc, P;
+};
+
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Wait until *flag >= e; a peer that never arrives is a hang: trap after 20 s.
+__device__ void spin_until(const unsigned long long* flag, unsigned long long e) {
+  const unsigned long long t0 = globaltimer_ns();
+  for (uint32_t i = 1; ld_acquire_sys(flag) < e; ++i) {
+    if ((i & 1023) == 0 && globaltimer_ns() - t0 > 20000000000ull) {
+      printf("rafi: peer control flag timed out (epoch %llu)\n", e);
+      __trap();
+    }
+  }
+}
+
+// Count exchange by one whole block: push this process's L count rows
+// (Cdev rows proc*L ..) into every process's mailbox, raise this process's
+// count flag there, wait for every process's flag, then copy the whole R x R
+// matrix into Cdev (where the plan and the host read it).
+__device__ void ctl_counts_block(const PeerCtl& pc, uint64_t* Cdev, int L, int R) {
+  __shared__ unsigned long long se;
+  unsigned long long* mine = pc.mbox[pc.proc];
+  const int tid = threadIdx.x, P = pc.P;
+  if (tid == 0) { se = mine[0] + 1; mine[0] = se; }
+  __syncthreads();
+  const unsigned long long e = se;
+  const size_t C0 = 8 + 2 * (size_t)P, row0 = (size_t)pc.proc * L * R, n = (size_t)L * R;
+  for (size_t x = tid; x < (size_t)P * n; x += blockDim.x) {
+    const size_t p = x / n, i = x - p * n;
+    pc.mbox[p][C0 + row0 + i] = Cdev[row0 + i];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence_system();  // the rows before the flags, at every peer
+    for (int p = 0; p < P; ++p) st_relaxed_sys(&pc.mbox[p][8 + pc.proc], e);
+  }
+  for (int p = tid; p < P; p += blockDim.x) spin_until(&mine[8 + p], e);
+  __syncthreads();
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  for (size_t x = tid; x < (size_t)R * R; x += blockDim.x)
+    Cdev[x] = *reinterpret_cast<volatile unsigned long long*>(&mine[C0 + x]);
+  __syncthreads();
+}
+
+// Completion barrier by one whole block: this process's pushes of the round
+// (made visible system-wide before the call) precede its flag in every
+// mailbox; return once every process's flag is up.
+__device__ void ctl_barrier_block(const PeerCtl& pc) {
+  unsigned long long* mine = pc.mbox[pc.proc];
+  const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&mine[0]);
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int p = 0; p < pc.P; ++p) st_relaxed_sys(&pc.mbox[p][8 + pc.P + pc.proc], e);
+  }
+  for (int p = threadIdx.x; p < pc.P; p += blockDim.x) spin_until(&mine[8 + pc.P + p], e);
+  __syncthreads();
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(256) k_ctl_counts(PeerCtl pc, uint64_t* Cdev, int L, int R) {
+  ctl_counts_block(pc, Cdev, L, R);
+}
+
+__global__ void k_ctl_barrier(PeerCtl pc) { ctl_barrier_block(pc); }
+
 // ---------------------------------------------------------------- a3 scan
 
 // One CTA per (destination d, local rank l): in place, H[l][d][b] := items
@@ -401,7 +488,7 @@ __global__ void __launch_bounds__(kScanThreads)
 k_scan(const RankDev* __restrict__ rk, CtrlDev* __restrict__ ctrl, uint64_t* __restrict__ Cmat,
        int grank0, int R, uint64_t cap, uint32_t T, int L, int plan_mode, unsigned* __restrict__ done,
        uint64_t* __restrict__ dst_off, uint64_t* __restrict__ num_in, int* __restrict__ ovf,
-       unsigned long long* __restrict__ G_out) {
+       unsigned long long* __restrict__ G_out, PeerCtl pc) {
   __shared__ uint32_t wsum[kScanThreads / 32];
   __shared__ uint32_t carry_s;
   __shared__ uint32_t sh[kScanThreads * kScanV];
@@ -464,10 +551,13 @@ k_scan(const RankDev* __restrict__ rk, CtrlDev* __restrict__ ctrl, uint64_t* __r
       c.invalid_last = c.invalid;
     }
   }
-  // plan_mode 1 (staged) / 2 (FUSED, single process): the last block also
-  // computes every local rank's plan, saving a launch
-  if (plan_mode && last_block(done))
-    plan_all(Cmat, grank0, L, R, cap, plan_mode == 2, dst_off, num_in, ovf, G_out);
+  // the last block: with peer control, the count exchange (every rank's rows
+  // into Cmat); then, plan_mode 1 (staged) / 2 (FUSED), every local rank's
+  // plan -- one launch instead of three
+  if ((plan_mode || pc.mbox) && last_block(done)) {
+    if (pc.mbox) ctl_counts_block(pc, Cmat, L, R);
+    if (plan_mode) plan_all(Cmat, grank0, L, R, cap, plan_mode == 2, dst_off, num_in, ovf, G_out);
+  }
 }
 
 // ---------------------------------------------------------------- a4 scatter
@@ -567,7 +657,8 @@ __global__ void __launch_bounds__(kThreads, kMinB)
 k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint8_t* const* __restrict__ dst_table,
           const uint64_t* __restrict__ dst_off, const int* __restrict__ ovf, int L, int R, uint64_t cap, uint32_t T,
           int cur, uint32_t B, uint32_t UPI, FastDiv divU, FastDiv divB, ScatterLayout lay, unsigned* __restrict__ wrap_done,
-          CtrlDev* __restrict__ ctrl_w, const uint64_t* __restrict__ wrap_num_in, uint64_t g_lo, uint64_t g_hi) {
+          CtrlDev* __restrict__ ctrl_w, const uint64_t* __restrict__ wrap_num_in, uint64_t g_lo, uint64_t g_hi,
+          PeerCtl pc) {
   if (ovf && *ovf) return;  // collective receive overflow: move nothing (Z3)
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + lay.off_mbar);
@@ -775,6 +866,9 @@ k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint
       ctrl_w[l2].invalid = 0;
       ctrl_w[l2].num_in = wrap_num_in[l2];
     }
+    // peer control: the completion barrier (every block's pushes were made
+    // visible system-wide before it counted itself in last_block)
+    if (pc.mbox) ctl_barrier_block(pc);
   }
 }
 
@@ -842,7 +936,8 @@ __global__ void __launch_bounds__(kThreads, kMinB)
 k_scatter_perm(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint8_t* const* __restrict__ dst_table,
                const uint64_t* __restrict__ dst_off, const int* __restrict__ ovf, int L, int R, uint64_t cap, uint32_t T,
                int cur, uint32_t B, uint32_t UPI, BulkLayout lay, unsigned* __restrict__ wrap_done,
-               CtrlDev* __restrict__ ctrl_w, const uint64_t* __restrict__ wrap_num_in, uint64_t g_lo, uint64_t g_hi) {
+               CtrlDev* __restrict__ ctrl_w, const uint64_t* __restrict__ wrap_num_in, uint64_t g_lo, uint64_t g_hi,
+          PeerCtl pc) {
   if (ovf && *ovf) return;  // collective receive overflow: move nothing (Z3)
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + lay.off_mbar);
@@ -1039,6 +1134,9 @@ k_scatter_perm(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl,
       ctrl_w[l2].invalid = 0;
       ctrl_w[l2].num_in = wrap_num_in[l2];
     }
+    // peer control: the completion barrier (every block's pushes were made
+    // visible system-wide before it counted itself in last_block)
+    if (pc.mbox) ctl_barrier_block(pc);
   }
 }
 
@@ -1113,88 +1211,23 @@ int launch_pass_bounds(Ctx* c, int K) {
   return RAFI_OK;
 }
 
-// ---------------------------------------------------------------- a5/a8 peer control
-
-// The count exchange (PAPER:126) and the completion barrier of a FUSED/CE
-// forward without NCCL: every process owns a mailbox (mbox_words), CUDA-IPC
-// mapped by every peer.  A round's epoch is the local counter mbox[0], bumped
-// in lockstep by every process.
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned long long globaltimer_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-// Wait until *flag >= e; a peer that never arrives is a hang: trap after 20 s.
-__device__ void spin_until(const unsigned long long* flag, unsigned long long e) {
-  const unsigned long long t0 = globaltimer_ns();
-  for (uint32_t i = 1; ld_acquire_sys(flag) < e; ++i) {
-    if ((i & 1023) == 0 && globaltimer_ns() - t0 > 20000000000ull) {
-      printf("rafi: peer control flag timed out (epoch %llu)\n", e);
-      __trap();
-    }
-  }
-}
-
-// Count exchange: push this process's L count rows into every process's
-// mailbox, raise its count flag there, wait for every process's flag, then
-// copy the whole R x R matrix into Cdev (where k_plan and the host read it).
-__global__ void __launch_bounds__(256) k_ctl_counts(unsigned long long* const* __restrict__ mbox, uint64_t* Cdev,
-                                                    int proc, int P, int L, int R) {
-  __shared__ unsigned long long se;
-  unsigned long long* mine = mbox[proc];
-  const int tid = threadIdx.x;
-  if (tid == 0) { se = mine[0] + 1; mine[0] = se; }
-  __syncthreads();
-  const unsigned long long e = se;
-  const size_t C0 = 8 + 2 * (size_t)P, row0 = (size_t)proc * L * R, n = (size_t)L * R;
-  for (size_t x = tid; x < (size_t)P * n; x += blockDim.x) {
-    const size_t p = x / n, i = x - p * n;
-    mbox[p][C0 + row0 + i] = Cdev[row0 + i];
-  }
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence_system();
-    for (int p = 0; p < P; ++p) st_release_sys(&mbox[p][8 + proc], e);
-  }
-  for (int p = tid; p < P; p += blockDim.x) spin_until(&mine[8 + p], e);
-  __syncthreads();
-  asm volatile("fence.acq_rel.sys;" ::: "memory");
-  for (size_t x = tid; x < (size_t)R * R; x += blockDim.x)
-    Cdev[x] = *reinterpret_cast<volatile unsigned long long*>(&mine[C0 + x]);
-}
-
-// Completion barrier: every push of this round (issued by the kernels before
-// this one on the stream) is visible system-wide, then the flag goes up in
-// every mailbox; return once every process's flag is up.
-__global__ void k_ctl_barrier(unsigned long long* const* __restrict__ mbox, int proc, int P) {
-  unsigned long long* mine = mbox[proc];
-  const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&mine[0]);
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    for (int p = 0; p < P; ++p) st_release_sys(&mbox[p][8 + P + proc], e);
-  }
-  for (int p = threadIdx.x; p < P; p += blockDim.x) spin_until(&mine[8 + P + p], e);
-  __syncthreads();
-  asm volatile("fence.acq_rel.sys;" ::: "memory");
+static PeerCtl peer_ctl(Ctx* c, bool on) {
+  PeerCtl pc;
+  pc.mbox = on ? c->mbox_table_dev : nullptr;
+  pc.proc = c->proc;
+  pc.P = c->nprocs;
+  return pc;
 }
 
 int launch_ctl_counts(Ctx* c) {
-  k_ctl_counts<<<1, 256, 0, c->stream>>>(c->mbox_table_dev, c->Cdev, c->proc, c->nprocs, c->L, c->R);
+  k_ctl_counts<<<1, 256, 0, c->stream>>>(peer_ctl(c, true), c->Cdev, c->L, c->R);
   RAFI_CK_CUDA(cudaGetLastError());
   c->launches += 1; c->fwd_launches += 1;
   return RAFI_OK;
 }
 
 int launch_ctl_barrier(Ctx* c) {
-  k_ctl_barrier<<<1, 32, 0, c->stream>>>(c->mbox_table_dev, c->proc, c->nprocs);
+  k_ctl_barrier<<<1, 32, 0, c->stream>>>(peer_ctl(c, true));
   RAFI_CK_CUDA(cudaGetLastError());
   c->launches += 1; c->fwd_launches += 1;
   return RAFI_OK;
@@ -1308,10 +1341,10 @@ int launch_hist(Ctx* c) {
   return RAFI_OK;
 }
 
-int launch_scan(Ctx* c, int plan_mode, unsigned long long* G_out) {
+int launch_scan(Ctx* c, int plan_mode, unsigned long long* G_out, bool ctl) {
   k_scan<<<dim3(c->R, c->L), kScanThreads, 0, c->stream>>>(rank_table(c), c->ctrl, c->Cdev, c->proc * c->L, c->R,
                                                            c->cap, c->tile, c->L, plan_mode, c->done_dev, c->off_dev,
-                                                           c->plan_dev, c->ovf_dev, G_out);
+                                                           c->plan_dev, c->ovf_dev, G_out, peer_ctl(c, ctl));
   RAFI_CK_CUDA(cudaGetLastError());
   c->launches += 1; c->fwd_launches += 1;
   return RAFI_OK;
@@ -1330,7 +1363,7 @@ static int launch_scatter_kk(Ctx* c, bool fused, bool wrap, uint32_t UPI, int gr
   k<<<grid, kThreads, lay.total, c->stream>>>(rank_table(c), c->ctrl, table, c->off_dev, ovf, c->L, c->R, c->cap,
                                              c->tile, c->cur, (uint32_t)c->B, UPI, FastDiv(UPI),
                                              FastDiv((uint32_t)c->B), lay, wrap ? c->done_dev + 1 : nullptr, c->ctrl,
-                                             c->plan_dev, c->g_lo, c->g_hi);
+                                             c->plan_dev, c->g_lo, c->g_hi, peer_ctl(c, c->scatter_barrier));
   RAFI_CK_CUDA(cudaGetLastError());
   return RAFI_OK;
 }
@@ -1411,7 +1444,7 @@ static int launch_perm_k(Ctx* c, bool fused, bool wrap, uint32_t UPI, int grid) 
                                              fused ? (ce ? c->ce_table_dev : c->in_table_dev) : nullptr, c->off_dev,
                                              fused && !ce ? c->ovf_dev : nullptr, c->L, c->R, c->cap, c->tile, c->cur,
                                              (uint32_t)c->B, UPI, lay, wrap ? c->done_dev + 1 : nullptr, c->ctrl,
-                                             c->plan_dev, c->g_lo, c->g_hi);
+                                             c->plan_dev, c->g_lo, c->g_hi, peer_ctl(c, c->scatter_barrier));
   RAFI_CK_CUDA(cudaGetLastError());
   return RAFI_OK;
 }
