@@ -9,6 +9,8 @@
 //   sm_pull     ld.global.v4 from the peer (1 reads 0)
 //   sm_push_bi  every GPU pushes to its ring successor at once
 //   tma_push_bi cp.async.bulk global->shared->peer global, every GPU at once
+//   mix_F       every GPU sends to its ring successor: fraction F/10 by SM
+//               stores, the rest by the copy engines, at the same time
 //   a2a_push    every GPU pushes 1/N of its buffer to each GPU (itself
 //               included: the FUSED exchange's traffic without the binning);
 //               reported per GPU as remote bytes / time
@@ -213,6 +215,30 @@ int main(int argc, char** argv) {
     k_tma_copy<<<SMS * 3, 32, 64 * 1024, st[d]>>>(a[d], b[(d + 1) % G], BYTES);
   }, all);
   line("tma_push_bi", G, ms, BYTES);
+  {  // SM stores and copy engines sharing the links: does their sum exceed either?
+    std::vector<cudaStream_t> s2(G);
+    std::vector<cudaEvent_t> f(G);
+    for (int d = 0; d < G; ++d) {
+      CK(cudaSetDevice(d));
+      CK(cudaStreamCreateWithFlags(&s2[d], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&f[d], cudaEventDisableTiming));
+    }
+    for (int F : {3, 5, 7}) {
+      const size_t nsm = (n16 * F / 10) & ~(size_t)255, nce = n16 - nsm;
+      ms = timed([&](int d) {
+        const int q = (d + 1) % G;
+        CK(cudaEventRecord(f[d], st[d]));
+        CK(cudaStreamWaitEvent(s2[d], f[d], 0));
+        CK(cudaMemcpyPeerAsync(b[q] + nsm * 16, q, a[d] + nsm * 16, d, nce * 16, s2[d]));
+        k_copy16<<<grid, 256, 0, st[d]>>>((const uint4*)a[d], (uint4*)b[q], nsm);
+        CK(cudaEventRecord(f[d], s2[d]));
+        CK(cudaStreamWaitEvent(st[d], f[d], 0));
+      }, all);
+      char name[16];
+      snprintf(name, sizeof(name), "mix_%d", F);
+      line(name, G, ms, BYTES);
+    }
+  }
   ms = timed([&](int d) { k_copy16<<<grid, 256, 0, st[d]>>>((const uint4*)a[d], (uint4*)b[d], n16); }, one);
   line("local_copy", 1, ms, 2.0 * BYTES);  // read + write, the HBM copy figure
   Dsts ds{};
