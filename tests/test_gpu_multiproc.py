@@ -50,9 +50,9 @@ def _worker(rank, world, port, B, n, pattern, exchange, rounds, scatter=1, passe
     cap = n * world
     ctx = rafi.Context(B, cap, comm=comm, stream=torch.cuda.current_stream())
     ctx.set_option(rafi.OPT_EXCHANGE, exchange)
-    assert ctx.get_option(rafi.OPT_EXCHANGE) == exchange
+    assert ctx.get_option(rafi.OPT_EXCHANGE) == (exchange or rafi.EXCHANGE_FUSED)
     ctx.set_option(rafi.OPT_SCATTER, scatter)
-    assert ctx.get_option(rafi.OPT_SCATTER) == scatter
+    assert ctx.get_option(rafi.OPT_SCATTER) == (scatter or rafi.SCATTER_BULK)
     ctx.set_option(rafi.OPT_CE_PASSES, passes)
     ctx.set_option(rafi.OPT_CONTROL, control)
     if control:
@@ -116,6 +116,16 @@ def test_multigpu_control_modes(world, control, exchange):
     _need(world)
     import torch.multiprocessing as mp
     mp.spawn(_worker, args=(world, _free_port(), 48, 20011, "skewed", exchange, 5, 1, 0, control), nprocs=world,
+             join=True)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_multigpu_large_default_path(world):
+    """The bench's own configuration (AUTO: FUSED exchange, BULK pushes, peer
+    control) at 2M x 48-B items per rank, two rounds: P1 bit-exact."""
+    _need(world)
+    import torch.multiprocessing as mp
+    mp.spawn(_worker, args=(world, _free_port(), 48, 2 * 1024 * 1024, "uniform", 0, 2, 0, 0, 0), nprocs=world,
              join=True)
 
 

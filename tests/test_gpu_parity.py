@@ -291,6 +291,19 @@ def test_full_size_cfg2_shape(L, n, exchange):
         p1_forward(ctx, L, B)
 
 
+@pytest.mark.parametrize("B,scatter", [(44, "threads"), (64, "threads"), (48, "bulk"), (24, "threads")])
+def test_full_size_item_sizes(B, scatter):
+    """16M items of the cfg5 sweep sizes at R=4 logical ranks, in the launch
+    configuration the benches use (auto tile), including the 16-B chunk
+    gather (44 B) and the bulk-store path: P1 bit-exact."""
+    L, n = 4, 4 * 1024 * 1024
+    with _ctx(B, n + n // 8, L) as ctx:
+        ctx.set_option(rafi.OPT_SCATTER, SCATTERS[scatter])
+        for l in range(L):
+            ctx.drv_emit_synthetic(synth.PATTERNS["uniform"], synth.CONFIG_SEEDS[5], 0, n, local=l)
+        p1_forward(ctx, L, B)
+
+
 def test_host_io_overlap_rounds():
     """rafi_emit_bulk from pinned host memory (copy-in stream, double-buffered
     staging) and rafi_read_incoming_async (copy-out stream) over several

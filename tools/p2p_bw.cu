@@ -11,6 +11,7 @@
 //   tma_push_bi cp.async.bulk global->shared->peer global, every GPU at once
 //   mix_F       every GPU sends to its ring successor: fraction F/10 by SM
 //               stores, the rest by the copy engines, at the same time
+//   a2a_pull    the same exchange done by the receivers' loads
 //   a2a_push    every GPU pushes 1/N of its buffer to each GPU (itself
 //               included: the FUSED exchange's traffic without the binning);
 //               reported per GPU as remote bytes / time
@@ -57,6 +58,32 @@ __global__ void __launch_bounds__(256) k_a2a(const uint4* __restrict__ src, Dsts
     const size_t c = f / G;
     const uint4* s = src + (size_t)p * part + c * CH;
     uint4* d = dst.p[p] + (size_t)me * part + c * CH;
+    const size_t lim = part - c * CH < CH ? part - c * CH : CH;
+    uint4 v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const size_t i = threadIdx.x + j * 256;
+      if (i < lim) v[j] = s[i];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const size_t i = threadIdx.x + j * 256;
+      if (i < lim) d[i] = v[j];
+    }
+  }
+}
+
+// all-to-all pull: part me of every GPU p's buffer is read into dst + p*part
+// (the receiver side of the same exchange), destinations rotated per reader.
+struct Srcs { const uint4* p[8]; };
+__global__ void __launch_bounds__(256) k_a2a_pull(Srcs src, uint4* __restrict__ dst, int me, int G, size_t part) {
+  constexpr size_t CH = 256 * 4;
+  const size_t nch = (part + CH - 1) / CH;
+  for (size_t f = blockIdx.x; f < nch * G; f += gridDim.x) {
+    const int p = (int)((me + f) % G);
+    const size_t c = f / G;
+    const uint4* s = src.p[p] + (size_t)me * part + c * CH;
+    uint4* d = dst + (size_t)p * part + c * CH;
     const size_t lim = part - c * CH < CH ? part - c * CH : CH;
     uint4 v[4];
 #pragma unroll
@@ -248,5 +275,9 @@ int main(int argc, char** argv) {
     k_a2a<<<grid, 256, 0, st[d]>>>((const uint4*)a[d], ds, d, G, part);
   }, all);
   line("a2a_push", G, ms, (double)part * 16 * (G - 1));
+  Srcs ss{};
+  for (int p = 0; p < G; ++p) ss.p[p] = (const uint4*)a[p];
+  ms = timed([&](int d) { k_a2a_pull<<<grid, 256, 0, st[d]>>>(ss, (uint4*)b[d], d, G, part); }, all);
+  line("a2a_pull", G, ms, (double)part * 16 * (G - 1));
   return 0;
 }
