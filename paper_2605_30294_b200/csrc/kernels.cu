@@ -1419,9 +1419,12 @@ size_t perm_smem_bytes(int mode, uint32_t T, uint64_t B, int R) {
   return bulk_layout(T, B, R, perm_nobuf(mode, T, B, R)).total;
 }
 
-// Largest tile (256 * 2^k) whose layout fits four CTAs per SM, else two, else one.
+// Largest tile (256 * 2^k) whose layout fits four CTAs per SM, else two, else
+// one.  BULK starts at two: its NVLink pushes gain 2-9% from 512-item tiles
+// over 256-item ones at N=2 and N=4 (profiles/r01_bulk_tiles_multigpu.md).
 uint32_t choose_tile_perm(int mode, uint64_t B, int R) {
   for (uint32_t budget : {56u * 1024u, 112u * 1024u, 227u * 1024u}) {
+    if (mode == RAFI_SCATTER_BULK && budget < 112u * 1024u) continue;
     uint32_t best = 0;
     for (uint32_t T = kThreads; T <= kThreads * kMaxK; T *= 2)
       if (perm_smem_bytes(mode, T, B, R) <= budget) best = T;
