@@ -379,7 +379,10 @@ def main():
         # two pinned result buffers: step k's read-back (copy-out stream) overlaps
         # step k+1's host-to-device copy (copy-in stream) over full-duplex PCIe
         outs = [torch.empty((cap, B), dtype=torch.uint8).pin_memory() for _ in range(2)]
-        Ke = max(3, min(K, 5))
+        # as many steps as the device-resident measurement: the pipeline's
+        # one-time fill (first upload) and drain (last read-back) are inside
+        # the timed region and amortise over K steps
+        Ke = max(3, K)
         for k in range(2):
             ctx.emit_bulk(items_p, dests_p, n)
             ctx.forward()
