@@ -261,16 +261,29 @@ k_hist(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, int R, 
       for (int k = 0; k < TPW; ++k) {
         const uint64_t t = tb + w * TPW + k;
         const uint32_t nt = t < tiles ? (uint32_t)umin64(T, n - t * T) : 0u;
-#pragma unroll
-        for (int j = 0; j < kHistVec; ++j) {
-          const uint32_t i0 = (q0 + j * 32 + lane) * 4;
-          const int e[4] = {v[k][j].x, v[k][j].y, v[k][j].z, v[k][j].w};
-#pragma unroll
-          for (int m = 0; m < 4; ++m) {
-            const int d = i0 + m < nt ? e[m] : -1;  // -1 (and any d >= RMAX) matches no word
+        // every queued dest is in [0, R) (invalid ones were rejected at emit)
+        auto add = [&](int d) {
+          if (NW == 1) {
+            c[k][0] += 1ull << ((unsigned)d << 3);
+          } else {
             const uint64_t one = 1ull << ((d & 7) * 8);
 #pragma unroll
             for (int x = 0; x < NW; ++x) c[k][x] += (d >> 3) == x ? one : 0ull;
+          }
+        };
+        if ((q0 + 32 * kHistVec) * 4 <= nt) {  // the whole batch is in the tile: no bounds checks
+#pragma unroll
+          for (int j = 0; j < kHistVec; ++j) {
+            add(v[k][j].x); add(v[k][j].y); add(v[k][j].z); add(v[k][j].w);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < kHistVec; ++j) {
+            const uint32_t i0 = (q0 + j * 32 + lane) * 4;
+            const int e[4] = {v[k][j].x, v[k][j].y, v[k][j].z, v[k][j].w};
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+              if (i0 + m < nt) add(e[m]);
           }
         }
       }
