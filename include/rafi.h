@@ -119,6 +119,10 @@ typedef struct {
                                       about 2M items per pass, at most 8) */
 #define RAFI_OPT_CONTROL 7         /* count exchange and completion barrier of FUSED/CE forwards:
                                       RAFI_CONTROL_* (default AUTO) */
+#define RAFI_OPT_FORWARD_GRAPH 8   /* 1 (default) = a blocking FUSED rafi_forward launches its kernels, the
+                                      collectives and the read-back of the counts as one cached CUDA graph
+                                      (re-captured after any option change or resize); 0 = one launch each.
+                                      Forwards timed by RAFI_OPT_TIMING always launch one by one */
 #define RAFI_OPT_SCATTER 5         /* how the binning scatter writes destination runs:
                                       RAFI_SCATTER_* (default AUTO).  Same result bytes either way.
                                       Only between rounds; re-chooses the tile unless RAFI_OPT_TILE

@@ -175,6 +175,8 @@ static int exchange_peer_pointers(Ctx* c) {
   return rc;
 }
 
+static void drop_fwd_graph(Ctx* c);
+
 static void free_ce(Ctx* c) {
   for (size_t i = 0; i < c->ce_streams.size(); ++i) {
     if (c->ce_streams[i]) { cudaStreamSynchronize(c->ce_streams[i]); cudaStreamDestroy(c->ce_streams[i]); }
@@ -298,6 +300,8 @@ static void destroy_ctx(Ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   free_ce(c);
+  drop_fwd_graph(c);
+  if (c->cap_stream) { cudaStreamDestroy(c->cap_stream); c->cap_stream = nullptr; }
   close_ipc(c);
   for (auto& r : c->lr) free_rank(r);
   cudaFree(c->rank_dev); cudaFree(c->ctrl); cudaFree(c->runs_dev); cudaFree(c->plan_dev);
@@ -438,25 +442,29 @@ static int book_keep(Ctx* c, uint64_t* G_out) {
 // FUSED forward: counts first, then one kernel bins and pushes every run
 // straight into its destination's incoming queue (NEXT-1 of SURVEY §8(f)).
 //   hist -> scan -> [all-gather counts] -> plan -> scatter+push -> [barrier] -> wrap-up
+// Phase event i on the context stream (timed forwards launch directly, not
+// from the cached graph: event record nodes inside a graph cost ~4 us each).
+static cudaError_t record_ev(Ctx* c, int i) { return cudaEventRecord(c->ev[i], c->stream); }
+
 static int enqueue_fused(Ctx* c, unsigned long long* G_dev, bool T) {
   const int R = c->R, L = c->L;
   c->fwd_launches = 0;
-  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[0], c->stream));
+  if (T) RAFI_CK_CUDA(record_ev(c, 0));
   RAFI_CK(launch_hist(c));
-  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[1], c->stream));
+  if (T) RAFI_CK_CUDA(record_ev(c, 1));
   // a3 (+ a5's plan when this process holds every rank: the scan's last block
   // plans; with peer control it first exchanges the counts through the
   // mailboxes, so one kernel does scan + count exchange + plan)
   const bool peer = c->nprocs > 1 && c->ctl_peer;
   RAFI_CK(launch_scan(c, (c->nprocs == 1 || peer) ? 2 : 0, G_dev, peer));
-  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[2], c->stream));
+  if (T) RAFI_CK_CUDA(record_ev(c, 2));
   if (c->nprocs > 1 && !peer) {
     // a5: the whole R x R matrix on every rank; offsets + overflow on device
     RAFI_CK_NCCL(ncclAllGather(c->Cdev + (size_t)c->proc * L * R, c->Cdev, (size_t)L * R, ncclUint64, c->comm,
                                c->stream));
     RAFI_CK(launch_plan(c, true, G_dev));
   }
-  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[3], c->stream));
+  if (T) RAFI_CK_CUDA(record_ev(c, 3));
   // a4 + a6: stable scatter, each destination run written into its receiver's
   // queue; a7 wrap-up by its last block (skipped on overflow), and with peer
   // control the completion barrier after it
@@ -464,13 +472,13 @@ static int enqueue_fused(Ctx* c, unsigned long long* G_dev, bool T) {
   const int rc = launch_scatter(c, true, true);
   c->scatter_barrier = false;
   RAFI_CK(rc);
-  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[4], c->stream));
+  if (T) RAFI_CK_CUDA(record_ev(c, 4));
   // every push has landed before any rank's next app kernel reads its queue:
   // the all-reduce completes only after every rank's scatter kernel completed
   if (c->nprocs > 1 && !peer)
     RAFI_CK_NCCL(ncclAllReduce(c->ovf_dev + 1, c->ovf_dev + 1, 1, ncclInt32, ncclMax, c->comm, c->stream));
-  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[5], c->stream));
-  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[6], c->stream));
+  if (T) RAFI_CK_CUDA(record_ev(c, 5));
+  if (T) RAFI_CK_CUDA(record_ev(c, 6));
   return RAFI_OK;
 }
 
@@ -533,11 +541,67 @@ static void mark_timing(Ctx* c, bool fused) {
   c->emit_mark = c->emit_tail;
 }
 
+static void drop_fwd_graph(Ctx* c) {
+  if (c->fwd_exec) { cudaGraphExecDestroy(c->fwd_exec); c->fwd_exec = nullptr; }
+  c->fwd_dirty = true;
+}
+
+// Capture [enqueue_fused + read-back of counters and count matrix] on a
+// private stream into a graph; its kernels are counted at every replay.
+static int build_fwd_graph(Ctx* c, bool T) {
+  drop_fwd_graph(c);
+  if (!c->cap_stream) RAFI_CK_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  cudaStream_t user = c->stream;
+  const uint64_t l0 = c->launches;
+  RAFI_CK_CUDA(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeRelaxed));
+  c->stream = c->cap_stream;
+  int rc = enqueue_fused(c, nullptr, T);
+  if (rc == RAFI_OK &&
+      cudaMemcpyAsync(c->ctrl_host, c->ctrl, ctrl_c_bytes(c), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess) {
+    set_error("cudaMemcpyAsync (capture)");
+    rc = RAFI_ERR_CUDA;
+  }
+  c->stream = user;
+  cudaGraph_t g = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(c->cap_stream, &g);
+  if (rc == RAFI_OK && e != cudaSuccess) { set_error(std::string("cudaStreamEndCapture: ") + cudaGetErrorString(e)); rc = RAFI_ERR_CUDA; }
+  if (rc == RAFI_OK && cudaGraphInstantiate(&c->fwd_exec, g, 0) != cudaSuccess) {
+    set_error("cudaGraphInstantiate (forward)");
+    c->fwd_exec = nullptr;
+    rc = RAFI_ERR_CUDA;
+  }
+  if (g) cudaGraphDestroy(g);
+  cudaGetLastError();
+  c->fwd_graph_launches = c->launches - l0;
+  c->launches = l0;
+  if (rc != RAFI_OK) return rc;
+  c->fwd_dirty = false;
+  c->fwd_T = T;
+  return RAFI_OK;
+}
+
 static int64_t forward_fused(Ctx* c) {
   const bool T = c->timing;
-  RAFI_CK(enqueue_fused(c, nullptr, T));
   uint64_t G = 0;
-  RAFI_CK(refresh_host(c, &G));
+  if (c->fwd_graph && !T) {
+    // one graph launch instead of 3-6 launches and a copy: what a small,
+    // latency-bound round costs on the host.  Timed forwards (RAFI_OPT_TIMING)
+    // launch directly, with their events between the launches.
+    if (c->fwd_dirty || !c->fwd_exec || c->fwd_T != T) RAFI_CK(build_fwd_graph(c, T));
+    RAFI_CK_CUDA(cudaGraphLaunch(c->fwd_exec, c->stream));
+    c->launches += c->fwd_graph_launches;
+    c->fwd_launches = c->fwd_graph_launches;
+    RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
+    c->host_stale = false;
+    if (book_keep(c, &G)) {
+      c->broken = true;
+      set_error("receive overflow: some rank would receive more than its capacity");
+      return RAFI_ERR_RECV_OVERFLOW;
+    }
+  } else {
+    RAFI_CK(enqueue_fused(c, nullptr, T));
+    RAFI_CK(refresh_host(c, &G));
+  }
   if (T) mark_timing(c, true);
   c->last_fused = true;
   c->round += 1;
@@ -869,6 +933,7 @@ int rafi_resize(rafi_ctx* ctx, size_t capacity) {
   for (auto& r : old) free_rank(r);
   RAFI_CK(upload_rank_table(c));
   c->cur = 0;
+  drop_fwd_graph(c);  // captured with the old buffers and grid sizes
   RAFI_CK(exchange_peer_pointers(c));
   free_ce(c);  // its table points at the old queues
   RAFI_CK(resolve_exchange(c));
@@ -1132,6 +1197,9 @@ int rafi_get_stats(const rafi_ctx* ctx, int local, rafi_stats* out) {
 int rafi_set_option(rafi_ctx* ctx, int key, long long v) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c) return RAFI_ERR_INVALID_ARG;
+  // any option but the timing switch may change what the cached forward graph
+  // launches (the graph is only used untimed)
+  if (key != RAFI_OPT_TIMING) c->fwd_dirty = true;
   switch (key) {
     case RAFI_OPT_EXCHANGE: {
       if (v < RAFI_EXCHANGE_AUTO || v > RAFI_EXCHANGE_CE) return RAFI_ERR_INVALID_ARG;
@@ -1171,6 +1239,10 @@ int rafi_set_option(rafi_ctx* ctx, int key, long long v) {
       return RAFI_OK;
     }
     case RAFI_OPT_SELF_DIRECT: return v == 0 ? RAFI_OK : RAFI_ERR_UNSUPPORTED;
+    case RAFI_OPT_FORWARD_GRAPH:
+      if (v != 0 && v != 1) return RAFI_ERR_INVALID_ARG;
+      c->fwd_graph = v != 0;
+      return RAFI_OK;
     case RAFI_OPT_CONTROL:
       if (v < RAFI_CONTROL_AUTO || v > RAFI_CONTROL_PEER) return RAFI_ERR_INVALID_ARG;
       if (v == RAFI_CONTROL_PEER && c->nprocs > 1 && !c->peer_ok) {
@@ -1198,6 +1270,7 @@ int rafi_get_option(const rafi_ctx* ctx, int key, long long* v) {
     case RAFI_OPT_SCATTER: *v = c->scatter_eff; return RAFI_OK;
     case RAFI_OPT_CE_PASSES: *v = c->ce_passes; return RAFI_OK;
     case RAFI_OPT_CONTROL: *v = c->ctl_peer ? RAFI_CONTROL_PEER : RAFI_CONTROL_NCCL; return RAFI_OK;
+    case RAFI_OPT_FORWARD_GRAPH: *v = c->fwd_graph; return RAFI_OK;
     case RAFI_OPT_SELF_DIRECT: *v = 0; return RAFI_OK;
     default: return RAFI_ERR_INVALID_ARG;
   }

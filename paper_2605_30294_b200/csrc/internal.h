@@ -163,6 +163,13 @@ struct Ctx {
   std::vector<cudaStream_t> ce_streams;  // [R] one copy stream per peer
   std::vector<cudaEvent_t> ce_done;      // [R]
   cudaEvent_t ce_pass[kMaxPasses] = {};
+  // blocking FUSED forward replayed as one cached CUDA graph (RAFI_OPT_FORWARD_GRAPH)
+  bool fwd_graph = true;
+  bool fwd_dirty = true;            // options / buffers changed since the graph was captured
+  bool fwd_T = false;               // the cached graph records the timing events
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t fwd_exec = nullptr;
+  uint64_t fwd_graph_launches = 0;  // kernels in the cached graph
   cudaEvent_t ev[8] = {};
   static constexpr int kEmitEv = 32;     // ring of (start, end) event pairs for timed bulk emits
   cudaEvent_t ev_emit[kEmitEv][2] = {};

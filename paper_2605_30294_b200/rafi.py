@@ -32,6 +32,7 @@ OPT_SELF_DIRECT = 4
 OPT_SCATTER = 5
 OPT_CE_PASSES = 6
 OPT_CONTROL = 7
+OPT_FORWARD_GRAPH = 8
 CONTROL_AUTO, CONTROL_NCCL, CONTROL_PEER = 0, 1, 2
 SCATTER_AUTO, SCATTER_THREADS, SCATTER_BULK, SCATTER_ALIGNED, SCATTER_UNITS = 0, 1, 2, 3, 4
 EXCHANGE_AUTO, EXCHANGE_NCCL, EXCHANGE_PEER, EXCHANGE_FUSED, EXCHANGE_CE = 0, 1, 2, 3, 4

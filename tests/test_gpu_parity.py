@@ -330,3 +330,28 @@ def test_host_io_overlap_rounds():
         ctx.read_wait()
     for rnd in range(rounds):
         assert np.array_equal(canonical(pins[rnd][: sizes[rnd]].numpy()), canonical(exp[rnd])), rnd
+
+
+@pytest.mark.parametrize("graph", [0, 1])
+def test_forward_graph_rounds_with_option_changes(graph):
+    """The blocking forward replayed from its cached CUDA graph (default) or
+    launched kernel by kernel: P1 bit-exact over rounds of changing sizes,
+    with tile / scatter / timing changes between rounds (each forces a
+    re-capture)."""
+    B, L = 44, 3
+    with _ctx(B, 60000, L) as ctx:
+        ctx.set_option(rafi.OPT_FORWARD_GRAPH, graph)
+        assert ctx.get_option(rafi.OPT_FORWARD_GRAPH) == graph
+        steps = [(20000, None), (7, None), (15000, (rafi.OPT_TILE, 1024)), (0, None),
+                 (19999, (rafi.OPT_TIMING, 1)), (12345, (rafi.OPT_SCATTER, rafi.SCATTER_UNITS)),
+                 (20000, (rafi.OPT_TILE, 0))]
+        for rnd, (n, opt) in enumerate(steps):
+            if opt:
+                ctx.set_option(*opt)
+            inputs = make_inputs(L, n, B, "skewed", 300 + rnd, rnd=rnd)
+            _emit_all(ctx, inputs)
+            p1_forward(ctx, L, B)
+            if ctx.get_option(rafi.OPT_TIMING) and n:
+                st = ctx.stats()  # phase events are recorded by the graph replay too
+                assert st["ms_scatter"] > 0 and st["ms_hist"] > 0 and st["ms_total"] > 0, st
+        assert ctx.forward() == 0
