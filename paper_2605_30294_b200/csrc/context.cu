@@ -307,7 +307,6 @@ static void destroy_ctx(Ctx* c) {
   cudaFree(c->rank_dev); cudaFree(c->ctrl); cudaFree(c->runs_dev); cudaFree(c->plan_dev);
   cudaFree(c->off_dev); cudaFree(c->ovf_dev); cudaFree(c->in_table_dev); cudaFree(c->done_dev);
   cudaFree(c->mbox_table_dev);
-  cudaFree(c->stage);
   if (c->io_in) {
     cudaStreamSynchronize(c->io_in); cudaStreamSynchronize(c->io_out);
     cudaStreamDestroy(c->io_in); cudaStreamDestroy(c->io_out);

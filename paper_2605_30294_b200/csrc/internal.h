@@ -140,8 +140,6 @@ struct Ctx {
   bool cls_dev[2] = {false, false};
   // host I/O: staging for rafi_emit_bulk from host memory (double-buffered,
   // filled on io_in) and asynchronous read-back (io_out)
-  uint8_t* stage = nullptr;   // (legacy single buffer, unused)
-  size_t stage_bytes = 0;
   cudaStream_t io_in = nullptr, io_out = nullptr;
   uint8_t* stage2[2] = {nullptr, nullptr};
   size_t stage_cap[2] = {0, 0};

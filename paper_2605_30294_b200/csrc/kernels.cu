@@ -71,11 +71,6 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 __device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
@@ -798,14 +793,6 @@ k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint
           const uint32_t s1 = e + 16 > B ? (uint32_t)src_of[p0 + q + 1] * B + e - B : s0;
           RAFI_DCHECK(s0 % 4 == 0 && s1 % 4 == 0 && ((uintptr_t)src8 & 3) == 0, "chunk source alignment");
           uint32_t v[4];
-#ifdef RAFI_CHUNK_DIAG
-          if ((g & 15) || s0 + 16 > T * B + 16 || s1 + 16 > T * B + 16 || ((uintptr_t)src8 & 15)) {
-            printf("DIAG blk %d tid %d it %u d %d x %u p0 %u p1 %u rs %llx re %llx g %llx o %u q %u e %u s0 %u s1 %u src8 %p\n",
-                   (int)blockIdx.x, tid, it, d, x, p0, p1, (unsigned long long)rs, (unsigned long long)re,
-                   (unsigned long long)g, o, q, e, s0, s1, src8);
-            continue;
-          }
-#endif
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             v[j] = *reinterpret_cast<const uint32_t*>(src8 + (e + 4 * j < B ? s0 : s1) + 4 * j);
