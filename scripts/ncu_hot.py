@@ -14,7 +14,12 @@ rows = list(csv.reader(io.StringIO("\n".join(lines[1:]))))
 h = rows[0]
 iS, iSrc = h.index("Warp Stall Sampling (All Samples)"), h.index("Source")
 stall_cols = [i for i, c in enumerate(h) if c.startswith("stall_") and "Not Issued" not in c]
-data = [r for r in rows[1:] if len(r) == len(h)]
+data = []
+for r in rows[1:]:  # the first kernel's section only (a later section starts with its own header)
+    if len(r) == len(h) and r[iS] == h[iS]:
+        break
+    if len(r) == len(h):
+        data.append(r)
 tot = sum(int(r[iS] or 0) for r in data)
 print("total samples", tot)
 def reasons(r):
