@@ -50,6 +50,7 @@ def parse():
     p.add_argument("--control", default="auto", choices=["auto", "nccl", "peer"])
     p.add_argument("--scatter", default="auto", choices=["auto", "threads", "bulk", "aligned", "units"])
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-graph", action="store_true", help="skip the supplementary graph-replay measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle cpu_baseline sample")
     return p.parse_args()
@@ -244,7 +245,10 @@ def main():
         comm = rafi.nccl_comm_init(world, rank, obj[0], local)
 
     B, n = args.item_bytes, args.items
-    stream = torch.cuda.current_stream()
+    # the context's own (non-default) stream: everything below is ordered on
+    # it, and it can be captured into a CUDA graph
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.synchronize()
     cap = n + n // 8 + 4096
     ctx = rafi.Context(B, cap, comm=comm, stream=stream, device=local)
     if args.exchange != "auto":
@@ -424,6 +428,34 @@ def main():
         e2e = {"value": N * n * Ke / (ms_e / 1e3), "unit": "items/s", "h2d_bytes_per_step": n * (B + 4),
                "d2h_bytes_per_step": int(d2h / Ke), "steps": Ke}
 
+    # ---- the same step as an application-side CUDA graph (NEXT-3): [emit_bulk +
+    # rafi_forward_async] captured once and replayed K times, G stays on the
+    # device (no host synchronisation per step); supplementary, not the headline
+    graph = None
+    if not args.no_graph:
+        ctx.set_option(rafi.OPT_TIMING, 0)
+        G_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+        ctx.capture_begin()
+        ctx.emit_bulk(items_d, dests_d, n)
+        ctx.forward_async(G_dev)
+        ex = ctx.capture_end()
+        for _ in range(args.warmup):
+            ctx.graph_launch(ex)
+        barrier()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(K):
+            ctx.graph_launch(ex)
+        g1.record(stream)
+        barrier()
+        ms_g = max_over_ranks(g0.elapsed_time(g1))
+        assert int(G_dev.item()) == N * n
+        ctx.sync_host()
+        rafi.Context.graph_destroy(ex)
+        graph = {"value": N * n * K / (ms_g / 1e3), "unit": "items/s", "ms_per_step": ms_g / K,
+                 "what": "[emit_bulk + rafi_forward_async] captured as one CUDA graph, replayed K times"}
+
     # ---- cpu baseline: the oracle on the host, rank 0 at N=1 only
     cpu = None
     if N == 1 and rank == 0 and not args.no_cpu_baseline:
@@ -439,7 +471,7 @@ def main():
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clk, "phases_ms": ph, "phases_source": "instrumented pass of the same K steps (CUDA events "
         "between launches); its ms_per_step: %.4f" % ms_instr, "kernels": kern, "exchange": exch, "exchange_transport": exchange,
-        "scatter_write": scatter, "tile": ctx_tile, "control": control, "per_gpu_items_per_s": value / N,
+        "graph_replay": graph, "scatter_write": scatter, "tile": ctx_tile, "control": control, "per_gpu_items_per_s": value / N,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
