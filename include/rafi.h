@@ -129,7 +129,8 @@ typedef struct {
                                       pinned it.  RAFI_ERR_UNSUPPORTED if BULK/ALIGNED is asked for an
                                       item size that is not a multiple of 4 or a tile that does not fit */
 
-#define RAFI_SCATTER_AUTO 0        /* BULK when supported, else THREADS */
+#define RAFI_SCATTER_AUTO 0        /* BULK when the scatter pushes runs to NVLink peers (FUSED over several
+                                      processes) and BULK is supported, else THREADS (measured winners) */
 #define RAFI_SCATTER_THREADS 1     /* threads store every run with coalesced stores: 16/8/4/2/1-B item units,
                                       or, for 4-B units (item_bytes % 8 == 4, >= 16), 16-B-aligned chunks
                                       gathered from the (at most two) items they cover */
@@ -143,10 +144,11 @@ typedef struct {
 
 #define RAFI_CONTROL_AUTO 0        /* PEER when every rank's queues are mapped, else NCCL */
 #define RAFI_CONTROL_NCCL 1        /* ncclAllGather of the count rows, ncclAllReduce as the completion barrier */
-#define RAFI_CONTROL_PEER 2        /* one small kernel pushes this process's count rows into every peer's
-                                      CUDA-IPC mailbox over NVLink and raises a flag (st.release.sys);
-                                      the completion barrier is a flag per process; both spin on
-                                      ld.acquire.sys (a peer that never arrives traps after 20 s) */
+#define RAFI_CONTROL_PEER 2        /* the scan kernel's last block pushes this process's count rows into
+                                      every peer's CUDA-IPC mailbox over NVLink, fences once and raises a
+                                      flag in each; the scatter kernel's last block runs the completion
+                                      barrier the same way; both spin on ld.acquire.sys (a peer that never
+                                      arrives traps after 20 s).  Every rank must use the same setting */
 
 #define RAFI_EXCHANGE_AUTO 0       /* FUSED when every rank's queues are addressable, else NCCL */
 #define RAFI_EXCHANGE_NCCL 1       /* stage the sorted batch, grouped ncclSend/ncclRecv (one local rank per process) */
@@ -154,7 +156,8 @@ typedef struct {
                                       local / CUDA-IPC peer pointers (NVLink) */
 #define RAFI_EXCHANGE_FUSED 3      /* the scatter writes every destination run straight into the destination
                                       rank's incoming queue (local HBM or NVLink peer memory); the count
-                                      matrix is all-gathered first; no send batch, no separate copy */
+                                      matrix is exchanged first (RAFI_OPT_CONTROL); no send batch, no
+                                      separate copy */
 #define RAFI_EXCHANGE_CE 4         /* copy-engine pipeline: counts all-gathered first; the scatter runs in
                                       passes over the batch, writing the self run straight into the own
                                       incoming queue and peer runs into the send batch; after each pass the
