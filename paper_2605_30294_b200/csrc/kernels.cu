@@ -1269,10 +1269,11 @@ static uint32_t unit_for(uint64_t B, uintptr_t align_bits) {
 // two 110-KiB CTAs (longer tiles).  Measured with the cfg5 size sweep
 // (profiles/r01_scatter_variants.md).
 static int scatter_minb(uint64_t B) { return B <= 96 ? 4 : 2; }
-// Items of 17-24 B: 1024-item tiles at three CTAs/SM beat 512-item tiles at
-// four (cfg5 tile sweep, profiles/r01_suite_n1_tiles_threads.md).
+// Up to 64 B the tile may use 62 KiB: that doubles the tile where a 54-KiB
+// budget falls just short (24 B: 1024 items, 56 B: 512 items; three CTAs/SM
+// then) and changes nothing else (tile sweeps, profiles/r01_suite_n1_tiles_threads.md).
 static uint32_t scatter_budget(uint64_t B) {
-  if (B > 16 && B <= 24) return 62u * 1024u;
+  if (B <= 64) return 62u * 1024u;
   return scatter_minb(B) == 4 ? 54u * 1024u : 110u * 1024u;
 }
 
