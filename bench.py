@@ -432,7 +432,7 @@ def main():
     # rafi_forward_async] captured once and replayed K times, G stays on the
     # device (no host synchronisation per step); supplementary, not the headline
     graph = None
-    if not args.no_graph:
+    if not args.no_graph and exchange == "fused":  # rafi_forward_async is FUSED-only
         ctx.set_option(rafi.OPT_TIMING, 0)
         G_dev = torch.zeros(1, dtype=torch.int64, device=dev)
         ctx.capture_begin()
