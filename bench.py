@@ -46,9 +46,9 @@ def parse():
     p.add_argument("--items", type=int, default=DEF_N, help="items per rank per step")
     p.add_argument("--item-bytes", type=int, default=DEF_B)
     p.add_argument("--pattern", default="uniform")
-    p.add_argument("--exchange", default="auto", choices=["auto", "nccl", "peer", "fused", "ce"])
+    p.add_argument("--exchange", default="auto", choices=["auto", "nccl", "peer", "fused"])
     p.add_argument("--control", default="auto", choices=["auto", "nccl", "peer"])
-    p.add_argument("--scatter", default="auto", choices=["auto", "threads", "bulk", "aligned", "units"])
+    p.add_argument("--scatter", default="auto", choices=["auto", "threads", "bulk"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-graph", action="store_true", help="skip the supplementary graph-replay measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -253,17 +253,15 @@ def main():
     ctx = rafi.Context(B, cap, comm=comm, stream=stream, device=local)
     if args.exchange != "auto":
         ctx.set_option(rafi.OPT_EXCHANGE, {"nccl": rafi.EXCHANGE_NCCL, "peer": rafi.EXCHANGE_PEER,
-                                           "fused": rafi.EXCHANGE_FUSED, "ce": rafi.EXCHANGE_CE}[args.exchange])
-    exchange = {1: "nccl", 2: "peer", 3: "fused", 4: "ce"}[ctx.get_option(rafi.OPT_EXCHANGE)]
+                                           "fused": rafi.EXCHANGE_FUSED}[args.exchange])
+    exchange = {1: "nccl", 2: "peer", 3: "fused"}[ctx.get_option(rafi.OPT_EXCHANGE)]
     if args.scatter != "auto":
-        ctx.set_option(rafi.OPT_SCATTER, {"threads": rafi.SCATTER_THREADS, "bulk": rafi.SCATTER_BULK,
-                                          "aligned": rafi.SCATTER_ALIGNED,
-                                          "units": rafi.SCATTER_UNITS}[args.scatter])
-    scatter = {1: "threads", 2: "bulk", 3: "aligned", 4: "units"}[ctx.get_option(rafi.OPT_SCATTER)]
+        ctx.set_option(rafi.OPT_SCATTER, {"threads": rafi.SCATTER_THREADS, "bulk": rafi.SCATTER_BULK}[args.scatter])
+    scatter = {1: "threads", 2: "bulk"}[ctx.get_option(rafi.OPT_SCATTER)]
     ctx_tile = ctx.get_option(rafi.OPT_TILE)
     if args.control != "auto":
         ctx.set_option(rafi.OPT_CONTROL, {"nccl": rafi.CONTROL_NCCL, "peer": rafi.CONTROL_PEER}[args.control])
-    control = {1: "nccl", 2: "peer"}[ctx.get_option(rafi.OPT_CONTROL)] if N > 1 else None
+    control = {1: "nccl", 2: "peer", 3: "host"}[ctx.get_option(rafi.OPT_CONTROL)] if N > 1 else None
 
     # resident inputs (generated on the host by the shared generator, uploaded once)
     items_h = synth.make_items(rank, 0, n, max(B, 16))[:, :B].copy()
@@ -372,21 +370,19 @@ def main():
                 "unit": "GB/s", "frac": kern[dom]["frac"], "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": kern[dom]["bytes"]}
     exch = None
-    xfer_ms = {"fused": ph["scatter"], "ce": ph["scatter"] + ph["payload_exchange"]}.get(exchange,
-                                                                                      ph["payload_exchange"])
+    xfer_ms = ph["scatter"] if exchange == "fused" else ph["payload_exchange"]
     if N > 1 and xfer_ms > 0:
         # remote payload bytes this GPU sends per step / time of the phase that moves them
-        # (FUSED: the scatter pushes over NVLink; CE: scatter passes + the copy-engine tail;
-        # staged: the copy kernel / NCCL send-recv)
+        # (FUSED: the scatter pushes over NVLink; staged: the copy kernel / NCCL send-recv)
         gbs = (remote / K) / (xfer_ms / 1e3) / 1e9
         ceil = nvlink_ceilings(N)
         exch = {"gbs_per_gpu": gbs, "frac_of_900": gbs / 900.0, "frac_of_770_measured_p2p": gbs / 770.0,
                 "transport": exchange, "remote_bytes_per_step": remote / K, "kernel_ms": xfer_ms,
                 "ceilings_gbs": ceil}
-        if exchange in ("fused", "ce") and xfer_ms >= max(v["ms"] for v in kern.values()):
+        if exchange == "fused" and xfer_ms >= max(v["ms"] for v in kern.values()):
             # the step's dominant phase moves bytes over NVLink: that is its roofline
             # (peak: the profiling guide's measured 770 GB/s peer copy per direction)
-            roofline = {"bound": "nvlink", "kernel": "scatter" if exchange == "fused" else "scatter+ce_copies",
+            roofline = {"bound": "nvlink", "kernel": "scatter",
                         "achieved": gbs, "peak": 770.0, "unit": "GB/s", "frac": gbs / 770.0,
                         "traffic": None, "peak_source": "B200_PROFILING.md: measured peer copy 770 GB/s per "
                         "direction (nominal 900); this box's ceilings from tools/p2p_bw in ceilings_gbs",

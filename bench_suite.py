@@ -50,7 +50,7 @@ class Env:
         (self.torch, self.dist, self.rafi, self.world, self.rank, self.local, self.dev,
          self.comm) = setup(args)
         self.stream = self.torch.cuda.current_stream()
-        self.scatter = {"auto": 0, "threads": 1, "bulk": 2, "aligned": 3, "units": 4}[getattr(args, "scatter", "auto")]
+        self.scatter = {"auto": 0, "threads": 1, "bulk": 2}[getattr(args, "scatter", "auto")]
         self.tile = getattr(args, "tile", 0)
         self.control = {"auto": 0, "nccl": 1, "peer": 2}[getattr(args, "control", "auto")]
 
@@ -359,7 +359,7 @@ def fwd_rate(env, B, n, steps=5, warmup=2, pattern="uniform", graph=False):
     remote = st["bytes_sent_remote"]
     out = {"items_per_rank": n, "item_bytes": B, "ms_per_step": ms / steps, "instrumented_ms_per_step": ms_instr / steps,
            "value": N * n * steps / (ms / 1e3), "unit": "items/s",
-           "scatter": {1: "threads", 2: "bulk", 3: "aligned", 4: "units"}[ctx.get_option(env.rafi.OPT_SCATTER)],
+           "scatter": {1: "threads", 2: "bulk"}[ctx.get_option(env.rafi.OPT_SCATTER)],
            "tile": ctx.get_option(env.rafi.OPT_TILE), "scatter_ms": scat, "scatter_hbm_gbs": n * (2 * B + 4) / (scat / 1e3) / 1e9,
            "nvlink_gbs_per_gpu": (remote / (scat / 1e3) / 1e9) if N > 1 else None}
     if graph:
@@ -411,7 +411,7 @@ def main():
     p.add_argument("workload", choices=["cfg1", "cfg3", "cfg4", "cfg5", "sweep", "latency", "nbody", "streamlines"])
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--items", type=int, default=0)
-    p.add_argument("--scatter", default="auto", choices=["auto", "threads", "bulk", "aligned", "units"])
+    p.add_argument("--scatter", default="auto", choices=["auto", "threads", "bulk"])
     p.add_argument("--tile", type=int, default=0, help="RAFI_OPT_TILE (0 = automatic)")
     p.add_argument("--control", default="auto", choices=["auto", "nccl", "peer"])
     p.add_argument("--sizes", default="", help="cfg5: comma-separated item sizes (default: the full sweep)")

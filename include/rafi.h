@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define RAFI_ABI_VERSION 1
+#define RAFI_ABI_VERSION 2
 
 typedef enum {
   RAFI_OK = 0,
@@ -45,7 +45,9 @@ typedef enum {
   RAFI_ERR_NOMEM = -4,         /* device or pinned-host allocation failed */
   RAFI_ERR_RECV_OVERFLOW = -5, /* some rank would receive more than its capacity (collective) */
   RAFI_ERR_STATE = -6,         /* context is unusable after an earlier collective error */
-  RAFI_ERR_UNSUPPORTED = -7    /* valid request this build/configuration does not support */
+  RAFI_ERR_UNSUPPORTED = -7,   /* valid request this build/configuration does not support */
+  RAFI_ERR_TIMEOUT = -8,       /* a peer-control wait exceeded RAFI_OPT_PEER_TIMEOUT_MS (context unusable) */
+  RAFI_ERR_BOOTSTRAP = -9      /* the host all-gather callback of rafi_create_boot reported failure */
 } rafi_status;
 
 typedef struct rafi_ctx rafi_ctx; /* opaque; owns all queues */
@@ -115,10 +117,13 @@ typedef struct {
                                       accumulated sums in rafi_stats; default 0 */
 #define RAFI_OPT_TILE 3            /* binning tile in items (256 * 2^k, k <= 4); 0 = auto from item size */
 #define RAFI_OPT_SELF_DIRECT 4     /* reserved (self run placement); 0 */
-#define RAFI_OPT_CE_PASSES 6       /* RAFI_EXCHANGE_CE: scatter passes per forward, 1..16 (0 = automatic:
-                                      about 2M items per pass, at most 8) */
-#define RAFI_OPT_CONTROL 7         /* count exchange and completion barrier of FUSED/CE forwards:
-                                      RAFI_CONTROL_* (default AUTO) */
+#define RAFI_OPT_CONTROL 7         /* count exchange and completion barrier of FUSED forwards:
+                                      RAFI_CONTROL_* (default AUTO).  Every rank must use the same setting */
+#define RAFI_OPT_PEER_TIMEOUT_MS 9 /* RAFI_CONTROL_PEER: how long a kernel waits for a peer's mailbox flag
+                                      before giving up, ms (default 20000; 0 = wait forever).  A wait that
+                                      times out moves nothing, leaves the kernel normally and makes the
+                                      forward (or the next rafi_sync_host) return RAFI_ERR_TIMEOUT; the
+                                      context is then unusable.  No trap: the CUDA context stays healthy */
 #define RAFI_OPT_FORWARD_GRAPH 8   /* 1 (default) = a blocking FUSED rafi_forward launches its kernels, the
                                       collectives and the read-back of the counts as one cached CUDA graph
                                       (re-captured after any option change or resize); 0 = one launch each.
@@ -126,8 +131,8 @@ typedef struct {
 #define RAFI_OPT_SCATTER 5         /* how the binning scatter writes destination runs:
                                       RAFI_SCATTER_* (default AUTO).  Same result bytes either way.
                                       Only between rounds; re-chooses the tile unless RAFI_OPT_TILE
-                                      pinned it.  RAFI_ERR_UNSUPPORTED if BULK/ALIGNED is asked for an
-                                      item size that is not a multiple of 4 or a tile that does not fit */
+                                      pinned it.  RAFI_ERR_UNSUPPORTED if BULK is asked for an item size
+                                      that is not a multiple of 4 or a tile that does not fit */
 
 #define RAFI_SCATTER_AUTO 0        /* BULK when the scatter pushes runs to NVLink peers (FUSED over several
                                       processes) and BULK is supported, else THREADS (measured winners) */
@@ -137,18 +142,22 @@ typedef struct {
 #define RAFI_SCATTER_BULK 2        /* runs are permuted in shared memory and written by TMA bulk stores
                                       (cp.async.bulk shared->global, local or NVLink peer); threads write
                                       only the unaligned < 16-B heads and tails; item_bytes % 4 == 0 */
-#define RAFI_SCATTER_UNITS 4       /* THREADS with item-unit stores only (no 16-B chunk gathering): comparison */
-#define RAFI_SCATTER_ALIGNED 3     /* runs are permuted in shared memory, placed congruent to their global
-                                      address mod 16, and written by threads as 16-B-aligned vector
-                                      stores whatever the item size; item_bytes % 4 == 0 */
 
-#define RAFI_CONTROL_AUTO 0        /* PEER when every rank's queues are mapped, else NCCL */
+#define RAFI_CONTROL_AUTO 0        /* PEER when every rank's queues are mapped and no two processes share a
+                                      device, else NCCL when there is a communicator, else HOST */
 #define RAFI_CONTROL_NCCL 1        /* ncclAllGather of the count rows, ncclAllReduce as the completion barrier */
 #define RAFI_CONTROL_PEER 2        /* the scan kernel's last block pushes this process's count rows into
                                       every peer's CUDA-IPC mailbox over NVLink, fences once and raises a
                                       flag in each; the scatter kernel's last block runs the completion
-                                      barrier the same way; both spin on ld.acquire.sys (a peer that never
-                                      arrives traps after 20 s).  Every rank must use the same setting */
+                                      barrier the same way; both spin on ld.acquire.sys (bounded by
+                                      RAFI_OPT_PEER_TIMEOUT_MS).  Refused (RAFI_ERR_UNSUPPORTED) when two
+                                      processes share a device: nothing makes their kernels co-resident */
+#define RAFI_CONTROL_HOST 3        /* the paper's host-side count exchange: each process copies
+                                      its count rows to the host, the bootstrap's all-gather callback
+                                      (rafi_create_boot) exchanges them, the plan runs on the device, and
+                                      after the scatter a host all-gather is the completion barrier.  No
+                                      kernel ever waits on another process.  Needs a bootstrap; blocking
+                                      forwards only (rafi_forward_async: RAFI_ERR_UNSUPPORTED) */
 
 #define RAFI_EXCHANGE_AUTO 0       /* FUSED when every rank's queues are addressable, else NCCL */
 #define RAFI_EXCHANGE_NCCL 1       /* stage the sorted batch, grouped ncclSend/ncclRecv (one local rank per process) */
@@ -158,13 +167,6 @@ typedef struct {
                                       rank's incoming queue (local HBM or NVLink peer memory); the count
                                       matrix is exchanged first (RAFI_OPT_CONTROL); no send batch, no
                                       separate copy */
-#define RAFI_EXCHANGE_CE 4         /* copy-engine pipeline: counts all-gathered first; the scatter runs in
-                                      passes over the batch, writing the self run straight into the own
-                                      incoming queue and peer runs into the send batch; after each pass the
-                                      DMA copy engines move that pass's runs into the peers' incoming queues
-                                      (cudaMemcpyAsync over CUDA-IPC pointers, one stream per peer) while the
-                                      SMs scatter the next pass.  Several processes, one local rank each,
-                                      every rank's queues mapped; not capturable (rafi_forward_async) */
 
 /* ---- lifecycle ------------------------------------------------------------ */
 
@@ -176,10 +178,37 @@ int rafi_create(rafi_ctx** out, size_t item_bytes, size_t capacity, void* nccl_c
 /* General form; see rafi_create_params.  COLLECTIVE over nccl_comm. */
 int rafi_create_ex(rafi_ctx** out, const rafi_create_params* params);
 
+/* Host all-gather over the process group: every process calls it with the
+ * same `bytes`; on return recv[p*bytes, (p+1)*bytes) holds process p's send.
+ * Blocking and collective; returns 0 on success.  Any host transport works
+ * (MPI_Allgather, a torch.distributed gloo group, ...): the paper exchanges
+ * counts over MPI on the host. */
+typedef int (*rafi_allgather_fn)(void* user, const void* send, void* recv, size_t bytes);
+
+typedef struct {
+  int nprocs;                  /* processes in the group (>= 1) */
+  int proc;                    /* this process's index in [0, nprocs) */
+  rafi_allgather_fn allgather; /* required when nprocs > 1 */
+  void* user;                  /* passed through to allgather */
+} rafi_bootstrap;
+
+/* rafi_create_ex with a host bootstrap instead of (or besides) an NCCL
+ * communicator: the process group is `boot` (params->nccl_comm may be NULL;
+ * if given it must span the same processes in the same order).  The bootstrap
+ * carries the CUDA-IPC handles of every queue, so without NCCL the FUSED and
+ * PEER exchanges run under RAFI_CONTROL_PEER or RAFI_CONTROL_HOST (the NCCL
+ * exchange and control need params->nccl_comm).  Processes may share a device
+ * (e.g. tests on one GPU): AUTO control is then HOST.  Creation fails on every
+ * process with RAFI_ERR_INVALID_ARG if item_bytes, capacity or local_ranks
+ * differ between processes.  COLLECTIVE over the group. */
+int rafi_create_boot(rafi_ctx** out, const rafi_create_params* params, const rafi_bootstrap* boot);
+
 /* resizeRayQueues(N): reallocates every queue of every local
  * rank to `capacity` items.  Incoming items are kept up to the new capacity;
  * the outgoing queue must be empty (no emits since the last forward), else
- * RAFI_ERR_INVALID_ARG.  Not concurrent with emits or forwards.  COLLECTIVE. */
+ * RAFI_ERR_INVALID_ARG.  Not concurrent with emits or forwards.  COLLECTIVE:
+ * every process must pass the same capacity (checked); the old queues are
+ * freed only after every process has closed its CUDA-IPC mappings of them. */
 int rafi_resize(rafi_ctx* ctx, size_t capacity);
 
 /* Frees all queues.  Does NOT destroy the communicator or the stream.  Waits
@@ -229,13 +258,14 @@ int64_t rafi_forward(rafi_ctx* ctx);
  * forward on the context stream (so it can be captured into a CUDA graph,
  * NCCL collectives included) and, when the work runs, writes G -- the same
  * value rafi_forward returns -- to *G_dev (device-visible u64;
- * it may be mapped pinned host memory).  On a receive overflow nothing moves
- * and *G_dev = ~0ull; the context becomes unusable at the next
- * rafi_sync_host.  Host-side counters (rafi_num_incoming, rafi_get_stats and
+ * it may be mapped pinned host memory).  On a receive overflow (or a peer
+ * control timeout) nothing moves and *G_dev = ~0ull; the context becomes
+ * unusable and the next rafi_sync_host returns the error.  Host-side counters (rafi_num_incoming, rafi_get_stats and
  * the num_in field of views) are NOT refreshed: device code must read
  * numIncoming through num_in_dev (rafi::Queue does), and launches sized on
  * the host should cover the capacity.  COLLECTIVE.  Needs the FUSED exchange
- * (RAFI_ERR_UNSUPPORTED otherwise). */
+ * (RAFI_ERR_UNSUPPORTED otherwise) and NCCL or PEER control.  A pending
+ * rafi_read_incoming_async is waited for in stream order first. */
 int rafi_forward_async(rafi_ctx* ctx, unsigned long long* G_dev);
 
 /* Blocks until the context stream is idle and refreshes the host-side
@@ -244,7 +274,10 @@ int rafi_sync_host(rafi_ctx* ctx);
 
 /* Capture work issued on the context stream (app kernels, rafi_forward_async)
  * into an executable CUDA graph (*exec, cudaGraphExec_t), and replay it.  The
- * context stream must not be the legacy default stream. */
+ * context stream must not be the legacy default stream.  rafi_capture_begin
+ * and rafi_graph_launch first make the context stream wait (stream-ordered)
+ * for any pending rafi_read_incoming_async, so a replayed forward never
+ * rewrites an incoming queue that is still being copied out. */
 int rafi_capture_begin(rafi_ctx* ctx);
 int rafi_capture_end(rafi_ctx* ctx, void** exec);
 int rafi_graph_launch(rafi_ctx* ctx, void* exec);
@@ -267,7 +300,8 @@ int rafi_read_incoming(const rafi_ctx* ctx, int local, void* dst, uint64_t first
  * work already enqueued on the context stream, and overlaps later work -- in
  * particular the next rafi_emit_bulk's host-to-device copy, which runs on a
  * separate copy-in stream.  The next forward waits for it before rewriting
- * the incoming queue.  dst must stay valid until rafi_read_wait returns. */
+ * the incoming queue.  dst must stay valid until rafi_read_wait returns.
+ * Not while the context stream is being captured (RAFI_ERR_UNSUPPORTED). */
 int rafi_read_incoming_async(rafi_ctx* ctx, int local, void* dst, uint64_t first, uint64_t count);
 
 /* Blocks until every rafi_read_incoming_async of the context has landed. */
@@ -302,6 +336,19 @@ int rafi_nccl_unique_id(void* id128);
 /* ncclCommInitRank on `device` (-1 = current); *comm receives an ncclComm_t. */
 int rafi_nccl_comm_init(void** comm, int nranks, int rank, const void* id128, int device);
 int rafi_nccl_comm_destroy(void* comm);
+
+/* ---- diagnostics ------------------------------------------------------------ */
+
+/* Self-test of the peer-control protocol (RAFI_CONTROL_PEER: the count
+ * exchange of a5, and the completion barrier) on ONE device, where
+ * processes cannot be co-scheduled: P blocks of one cooperative launch each
+ * play a process with its own mailbox and L local ranks, for `rounds` rounds
+ * of [write own count rows, count exchange, check the whole R x R matrix,
+ * completion barrier].  Block `absent` (>= 0) never arrives, so the others must
+ * give up after timeout_ms (0 = never: only with absent < 0).  *bad = matrix
+ * entries that arrived wrong; *timed_out = processes whose wait gave up. */
+int rafi_selftest_peer_control(int device, int P, int L, int rounds, int absent, long long timeout_ms,
+                               uint64_t* bad, uint64_t* timed_out);
 
 /* ---- host-side planning (pure host code; no GPU needed) --------------------- */
 

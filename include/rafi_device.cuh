@@ -17,15 +17,54 @@
  * exceed the output queue size will simply get dropped"); the
  * counter itself is not clamped, so the host can report drops.  A destination
  * outside [0, R) is rejected without taking a slot and counted separately.
+ *
+ * Item moves are vectorised by sizeof(T): 16-byte stores/loads when
+ * sizeof(T) % 16 == 0, 8-byte when % 8 == 0, 4-byte when % 4 == 0, bytes
+ * otherwise.  The queues are cudaMalloc'd (256-byte aligned), so slot *
+ * sizeof(T) keeps that alignment.  Needs C++17 (if constexpr).
  */
 #ifndef RAFI_DEVICE_CUH
 #define RAFI_DEVICE_CUH
 
+#include <cstring>
 #include <type_traits>
 
 #include "rafi.h"
 
 namespace rafi {
+
+/* Widest unit (16, 8, 4 or 1 bytes) that divides sizeof(T). */
+template <class T>
+struct ItemUnit {
+  using type = std::conditional_t<
+      sizeof(T) % 16 == 0, uint4,
+      std::conditional_t<sizeof(T) % 8 == 0, uint2, std::conditional_t<sizeof(T) % 4 == 0, unsigned, unsigned char>>>;
+  static constexpr size_t count = sizeof(T) / sizeof(type);
+};
+
+/* Store item at dst (aligned to ItemUnit<T>) in unit-wide stores. */
+template <class T>
+__device__ __forceinline__ void store_item(void* dst, const T& item) {
+  using U = typename ItemUnit<T>::type;
+  U tmp[ItemUnit<T>::count];
+  memcpy(tmp, &item, sizeof(T));
+  U* d = static_cast<U*>(dst);
+#pragma unroll
+  for (size_t k = 0; k < ItemUnit<T>::count; ++k) d[k] = tmp[k];
+}
+
+/* Load an item from src (aligned to ItemUnit<T>) in unit-wide loads. */
+template <class T>
+__device__ __forceinline__ T load_item(const void* src) {
+  using U = typename ItemUnit<T>::type;
+  U tmp[ItemUnit<T>::count];
+  const U* s = static_cast<const U*>(src);
+#pragma unroll
+  for (size_t k = 0; k < ItemUnit<T>::count; ++k) tmp[k] = s[k];
+  T item;
+  memcpy(&item, tmp, sizeof(T));
+  return item;
+}
 
 __device__ __forceinline__ unsigned lane_id() {
   unsigned l;
@@ -60,7 +99,7 @@ struct Queue {
 
   /* getIncoming(i). */
   __device__ T getIncoming(unsigned long long i) const {
-    return reinterpret_cast<const T*>(v.in)[i];
+    return load_item<T>(static_cast<const char*>(v.in) + i * sizeof(T));
   }
 
   /* emitOutgoing(item, dest); returns true iff stored. */
@@ -80,7 +119,7 @@ struct Queue {
     base = __shfl_sync(vmask, base, leader);
     const unsigned long long slot = base + __popc(vmask & lanemask_lt());
     if (slot >= v.capacity) return false;
-    reinterpret_cast<T*>(v.out)[slot] = item;
+    store_item<T>(static_cast<char*>(v.out) + slot * sizeof(T), item);
     v.dest[slot] = dest;
     return true;
   }

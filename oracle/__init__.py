@@ -19,7 +19,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "rafi_oracle.c")
-_SRCS = [_SRC, os.path.join(_HERE, "proxies.c"), os.path.join(_HERE, "nbody.c"), os.path.join(_HERE, "streamlines.c")]
+_SRCS = [_SRC, os.path.join(_HERE, "digest.c"), os.path.join(_HERE, "proxies.c"), os.path.join(_HERE, "nbody.c"),
+         os.path.join(_HERE, "streamlines.c")]
 _LIB = os.path.join(_HERE, "liborafi.so")
 
 OK = 0
@@ -79,6 +80,14 @@ def lib():
             "orc_send_off_ptr": (P, [P]),
             "orc_recv_off_ptr": (P, [P]),
             "orc_G": (u64, [P]),
+            # digest.c (streaming-digest mode of the plain forward)
+            "orc_digest_items": (u64, [vp, u64, u64]),
+            "orc_digest_create": (P, [i32, u64, u64]),
+            "orc_digest_destroy": (None, [P]),
+            "orc_digest_feed": (i32, [P, i32, vp, vp, u64]),
+            "orc_digest_finish": (i64, [P]),
+            "orc_digest_value": (u64, [P, i32]),
+            "orc_digest_C_ptr": (P, [P]),
             # proxies.c (CPU twins of the proxy applications)
             "orc_grid_owner": (i32, [C.c_float, C.c_float, C.c_float, i32, i32, i32]),
             "orc_advect_seed": (None, [P, i32, u64, u64, i32, i32, i32]),
@@ -233,6 +242,58 @@ class World:
     def march_step(self, r, seed, p_thr, max_bounces, max_steps, grid, result: np.ndarray):
         assert result.dtype == np.float32 and result.flags["C_CONTIGUOUS"]
         lib().orc_march_step(self._w, r, seed, p_thr, max_bounces, max_steps, *grid, result.ctypes.data)
+
+
+class Digest:
+    """Streaming-digest mode (oracle/digest.c): the plain forward's count
+    matrix, G and a digest of every incoming queue, from the sources' queues
+    fed once in (source, slot) order -- nothing materialised."""
+
+    def __init__(self, R: int, cap: int, B: int):
+        self.R, self.cap, self.B = int(R), int(cap), int(B)
+        self._g = lib().orc_digest_create(self.R, self.cap, self.B)
+        if not self._g:
+            raise MemoryError("orc_digest_create failed")
+
+    def close(self):
+        if self._g:
+            lib().orc_digest_destroy(self._g)
+            self._g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def feed(self, s: int, items: np.ndarray, dests: np.ndarray):
+        items = np.ascontiguousarray(items, dtype=np.uint8)
+        dests = np.ascontiguousarray(dests, dtype=np.int32)
+        n = dests.size
+        assert items.size == n * self.B
+        if n == 0:
+            return
+        rc = lib().orc_digest_feed(self._g, s, _ptr(items), _ptr(dests), n)
+        if rc != OK:
+            raise ValueError("orc_digest_feed rc=%d" % rc)
+
+    def finish(self) -> int:
+        return int(lib().orc_digest_finish(self._g))
+
+    def value(self, d: int) -> int:
+        return int(lib().orc_digest_value(self._g, d))
+
+    def C(self) -> np.ndarray:
+        return _view(lib().orc_digest_C_ptr(self._g), self.R * self.R, np.uint64).reshape(self.R, self.R).copy()
+
+
+def digest_items(items: np.ndarray, B: int) -> int:
+    """The digest fold of oracle/digest.c applied to a materialised queue."""
+    items = np.ascontiguousarray(items, dtype=np.uint8)
+    n = items.size // B
+    if n == 0:
+        return int(lib().orc_digest_items(None, 0, B))
+    return int(lib().orc_digest_items(_ptr(items), n, B))
 
 
 NB_STATS = 42

@@ -87,9 +87,49 @@ static int upload_rank_table(Ctx* c) {
   return RAFI_OK;
 }
 
-// Every rank learns every rank's binned[0..1] and in pointers: local ones
-// directly, other processes' through CUDA IPC handles all-gathered over NCCL.
-// Collective.  peer_ok is decided identically on all ranks.
+// Host all-gather over the process group (collective, blocking): the
+// bootstrap's callback when there is one, else NCCL through a small device
+// buffer on the context stream.  recv[p * bytes ..] = process p's send.
+static int proc_allgather(Ctx* c, const void* send, void* recv, size_t bytes) {
+  if (c->nprocs == 1) {
+    std::memcpy(recv, send, bytes);
+    return RAFI_OK;
+  }
+  if (c->boot.allgather) {
+    if (c->boot.allgather(c->boot.user, send, recv, bytes) != 0) {
+      set_error("bootstrap all-gather callback failed");
+      return RAFI_ERR_BOOTSTRAP;
+    }
+    return RAFI_OK;
+  }
+  uint8_t* dbuf = nullptr;
+  RAFI_CK(alloc_dev((void**)&dbuf, bytes * c->nprocs));
+  int rc = RAFI_OK;
+  do {
+    if (cudaMemcpyAsync(dbuf + bytes * c->proc, send, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess) { rc = RAFI_ERR_CUDA; break; }
+    const ncclResult_t nr = ncclAllGather(dbuf + bytes * c->proc, dbuf, bytes, ncclUint8, c->comm, c->stream);
+    if (nr != ncclSuccess) { set_error(std::string("ncclAllGather: ") + ncclGetErrorString(nr)); rc = RAFI_ERR_NCCL; break; }
+    if (cudaMemcpyAsync(recv, dbuf, bytes * c->nprocs, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess) { rc = RAFI_ERR_CUDA; break; }
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess) { rc = RAFI_ERR_CUDA; break; }
+  } while (0);
+  if (rc == RAFI_ERR_CUDA) { cudaGetLastError(); set_error("proc_allgather: CUDA copy failed"); }
+  cudaFree(dbuf);
+  return rc;
+}
+
+// Host barrier over the process group.
+static int proc_barrier(Ctx* c) {
+  int one = 1;
+  std::vector<int> all(c->nprocs);
+  return proc_allgather(c, &one, all.data(), sizeof(int));
+}
+
+// Every rank learns every rank's binned[0..1], in and mailbox pointers:
+// local ones directly, other processes' through CUDA IPC handles all-gathered
+// over the process group.  The same exchange checks that every process
+// agrees on (item_bytes, capacity, local_ranks) and notes whether two
+// processes share a device.  Collective; peer_ok, shared_gpu and any
+// disagreement are decided identically on all ranks.
 static constexpr int kMapped = 4;  // binned[0], binned[1], in, mbox
 
 static uint8_t* mapped_buf(LocalRank& r, int b) {
@@ -108,6 +148,12 @@ static int upload_in_table(Ctx* c) {
   return RAFI_OK;
 }
 
+struct ProcRecord {  // what every process publishes at create / resize
+  uint64_t item_bytes, capacity;
+  int32_t local_ranks, ipc_ok;
+  uint8_t uuid[16];  // device UUID
+};
+
 static int exchange_peer_pointers(Ctx* c) {
   close_ipc(c);
   c->peer_binned.assign((size_t)c->R * 2, nullptr);
@@ -120,100 +166,103 @@ static int exchange_peer_pointers(Ctx* c) {
   };
   for (int l = 0; l < c->L; ++l)
     for (int b = 0; b < kMapped; ++b) place(c->proc * c->L + l, b, mapped_buf(c->lr[l], b));
-  if (c->nprocs == 1) { c->peer_ok = true; return upload_in_table(c); }
-  const size_t per = sizeof(cudaIpcMemHandle_t) * kMapped * c->L;
-  std::vector<uint8_t> mine(per), all(per * c->nprocs);
-  int ok = 1;
+  if (c->nprocs == 1) { c->peer_ok = true; c->shared_gpu = false; return upload_in_table(c); }
+  const size_t nh = (size_t)kMapped * c->L;
+  const size_t per = sizeof(ProcRecord) + sizeof(cudaIpcMemHandle_t) * nh;
+  std::vector<uint8_t> mine(per, 0), all(per * c->nprocs);
+  ProcRecord me{};
+  me.item_bytes = c->B;
+  me.capacity = c->cap;
+  me.local_ranks = c->L;
+  me.ipc_ok = 1;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, c->device) == cudaSuccess) std::memcpy(me.uuid, &prop.uuid, 16);
+  else cudaGetLastError();
   for (int l = 0; l < c->L; ++l)
     for (int b = 0; b < kMapped; ++b) {
       cudaIpcMemHandle_t h;
       std::memset(&h, 0, sizeof(h));
-      if (cudaIpcGetMemHandle(&h, mapped_buf(c->lr[l], b)) != cudaSuccess) { ok = 0; cudaGetLastError(); }
-      std::memcpy(mine.data() + sizeof(h) * (kMapped * l + b), &h, sizeof(h));
+      if (cudaIpcGetMemHandle(&h, mapped_buf(c->lr[l], b)) != cudaSuccess) { me.ipc_ok = 0; cudaGetLastError(); }
+      std::memcpy(mine.data() + sizeof(ProcRecord) + sizeof(h) * (kMapped * l + b), &h, sizeof(h));
     }
-  uint8_t* dbuf = nullptr;
-  RAFI_CK(alloc_dev((void**)&dbuf, per * c->nprocs + sizeof(int)));
-  int* dflag = reinterpret_cast<int*>(dbuf + per * c->nprocs);
-  int rc = RAFI_OK;
-  do {
-    if (cudaMemcpyAsync(dbuf + per * c->proc, mine.data(), per, cudaMemcpyHostToDevice, c->stream) != cudaSuccess) { rc = RAFI_ERR_CUDA; break; }
-    ncclResult_t nr = ncclAllGather(dbuf + per * c->proc, dbuf, per, ncclUint8, c->comm, c->stream);
-    if (nr != ncclSuccess) { set_error(std::string("ncclAllGather(ipc): ") + ncclGetErrorString(nr)); rc = RAFI_ERR_NCCL; break; }
-    if (cudaMemcpyAsync(all.data(), dbuf, per * c->nprocs, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess) { rc = RAFI_ERR_CUDA; break; }
-    if (cudaStreamSynchronize(c->stream) != cudaSuccess) { rc = RAFI_ERR_CUDA; break; }
-    for (int p = 0; p < c->nprocs && ok; ++p) {
-      if (p == c->proc) continue;
-      for (int l = 0; l < c->L && ok; ++l)
-        for (int b = 0; b < kMapped && ok; ++b) {
-          cudaIpcMemHandle_t h;
-          std::memcpy(&h, all.data() + per * p + sizeof(h) * (kMapped * l + b), sizeof(h));
-          void* ptr = nullptr;
-          if (cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-            ok = 0; cudaGetLastError(); break;
-          }
-          c->ipc_opened.push_back(ptr);
-          place(p * c->L + l, b, (uint8_t*)ptr);
+  std::memcpy(mine.data(), &me, sizeof(me));
+  RAFI_CK(proc_allgather(c, mine.data(), all.data(), per));
+  auto rec = [&](int p) {
+    ProcRecord r;
+    std::memcpy(&r, all.data() + per * p, sizeof(r));
+    return r;
+  };
+  bool agree = true;
+  c->shared_gpu = false;
+  for (int p = 0; p < c->nprocs; ++p) {
+    const ProcRecord r = rec(p);
+    if (r.item_bytes != c->B || r.capacity != c->cap || r.local_ranks != c->L) agree = false;
+    for (int q = 0; q < p; ++q)
+      if (std::memcmp(rec(q).uuid, r.uuid, 16) == 0) c->shared_gpu = true;
+  }
+  if (!agree) {
+    set_error("processes disagree on item_bytes, capacity or local_ranks");
+    return RAFI_ERR_INVALID_ARG;
+  }
+  int ok = 1;
+  for (int p = 0; p < c->nprocs; ++p) ok &= rec(p).ipc_ok;
+  for (int p = 0; p < c->nprocs && ok; ++p) {
+    if (p == c->proc) continue;
+    for (int l = 0; l < c->L && ok; ++l)
+      for (int b = 0; b < kMapped && ok; ++b) {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, all.data() + per * p + sizeof(ProcRecord) + sizeof(h) * (kMapped * l + b), sizeof(h));
+        void* ptr = nullptr;
+        if (cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+          ok = 0; cudaGetLastError(); break;
         }
-    }
-    // agree: peer modes only if every process mapped every peer
-    if (cudaMemcpyAsync(dflag, &ok, sizeof(int), cudaMemcpyHostToDevice, c->stream) != cudaSuccess) { rc = RAFI_ERR_CUDA; break; }
-    nr = ncclAllReduce(dflag, dflag, 1, ncclInt32, ncclMin, c->comm, c->stream);
-    if (nr != ncclSuccess) { set_error(std::string("ncclAllReduce(ipc ok): ") + ncclGetErrorString(nr)); rc = RAFI_ERR_NCCL; break; }
-    int all_ok = 0;
-    if (cudaMemcpyAsync(&all_ok, dflag, sizeof(int), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess) { rc = RAFI_ERR_CUDA; break; }
-    if (cudaStreamSynchronize(c->stream) != cudaSuccess) { rc = RAFI_ERR_CUDA; break; }
-    c->peer_ok = all_ok != 0;
-  } while (0);
-  cudaFree(dbuf);
+        c->ipc_opened.push_back(ptr);
+        place(p * c->L + l, b, (uint8_t*)ptr);
+      }
+  }
+  // agree: peer modes only if every process mapped every peer
+  std::vector<int> oks(c->nprocs);
+  RAFI_CK(proc_allgather(c, &ok, oks.data(), sizeof(int)));
+  c->peer_ok = true;
+  for (int v : oks) c->peer_ok = c->peer_ok && v;
   if (!c->peer_ok) {
     close_ipc(c);
     c->peer_binned.assign((size_t)c->R * 2, nullptr);
     c->peer_in.assign((size_t)c->R, nullptr);
     c->peer_mbox.assign((size_t)c->R, nullptr);
   }
-  if (rc == RAFI_OK) rc = upload_in_table(c);
-  return rc;
+  return upload_in_table(c);
 }
 
 static void drop_fwd_graph(Ctx* c);
 
-static void free_ce(Ctx* c) {
-  for (size_t i = 0; i < c->ce_streams.size(); ++i) {
-    if (c->ce_streams[i]) { cudaStreamSynchronize(c->ce_streams[i]); cudaStreamDestroy(c->ce_streams[i]); }
-    if (c->ce_done[i]) cudaEventDestroy(c->ce_done[i]);
+// Effective control of a multi-process forward (RAFI_OPT_CONTROL): who
+// exchanges the counts (a5) and runs the completion barrier.
+static int resolve_control(Ctx* c, int want) {
+  int x = want;
+  const bool peer_possible = c->peer_ok && !c->shared_gpu;
+  if (c->nprocs == 1) {
+    x = RAFI_CONTROL_AUTO;  // one process: nothing to exchange
+  } else if (x == RAFI_CONTROL_AUTO) {
+    x = peer_possible ? RAFI_CONTROL_PEER : c->comm ? RAFI_CONTROL_NCCL : RAFI_CONTROL_HOST;
   }
-  c->ce_streams.clear(); c->ce_done.clear();
-  for (auto& e : c->ce_pass)
-    if (e) { cudaEventDestroy(e); e = nullptr; }
-  cudaFree(c->ce_table_dev); cudaFree(c->bounds_dev);
-  cudaFreeHost(c->bounds_host); cudaFreeHost(c->off_host);
-  c->ce_table_dev = nullptr; c->bounds_dev = c->bounds_host = nullptr; c->off_host = nullptr;
-}
-
-// RAFI_EXCHANGE_CE resources: the destination table (own incoming queue for
-// the self run, the send batch for every peer), pass bounds, copy streams.
-static int ensure_ce(Ctx* c) {
-  if (c->ce_table_dev) return RAFI_OK;
-  const int R = c->R, me = c->proc;
-  RAFI_CK(alloc_dev((void**)&c->ce_table_dev, sizeof(uint8_t*) * R));
-  RAFI_CK(alloc_dev((void**)&c->bounds_dev, sizeof(uint32_t) * (Ctx::kMaxPasses + 1) * R));
-  if (cudaMallocHost((void**)&c->bounds_host, sizeof(uint32_t) * (Ctx::kMaxPasses + 1) * R) != cudaSuccess ||
-      cudaMallocHost((void**)&c->off_host, sizeof(uint64_t) * R) != cudaSuccess) {
-    cudaGetLastError();
-    set_error("cudaMallocHost failed");
-    return RAFI_ERR_NOMEM;
+  if (x == RAFI_CONTROL_PEER && !peer_possible) {
+    set_error(c->shared_gpu ? "PEER control spins on flags other processes raise: refused when processes share a "
+                              "device (no co-residency guarantee); use HOST control"
+                            : "PEER control needs every rank's mailbox mapped (CUDA IPC failed)");
+    return RAFI_ERR_UNSUPPORTED;
   }
-  std::vector<uint8_t*> t(R);
-  for (int d = 0; d < R; ++d) t[d] = d == me ? c->lr[0].in : c->lr[0].binned[0];
-  RAFI_CK_CUDA(cudaMemcpy(c->ce_table_dev, t.data(), sizeof(uint8_t*) * R, cudaMemcpyHostToDevice));
-  c->ce_streams.assign(R, nullptr);
-  c->ce_done.assign(R, nullptr);
-  for (int d = 0; d < R; ++d) {
-    if (d == me) continue;
-    RAFI_CK_CUDA(cudaStreamCreateWithFlags(&c->ce_streams[d], cudaStreamNonBlocking));
-    RAFI_CK_CUDA(cudaEventCreateWithFlags(&c->ce_done[d], cudaEventDisableTiming));
+  if (x == RAFI_CONTROL_NCCL && !c->comm) {
+    set_error("NCCL control needs an NCCL communicator");
+    return RAFI_ERR_UNSUPPORTED;
   }
-  for (auto& e : c->ce_pass) RAFI_CK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  if (x == RAFI_CONTROL_HOST && !c->boot.allgather) {
+    set_error("HOST control needs a bootstrap all-gather (rafi_create_boot)");
+    return RAFI_ERR_UNSUPPORTED;
+  }
+  c->control = want;
+  c->ctl_eff = x;
+  c->ctl_peer = x == RAFI_CONTROL_PEER;
   return RAFI_OK;
 }
 
@@ -228,19 +277,17 @@ static int resolve_exchange(Ctx* c) {
     set_error("NCCL exchange supports one local rank per process");
     return RAFI_ERR_UNSUPPORTED;
   }
-  if (x == RAFI_EXCHANGE_CE && (c->nprocs < 2 || c->L != 1 || !c->peer_ok)) {
-    set_error("CE exchange needs several processes, one local rank each, with every rank's queues mapped");
+  if (x == RAFI_EXCHANGE_NCCL && c->nprocs > 1 && !c->comm) {
+    set_error("NCCL exchange needs an NCCL communicator");
     return RAFI_ERR_UNSUPPORTED;
   }
-  if (x == RAFI_EXCHANGE_CE) RAFI_CK(ensure_ce(c));
-  c->ctl_peer = c->nprocs > 1 && c->peer_ok && c->control != RAFI_CONTROL_NCCL;
+  RAFI_CK(resolve_control(c, c->control));
   c->exchange_eff = x;
   return RAFI_OK;
 }
 
 // Effective scatter write path (RAFI_OPT_SCATTER).
 static constexpr size_t kMaxSmem = 227u * 1024u;  // opt-in shared memory per CTA on sm_100a
-static bool is_perm(int mode) { return mode == RAFI_SCATTER_BULK || mode == RAFI_SCATTER_ALIGNED; }
 
 static int resolve_scatter(Ctx* c) {
   int x = c->scatter;
@@ -248,11 +295,11 @@ static int resolve_scatter(Ctx* c) {
     // BULK where the scatter pushes runs to NVLink peers (measured faster there:
     // DESIGN.md section 6); THREADS for local HBM (faster at every item size)
     const bool remote_push = c->nprocs > 1 && c->exchange_eff == RAFI_EXCHANGE_FUSED;
-    x = remote_push && perm_supported(c->B) && perm_smem_bytes(RAFI_SCATTER_BULK, 256, c->B, c->R) <= kMaxSmem
+    x = remote_push && perm_supported(c->B) && perm_smem_bytes(256, c->B, c->R) <= kMaxSmem
             ? RAFI_SCATTER_BULK
             : RAFI_SCATTER_THREADS;
   }
-  if (is_perm(x) && !(perm_supported(c->B) && perm_smem_bytes(x, 256, c->B, c->R) <= kMaxSmem)) {
+  if (x == RAFI_SCATTER_BULK && !(perm_supported(c->B) && perm_smem_bytes(256, c->B, c->R) <= kMaxSmem)) {
     set_error("permuting scatter needs item_bytes % 4 == 0 and a 256-item tile that fits in shared memory");
     return RAFI_ERR_UNSUPPORTED;
   }
@@ -261,7 +308,7 @@ static int resolve_scatter(Ctx* c) {
 }
 
 static uint32_t auto_tile(const Ctx* c) {
-  return is_perm(c->scatter_eff) ? choose_tile_perm(c->scatter_eff, c->B, c->R) : choose_tile(c->B);
+  return c->scatter_eff == RAFI_SCATTER_BULK ? choose_tile_perm(c->B, c->R) : choose_tile(c->B);
 }
 
 // Binning tile (between rounds); grows H/O when the tile count grows.
@@ -299,7 +346,6 @@ static void destroy_ctx(Ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  free_ce(c);
   drop_fwd_graph(c);
   if (c->cap_stream) { cudaStreamDestroy(c->cap_stream); c->cap_stream = nullptr; }
   close_ipc(c);
@@ -323,7 +369,7 @@ static void destroy_ctx(Ctx* c) {
   delete c;
 }
 
-static int create(Ctx** out, const rafi_create_params* p) {
+static int create(Ctx** out, const rafi_create_params* p, const rafi_bootstrap* boot) {
   *out = nullptr;
   if (!p || p->item_bytes < 1 || p->local_ranks < 1 || p->item_bytes > (1u << 30)) {
     set_error("rafi_create: item_bytes >= 1 and local_ranks >= 1 required");
@@ -331,6 +377,11 @@ static int create(Ctx** out, const rafi_create_params* p) {
   }
   if (p->capacity >= (1ull << 32)) {
     set_error("rafi_create: capacity must be < 2^32 items (32-bit index in the sort key, PAPER:109)");
+    return RAFI_ERR_INVALID_ARG;
+  }
+  if (boot && (boot->nprocs < 1 || boot->proc < 0 || boot->proc >= boot->nprocs ||
+               (boot->nprocs > 1 && !boot->allgather))) {
+    set_error("rafi_create_boot: 0 <= proc < nprocs and an all-gather callback (nprocs > 1) required");
     return RAFI_ERR_INVALID_ARG;
   }
   Ctx* c = new (std::nothrow) Ctx();
@@ -352,6 +403,15 @@ static int create(Ctx** out, const rafi_create_params* p) {
       return fail(RAFI_ERR_NCCL);
     }
     c->nprocs = n; c->proc = r;
+  }
+  if (boot) {
+    if (c->comm && (boot->nprocs != c->nprocs || boot->proc != c->proc)) {
+      set_error("rafi_create_boot: the bootstrap and the NCCL communicator describe different groups");
+      return fail(RAFI_ERR_INVALID_ARG);
+    }
+    c->boot = *boot;
+    c->nprocs = boot->nprocs;
+    c->proc = boot->proc;
   }
   c->L = p->local_ranks;
   c->R = c->nprocs * c->L;
@@ -481,18 +541,81 @@ static int enqueue_fused(Ctx* c, unsigned long long* G_dev, bool T) {
   return RAFI_OK;
 }
 
-// Host refresh after device work: count matrix + counters -> host bookkeeping.
-static int refresh_host(Ctx* c, uint64_t* G) {
-  // control blocks and count matrix are one allocation: one copy back
-  RAFI_CK_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl, ctrl_c_bytes(c), cudaMemcpyDeviceToHost, c->stream));
-  RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
+static void mark_timing(Ctx* c, bool fused);
+
+// After the mirrored control blocks and count matrix reached the host: a
+// peer-control timeout (flagged by the kernels), else the bookkeeping and the
+// collective receive-overflow decision (Z3).
+static int finish_host(Ctx* c, uint64_t* G) {
   c->host_stale = false;
+  if (c->ctrl_host[0].status) {
+    c->broken = true;
+    set_error("peer control: a mailbox wait exceeded RAFI_OPT_PEER_TIMEOUT_MS (some process never arrived)");
+    return RAFI_ERR_TIMEOUT;
+  }
   if (book_keep(c, G)) {
     c->broken = true;
     set_error("receive overflow: some rank would receive more than its capacity");
     return RAFI_ERR_RECV_OVERFLOW;
   }
   return RAFI_OK;
+}
+
+// Host refresh after device work: count matrix + counters -> host bookkeeping.
+static int refresh_host(Ctx* c, uint64_t* G) {
+  // control blocks and count matrix are one allocation: one copy back
+  RAFI_CK_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl, ctrl_c_bytes(c), cudaMemcpyDeviceToHost, c->stream));
+  RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
+  return finish_host(c, G);
+}
+
+// Count exchange on the host (a5 as the paper does it): after the
+// scan, copy this process's L count rows to the host, all-gather them over
+// the process group into the mirrored R x R matrix, and (to_dev) upload the
+// whole matrix for the device-side plan.  Blocking.
+static int host_count_exchange(Ctx* c, bool to_dev) {
+  const size_t rows = (size_t)c->L * c->R;
+  RAFI_CK_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl, ctrl_c_bytes(c), cudaMemcpyDeviceToHost, c->stream));
+  RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
+  std::vector<uint64_t> mine(c->Chost + c->proc * rows, c->Chost + (c->proc + 1) * rows);
+  RAFI_CK(proc_allgather(c, mine.data(), c->Chost, rows * sizeof(uint64_t)));  // process-major = rank-major
+  if (to_dev)
+    RAFI_CK_CUDA(cudaMemcpyAsync(c->Cdev, c->Chost, sizeof(uint64_t) * c->R * c->R, cudaMemcpyHostToDevice,
+                                 c->stream));
+  return RAFI_OK;
+}
+
+// FUSED forward under HOST control: no kernel waits on another process.
+//   hist -> scan -> D2H rows, host all-gather, H2D matrix -> plan ->
+//   scatter+push -> stream sync -> host barrier
+static int64_t forward_fused_host(Ctx* c) {
+  const bool T = c->timing;
+  c->fwd_launches = 0;
+  if (T) RAFI_CK_CUDA(record_ev(c, 0));
+  RAFI_CK(launch_hist(c));
+  if (T) RAFI_CK_CUDA(record_ev(c, 1));
+  RAFI_CK(launch_scan(c, 0, nullptr, false));
+  if (T) RAFI_CK_CUDA(record_ev(c, 2));
+  RAFI_CK(host_count_exchange(c, true));
+  RAFI_CK(launch_plan(c, true, nullptr));  // offsets, num_in, and ovf (identical on every rank)
+  if (T) RAFI_CK_CUDA(record_ev(c, 3));
+  uint64_t G = 0;
+  int rc = finish_host(c, &G);  // overflow: the scatter below moves nothing (ovf), every rank errs alike
+  RAFI_CK(launch_scatter(c, true, true));
+  if (T) RAFI_CK_CUDA(record_ev(c, 4));
+  RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
+  // completion barrier: every process's pushes have landed once all arrive
+  RAFI_CK(proc_barrier(c));
+  if (T) {
+    RAFI_CK_CUDA(record_ev(c, 5));
+    RAFI_CK_CUDA(record_ev(c, 6));
+  }
+  if (rc != RAFI_OK) return rc;
+  if (T) mark_timing(c, true);
+  c->last_fused = true;
+  c->round += 1;
+  c->last_G = (int64_t)G;
+  return (int64_t)G;
 }
 
 // Phase timings are read lazily -- at the next forward or stats read, off the
@@ -580,6 +703,7 @@ static int build_fwd_graph(Ctx* c, bool T) {
 }
 
 static int64_t forward_fused(Ctx* c) {
+  if (c->nprocs > 1 && c->ctl_eff == RAFI_CONTROL_HOST) return forward_fused_host(c);
   const bool T = c->timing;
   uint64_t G = 0;
   if (c->fwd_graph && !T) {
@@ -591,12 +715,7 @@ static int64_t forward_fused(Ctx* c) {
     c->launches += c->fwd_graph_launches;
     c->fwd_launches = c->fwd_graph_launches;
     RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
-    c->host_stale = false;
-    if (book_keep(c, &G)) {
-      c->broken = true;
-      set_error("receive overflow: some rank would receive more than its capacity");
-      return RAFI_ERR_RECV_OVERFLOW;
-    }
+    RAFI_CK(finish_host(c, &G));
   } else {
     RAFI_CK(enqueue_fused(c, nullptr, T));
     RAFI_CK(refresh_host(c, &G));
@@ -624,10 +743,17 @@ static int64_t forward_staged(Ctx* c) {
   // a5: every process learns the whole R x R count matrix.  The all-gather is
   // ordered after each process's scatter on its stream, so once it completes
   // every rank's send batch is final (what the PEER pull relies on).
-  if (c->nprocs > 1)
+  if (c->nprocs > 1 && c->comm) {
     RAFI_CK_NCCL(ncclAllGather(c->Cdev + (size_t)c->proc * L * R, c->Cdev, (size_t)L * R, ncclUint64, c->comm,
                                c->stream));
-  RAFI_CK_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl, ctrl_c_bytes(c), cudaMemcpyDeviceToHost, c->stream));
+    RAFI_CK_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl, ctrl_c_bytes(c), cudaMemcpyDeviceToHost, c->stream));
+  } else if (c->nprocs > 1) {
+    // no communicator: the rows go through the bootstrap's host all-gather
+    // (each process synchronises first, so every send batch is final)
+    RAFI_CK(host_count_exchange(c, false));
+  } else {
+    RAFI_CK_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl, ctrl_c_bytes(c), cudaMemcpyDeviceToHost, c->stream));
+  }
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[4], c->stream));
   RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
   // plan and the collective overflow decision (Z3)
@@ -716,110 +842,30 @@ static int64_t forward_staged(Ctx* c) {
   return (int64_t)G;
 }
 
-// CE forward: the payload moves on the DMA copy engines, pipelined with the
-// scatter (PAPER:492 names asynchronous streams as the way to overlap).
-//   hist -> scan -> [all-gather counts] -> pass bounds -> D2H, host plan ->
-//   for each pass k: scatter pass k (self run -> own incoming queue, peer runs
-//   -> send batch) ; copy streams: pass k's peer runs -> peers' incoming queues
-//   -> join copies -> [completion all-reduce]
-// Item order is the FUSED/staged order: source-major, slot order within a
-// source (pass k's run of (me, d) precedes pass k+1's in the receiver).
-static int64_t forward_ce(Ctx* c) {
-  const int R = c->R, me = c->proc;
-  const uint64_t B = c->B;
-  const bool T = c->timing;
-  c->fwd_launches = 0;
-  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[0], c->stream));
-  RAFI_CK(launch_hist(c));
-  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[1], c->stream));
-  RAFI_CK(launch_scan(c, 0, nullptr, c->ctl_peer));  // peer control: counts exchanged by its last block
-  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[2], c->stream));
-  if (!c->ctl_peer)
-    RAFI_CK_NCCL(ncclAllGather(c->Cdev + (size_t)me * R, c->Cdev, (size_t)R, ncclUint64, c->comm, c->stream));
-  // passes: this round's item count is not on the host yet, so the previous
-  // round's sizes it (any K gives the same bytes; K only sets the overlap)
-  int K = c->ce_passes;
-  if (K <= 0) K = (int)std::max<uint64_t>(1, std::min<uint64_t>(8, c->lr[0].n_out >> 21));
-  RAFI_CK(launch_pass_bounds(c, K));
-  RAFI_CK_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl, ctrl_c_bytes(c), cudaMemcpyDeviceToHost, c->stream));
-  RAFI_CK_CUDA(cudaMemcpyAsync(c->bounds_host, c->bounds_dev, sizeof(uint32_t) * (K + 1) * R,
-                               cudaMemcpyDeviceToHost, c->stream));
-  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[3], c->stream));
-  RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
-  c->host_stale = false;
-  uint64_t G = 0;
-  if (book_keep(c, &G)) {  // Z3, decided identically on every rank from the same matrix
-    c->broken = true;
-    set_error("receive overflow: some rank would receive more than its capacity");
-    return RAFI_ERR_RECV_OVERFLOW;
-  }
-  // bases: self run at recv_off_me[me] in the own incoming queue, peer d's run
-  // at send_off[d] in the send batch; each peer's run lands at recv_off_d[me]
-  std::vector<uint64_t> recv_off(R, 0);
-  uint64_t send_off = 0;
-  for (int d = 0; d < R; ++d) {
-    for (int s = 0; s < me; ++s) recv_off[d] += c->Chost[(size_t)s * R + d];
-    c->off_host[d] = d == me ? recv_off[d] : send_off;
-    send_off += c->Chost[(size_t)me * R + d];
-  }
-  c->plan_host[0] = c->lr[0].num_in;
-  RAFI_CK_CUDA(cudaMemcpyAsync(c->off_dev, c->off_host, sizeof(uint64_t) * R, cudaMemcpyHostToDevice, c->stream));
-  RAFI_CK_CUDA(cudaMemcpyAsync(c->plan_dev, c->plan_host, sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
-  const uint64_t n = c->lr[0].n_out;
-  const uint64_t tiles = (n + c->tile - 1) / c->tile;
-  const uint64_t nblk = (tiles + 7) / 8;  // kHistTilesPerCta
-  uint8_t* sb = c->lr[0].binned[0];
-  for (int k = 0; k < K; ++k) {
-    const uint64_t b0 = (uint64_t)k * nblk / K, b1 = (uint64_t)(k + 1) * nblk / K;
-    c->g_lo = std::min(tiles, 8 * b0);
-    c->g_hi = std::min(tiles, 8 * b1);
-    if (c->g_hi > c->g_lo || k == K - 1) {
-      if (c->g_hi <= c->g_lo) { c->g_lo = 0; c->g_hi = 0; }  // empty last pass: wrap-up only
-      int rc = launch_scatter(c, true, k == K - 1);
-      c->g_lo = 0; c->g_hi = ~0ull;
-      RAFI_CK(rc);
-    }
-    RAFI_CK_CUDA(cudaEventRecord(c->ce_pass[k], c->stream));
-    for (int d = 0; d < R; ++d) {
-      if (d == me) continue;
-      const uint64_t lo = c->bounds_host[(size_t)k * R + d], hi = c->bounds_host[(size_t)(k + 1) * R + d];
-      if (hi <= lo) continue;
-      RAFI_CK_CUDA(cudaStreamWaitEvent(c->ce_streams[d], c->ce_pass[k], 0));
-      RAFI_CK_CUDA(cudaMemcpyAsync(c->peer_in[d] + (recv_off[d] + lo) * B, sb + (c->off_host[d] + lo) * B,
-                                   (hi - lo) * B, cudaMemcpyDeviceToDevice, c->ce_streams[d]));
-    }
-  }
-  if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[4], c->stream));
-  for (int d = 0; d < R; ++d) {
-    if (d == me) continue;
-    RAFI_CK_CUDA(cudaEventRecord(c->ce_done[d], c->ce_streams[d]));
-    RAFI_CK_CUDA(cudaStreamWaitEvent(c->stream, c->ce_done[d], 0));
-  }
-  // every rank's copies into every queue have completed once the barrier has
-  if (c->ctl_peer)
-    RAFI_CK(launch_ctl_barrier(c));
-  else
-    RAFI_CK_NCCL(ncclAllReduce(c->ovf_dev + 1, c->ovf_dev + 1, 1, ncclInt32, ncclMax, c->comm, c->stream));
-  if (T) {
-    RAFI_CK_CUDA(cudaEventRecord(c->ev[5], c->stream));
-    RAFI_CK_CUDA(cudaEventRecord(c->ev[6], c->stream));
-    mark_timing(c, true);
-  }
-  c->last_fused = true;  // no readable send batch for the self run (it went straight to the queue)
-  c->round += 1;
-  c->last_G = (int64_t)G;
-  return (int64_t)G;
+static bool capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &st) != cudaSuccess) { cudaGetLastError(); return false; }
+  return st != cudaStreamCaptureStatusNone;
+}
+
+// An asynchronous read of the incoming queue (rafi_read_incoming_async) must
+// land before a forward rewrites the queue: the context stream waits for it
+// in stream order.  While the stream is being captured (a user-level capture
+// that did not go through rafi_capture_begin) an event recorded outside the
+// capture cannot be waited on, so the host waits instead.
+static int wait_pending_reads(Ctx* c) {
+  if (!c->out_pending) return RAFI_OK;
+  if (capturing(c->stream)) RAFI_CK_CUDA(cudaStreamSynchronize(c->io_out));
+  else RAFI_CK_CUDA(cudaStreamWaitEvent(c->stream, c->ev_out_done, 0));
+  c->out_pending = false;
+  return RAFI_OK;
 }
 
 static int64_t forward(Ctx* c) {
   if (c->broken) { set_error("context unusable after an earlier collective error"); return RAFI_ERR_STATE; }
   RAFI_CK_CUDA(cudaSetDevice(c->device));
   collect_timing(c);  // the previous forward's events, before they are re-recorded
-  if (c->out_pending) {  // an asynchronous read of the incoming queue must land before it is rewritten
-    RAFI_CK_CUDA(cudaStreamWaitEvent(c->stream, c->ev_out_done, 0));
-    c->out_pending = false;
-  }
-  if (c->exchange_eff == RAFI_EXCHANGE_CE) return forward_ce(c);
+  RAFI_CK(wait_pending_reads(c));
   return c->exchange_eff == RAFI_EXCHANGE_FUSED ? forward_fused(c) : forward_staged(c);
 }
 
@@ -870,10 +916,12 @@ const char* rafi_status_str(int s) {
   }
 }
 
-int rafi_create_ex(rafi_ctx** out, const rafi_create_params* p) {
+int rafi_create_ex(rafi_ctx** out, const rafi_create_params* p) { return rafi_create_boot(out, p, nullptr); }
+
+int rafi_create_boot(rafi_ctx** out, const rafi_create_params* p, const rafi_bootstrap* boot) {
   if (!out) return RAFI_ERR_INVALID_ARG;
   Ctx* c = nullptr;
-  int rc = create(&c, p);
+  int rc = create(&c, p, boot);
   if (rc != RAFI_OK) return rc;
   // rafi_ctx is never defined: the opaque handle is the Ctx address
   *out = reinterpret_cast<rafi_ctx*>(c);
@@ -902,11 +950,23 @@ int rafi_resize(rafi_ctx* ctx, size_t capacity) {
   if (c->io_out) RAFI_CK_CUDA(cudaStreamSynchronize(c->io_out));  // pending async reads of the old queues
   RAFI_CK_CUDA(cudaMemcpyAsync(c->ctrl_host, c->ctrl, sizeof(CtrlDev) * c->L, cudaMemcpyDeviceToHost, c->stream));
   RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
+  uint64_t mine[2] = {capacity, 1};
   for (int l = 0; l < c->L; ++l)
-    if (c->ctrl_host[l].ctr != 0 || c->ctrl_host[l].invalid != 0) {
-      set_error("rafi_resize: outgoing queue not empty (emits since the last forward)");
+    if (c->ctrl_host[l].ctr != 0 || c->ctrl_host[l].invalid != 0) mine[1] = 0;
+  // collective decision before anything changes: same capacity everywhere,
+  // every outgoing queue empty
+  std::vector<uint64_t> all(2 * (size_t)c->nprocs);
+  RAFI_CK(proc_allgather(c, mine, all.data(), sizeof(mine)));
+  for (int p = 0; p < c->nprocs; ++p) {
+    if (!all[2 * p + 1]) {
+      set_error("rafi_resize: an outgoing queue is not empty (emits since the last forward)");
       return RAFI_ERR_INVALID_ARG;
     }
+    if (all[2 * p] != capacity) {
+      set_error("rafi_resize: processes passed different capacities");
+      return RAFI_ERR_INVALID_ARG;
+    }
+  }
   std::vector<LocalRank> old = c->lr;
   const uint64_t keep_cap = c->cap;
   c->cap = capacity;
@@ -929,12 +989,14 @@ int rafi_resize(rafi_ctx* ctx, size_t capacity) {
   RAFI_CK(launch_wrapup(c));
   RAFI_CK_CUDA(cudaStreamSynchronize(c->stream));
   close_ipc(c);
+  // peers may still hold CUDA-IPC mappings of the old queues: free them only
+  // after every process has closed its own
+  RAFI_CK(proc_barrier(c));
   for (auto& r : old) free_rank(r);
   RAFI_CK(upload_rank_table(c));
   c->cur = 0;
   drop_fwd_graph(c);  // captured with the old buffers and grid sizes
   RAFI_CK(exchange_peer_pointers(c));
-  free_ce(c);  // its table points at the old queues
   RAFI_CK(resolve_exchange(c));
   RAFI_CK(refresh_scatter(c));
   return RAFI_OK;
@@ -1027,6 +1089,10 @@ int rafi_read_incoming_async(rafi_ctx* ctx, int local, void* dst, uint64_t first
   if (first > r.num_in || count > r.num_in - first) return RAFI_ERR_INVALID_ARG;
   if (!count) return RAFI_OK;
   RAFI_CK_CUDA(cudaSetDevice(c->device));
+  if (c->stream && capturing(c->stream)) {
+    set_error("rafi_read_incoming_async is not capturable");
+    return RAFI_ERR_UNSUPPORTED;
+  }
   RAFI_CK(ensure_io(c));
   RAFI_CK_CUDA(cudaEventRecord(c->ev_in_ready, c->stream));  // incoming queue final in stream order
   RAFI_CK_CUDA(cudaStreamWaitEvent(c->io_out, c->ev_in_ready, 0));
@@ -1057,7 +1123,12 @@ int rafi_forward_async(rafi_ctx* ctx, unsigned long long* G_dev) {
     set_error("rafi_forward_async needs the FUSED exchange");
     return RAFI_ERR_UNSUPPORTED;
   }
+  if (c->nprocs > 1 && c->ctl_eff == RAFI_CONTROL_HOST) {
+    set_error("rafi_forward_async needs NCCL or PEER control (HOST control synchronises with the host)");
+    return RAFI_ERR_UNSUPPORTED;
+  }
   RAFI_CK_CUDA(cudaSetDevice(c->device));
+  RAFI_CK(wait_pending_reads(c));
   RAFI_CK(enqueue_fused(c, G_dev, false));
   c->last_fused = true;
   c->host_stale = true;
@@ -1079,6 +1150,7 @@ int rafi_capture_begin(rafi_ctx* ctx) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c || !c->stream) { set_error("capture needs a non-default context stream"); return RAFI_ERR_INVALID_ARG; }
   RAFI_CK_CUDA(cudaSetDevice(c->device));
+  RAFI_CK(wait_pending_reads(c));  // before the capture: ordered ahead of every later replay on this stream
   RAFI_CK_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
   return RAFI_OK;
 }
@@ -1100,6 +1172,7 @@ int rafi_graph_launch(rafi_ctx* ctx, void* exec) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c || !exec) return RAFI_ERR_INVALID_ARG;
   RAFI_CK_CUDA(cudaSetDevice(c->device));
+  RAFI_CK(wait_pending_reads(c));  // a replayed forward must not rewrite a queue still being copied out
   RAFI_CK_CUDA(cudaGraphLaunch((cudaGraphExec_t)exec, c->stream));
   c->host_stale = true;
   return RAFI_OK;
@@ -1201,7 +1274,7 @@ int rafi_set_option(rafi_ctx* ctx, int key, long long v) {
   if (key != RAFI_OPT_TIMING) c->fwd_dirty = true;
   switch (key) {
     case RAFI_OPT_EXCHANGE: {
-      if (v < RAFI_EXCHANGE_AUTO || v > RAFI_EXCHANGE_CE) return RAFI_ERR_INVALID_ARG;
+      if (v < RAFI_EXCHANGE_AUTO || v > RAFI_EXCHANGE_FUSED) return RAFI_ERR_INVALID_ARG;
       const int old = c->exchange;
       c->exchange = (int)v;
       int rc = resolve_exchange(c);
@@ -1220,7 +1293,7 @@ int rafi_set_option(rafi_ctx* ctx, int key, long long v) {
       // only between rounds with an empty outgoing queue; re-sizes H/O
       if (v != 0 && (v < 256 || v > 4096 || (v & (v - 1)) != 0)) return RAFI_ERR_INVALID_ARG;  // 256 * 2^k
       const uint32_t t = v ? (uint32_t)v : auto_tile(c);
-      if (is_perm(c->scatter_eff) && perm_smem_bytes(c->scatter_eff, t, c->B, c->R) > kMaxSmem) {
+      if (c->scatter_eff == RAFI_SCATTER_BULK && perm_smem_bytes(t, c->B, c->R) > kMaxSmem) {
         set_error("tile too large for the permuting scatter's shared memory");
         return RAFI_ERR_UNSUPPORTED;
       }
@@ -1229,7 +1302,7 @@ int rafi_set_option(rafi_ctx* ctx, int key, long long v) {
       return RAFI_OK;
     }
     case RAFI_OPT_SCATTER: {
-      if (v < RAFI_SCATTER_AUTO || v > RAFI_SCATTER_UNITS) return RAFI_ERR_INVALID_ARG;
+      if (v < RAFI_SCATTER_AUTO || v > RAFI_SCATTER_BULK) return RAFI_ERR_INVALID_ARG;
       const int old = c->scatter;
       c->scatter = (int)v;
       int rc = resolve_scatter(c);
@@ -1242,18 +1315,16 @@ int rafi_set_option(rafi_ctx* ctx, int key, long long v) {
       if (v != 0 && v != 1) return RAFI_ERR_INVALID_ARG;
       c->fwd_graph = v != 0;
       return RAFI_OK;
-    case RAFI_OPT_CONTROL:
-      if (v < RAFI_CONTROL_AUTO || v > RAFI_CONTROL_PEER) return RAFI_ERR_INVALID_ARG;
-      if (v == RAFI_CONTROL_PEER && c->nprocs > 1 && !c->peer_ok) {
-        set_error("PEER control needs every rank's mailbox mapped (CUDA IPC failed)");
-        return RAFI_ERR_UNSUPPORTED;
-      }
-      c->control = (int)v;
-      c->ctl_peer = c->nprocs > 1 && c->peer_ok && c->control != RAFI_CONTROL_NCCL;
+    case RAFI_OPT_CONTROL: {
+      if (v < RAFI_CONTROL_AUTO || v > RAFI_CONTROL_HOST) return RAFI_ERR_INVALID_ARG;
+      const int old = c->control;
+      const int rc = resolve_control(c, (int)v);
+      if (rc != RAFI_OK) { resolve_control(c, old); return rc; }
       return RAFI_OK;
-    case RAFI_OPT_CE_PASSES:
-      if (v < 0 || v > Ctx::kMaxPasses) return RAFI_ERR_INVALID_ARG;
-      c->ce_passes = (int)v;
+    }
+    case RAFI_OPT_PEER_TIMEOUT_MS:
+      if (v < 0 || v > 3600000000ll) return RAFI_ERR_INVALID_ARG;
+      c->peer_timeout_ns = (uint64_t)v * 1000000ull;
       return RAFI_OK;
     default: return RAFI_ERR_INVALID_ARG;
   }
@@ -1267,12 +1338,55 @@ int rafi_get_option(const rafi_ctx* ctx, int key, long long* v) {
     case RAFI_OPT_TIMING: *v = c->timing; return RAFI_OK;
     case RAFI_OPT_TILE: *v = c->tile; return RAFI_OK;
     case RAFI_OPT_SCATTER: *v = c->scatter_eff; return RAFI_OK;
-    case RAFI_OPT_CE_PASSES: *v = c->ce_passes; return RAFI_OK;
-    case RAFI_OPT_CONTROL: *v = c->ctl_peer ? RAFI_CONTROL_PEER : RAFI_CONTROL_NCCL; return RAFI_OK;
+    case RAFI_OPT_CONTROL: *v = c->ctl_eff; return RAFI_OK;
+    case RAFI_OPT_PEER_TIMEOUT_MS: *v = (long long)(c->peer_timeout_ns / 1000000ull); return RAFI_OK;
     case RAFI_OPT_FORWARD_GRAPH: *v = c->fwd_graph; return RAFI_OK;
     case RAFI_OPT_SELF_DIRECT: *v = 0; return RAFI_OK;
     default: return RAFI_ERR_INVALID_ARG;
   }
+}
+
+int rafi_selftest_peer_control(int device, int P, int L, int rounds, int absent, long long timeout_ms,
+                               uint64_t* bad, uint64_t* timed_out) {
+  if (P < 1 || P > 128 || L < 1 || P * L > 1024 || rounds < 1 || absent >= P || timeout_ms < 0 ||
+      (absent >= 0 && timeout_ms == 0) || !bad || !timed_out)
+    return RAFI_ERR_INVALID_ARG;
+  if (device >= 0) RAFI_CK_CUDA(cudaSetDevice(device));
+  const int R = P * L;
+  const size_t mw = mbox_words(P, R);
+  std::vector<unsigned long long*> boxes(P, nullptr);
+  unsigned long long** table = nullptr;
+  uint64_t* Cs = nullptr;
+  unsigned long long* flags = nullptr;  // [P] err, [1] bad
+  int rc = RAFI_OK;
+  for (int p = 0; p < P && rc == RAFI_OK; ++p) {
+    rc = alloc_dev((void**)&boxes[p], mw * sizeof(unsigned long long));
+    if (rc == RAFI_OK && cudaMemset(boxes[p], 0, mw * sizeof(unsigned long long)) != cudaSuccess) rc = RAFI_ERR_CUDA;
+  }
+  if (rc == RAFI_OK) rc = alloc_dev((void**)&table, sizeof(void*) * P);
+  if (rc == RAFI_OK) rc = alloc_dev((void**)&Cs, sizeof(uint64_t) * (size_t)P * R * R);
+  if (rc == RAFI_OK) rc = alloc_dev((void**)&flags, sizeof(unsigned long long) * (P + 1));
+  if (rc == RAFI_OK && (cudaMemcpy(table, boxes.data(), sizeof(void*) * P, cudaMemcpyHostToDevice) != cudaSuccess ||
+                        cudaMemset(flags, 0, sizeof(unsigned long long) * (P + 1)) != cudaSuccess))
+    rc = RAFI_ERR_CUDA;
+  if (rc == RAFI_OK)
+    rc = launch_ctl_selftest(table, Cs, P, L, rounds, absent, (unsigned long long)timeout_ms * 1000000ull, flags,
+                             flags + P);
+  if (rc == RAFI_OK && cudaDeviceSynchronize() != cudaSuccess) { set_error("selftest kernel failed"); rc = RAFI_ERR_CUDA; }
+  if (rc == RAFI_OK) {
+    std::vector<unsigned long long> h(P + 1);
+    if (cudaMemcpy(h.data(), flags, sizeof(unsigned long long) * (P + 1), cudaMemcpyDeviceToHost) != cudaSuccess) {
+      rc = RAFI_ERR_CUDA;
+    } else {
+      *bad = h[P];
+      *timed_out = 0;
+      for (int p = 0; p < P; ++p) *timed_out += h[p] != 0;
+    }
+  }
+  if (rc == RAFI_ERR_CUDA) cudaGetLastError();
+  for (auto* b : boxes) cudaFree(b);
+  cudaFree(table); cudaFree(Cs); cudaFree(flags);
+  return rc;
 }
 
 int rafi_nccl_unique_id(void* id128) {

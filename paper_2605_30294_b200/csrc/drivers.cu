@@ -84,10 +84,25 @@ __global__ void k_drv_walk(rafi_device_view v, uint64_t seed, uint32_t rnd, uint
   }
 }
 
+template <int B>
+__global__ void k_drv_emit_items(rafi_device_view v, const uint8_t* __restrict__ items,
+                                 const int32_t* __restrict__ dests, uint64_t n) {
+  rafi::Queue<Item<B>> q(v);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    q.emitOutgoing(rafi::load_item<Item<B>>(items + i * B), dests[i]);
+}
+
 // Threads to launch for an app step over the incoming queue: the host-known
-// count, or the capacity when the count lives only on the device (after
-// rafi_forward_async; the kernels read numIncoming from num_in_dev).
-uint64_t launch_count(const rafi_impl::Ctx* c, const rafi_device_view& v) { return c->host_stale ? c->cap : v.num_in; }
+// count, or the capacity when the count lives only on the device -- after
+// rafi_forward_async / graph replays, and whenever the launch is being
+// captured into a graph (a replay must cover whatever count the device holds
+// then; the kernels read numIncoming from num_in_dev).
+uint64_t launch_count(const rafi_impl::Ctx* c, const rafi_device_view& v) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  if (c->stream && cudaStreamIsCapturing(c->stream, &st) != cudaSuccess) { cudaGetLastError(); st = cudaStreamCaptureStatusNone; }
+  const bool device_count = c->host_stale || st != cudaStreamCaptureStatusNone;
+  return device_count ? (c->cap ? c->cap : 1) : v.num_in;
+}
 
 template <int B>
 int launch_emit(rafi_impl::Ctx* c, const rafi_device_view& v, int pattern, uint64_t seed, uint32_t rnd, uint64_t n,
@@ -281,6 +296,7 @@ int check_grid(rafi_impl::Ctx* c, int gx, int gy, int gz) {
 }
 
 #define RAFI_DRV_SIZES(X) X(16) X(20) X(24) X(32) X(40) X(44) X(48) X(64) X(96) X(128)
+#define RAFI_DRV_ITEM_SIZES(X) X(4) X(8) X(12) RAFI_DRV_SIZES(X)
 
 }  // namespace
 
@@ -301,6 +317,29 @@ extern "C" int rafi_drv_emit_synthetic(rafi_ctx* ctx, int local, int pattern, ui
 #undef CASE
     default: rafi_impl::set_error("rafi_drv_emit_synthetic: unsupported item size"); return RAFI_ERR_UNSUPPORTED;
   }
+}
+
+extern "C" int rafi_drv_emit_items(rafi_ctx* ctx, int local, const void* items, const int32_t* dests, uint64_t n) {
+  auto* c = reinterpret_cast<rafi_impl::Ctx*>(ctx);
+  rafi_device_view v;
+  int rc = rafi_get_device_view(ctx, local, &v);
+  if (rc != RAFI_OK) return rc;
+  if (n == 0) return RAFI_OK;
+  if (!items || !dests || ((uintptr_t)items & 15)) return RAFI_ERR_INVALID_ARG;
+  if (cudaSetDevice(c->device) != cudaSuccess) return RAFI_ERR_CUDA;
+  const uint64_t blocks = (n + 255) / 256;
+  const int grid = (int)(blocks < 148 * 16 ? blocks : 148 * 16);
+  switch (v.item_bytes) {
+#define CASE(B)                                                                                          \
+  case B:                                                                                                \
+    k_drv_emit_items<B><<<grid, 256, 0, c->stream>>>(v, static_cast<const uint8_t*>(items), dests, n); \
+    break;
+    RAFI_DRV_ITEM_SIZES(CASE)
+#undef CASE
+    default: rafi_impl::set_error("rafi_drv_emit_items: unsupported item size"); return RAFI_ERR_UNSUPPORTED;
+  }
+  c->launches += 1;
+  return cudaGetLastError() == cudaSuccess ? RAFI_OK : RAFI_ERR_CUDA;
 }
 
 extern "C" int rafi_drv_random_walk(rafi_ctx* ctx, uint64_t seed, uint32_t rnd, uint32_t last_round) {

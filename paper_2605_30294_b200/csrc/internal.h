@@ -47,7 +47,8 @@ struct alignas(64) CtrlDev {
   unsigned long long n_out;     // min(ctr, cap) seen by the last forward
   unsigned long long dropped;   // ctr - n_out of the last forward
   unsigned long long invalid_last;
-  unsigned long long pad[2];
+  unsigned long long status;    // local rank 0 only: nonzero = a peer-control wait timed out (RAFI_ERR_TIMEOUT)
+  unsigned long long pad;
 };
 
 // Device table of one local rank's buffers (kernel argument array).
@@ -126,8 +127,12 @@ struct Ctx {
   std::vector<uint8_t*> peer_in;      // host copy of in_table
   std::vector<unsigned long long*> peer_mbox;  // [R] every global rank's mailbox (local or IPC-mapped)
   unsigned long long** mbox_table_dev = nullptr;  // [P] mailbox of each process's local rank 0
-  int control = RAFI_CONTROL_AUTO;     // RAFI_OPT_CONTROL
+  int control = RAFI_CONTROL_AUTO;     // RAFI_OPT_CONTROL (requested)
+  int ctl_eff = RAFI_CONTROL_AUTO;     // effective control of a multi-process forward (NCCL / PEER / HOST)
   bool ctl_peer = false;               // count exchange + completion barrier over peer mailboxes
+  rafi_bootstrap boot{};               // host all-gather of the process group (rafi_create_boot), or empty
+  bool shared_gpu = false;             // two processes of the group share one device (no cross-process spin waits)
+  uint64_t peer_timeout_ns = 20000000000ull;  // RAFI_OPT_PEER_TIMEOUT_MS (0 = wait forever)
   bool scatter_barrier = false;        // the next scatter launch ends with the peer completion barrier
   uint64_t* plan_host = nullptr;      // [L] pinned
   // peer pointers to every global rank's binned buffers ([R][2]); local ones
@@ -148,19 +153,6 @@ struct Ctx {
   cudaEvent_t ev_stage_ready[2] = {}, ev_stage_free[2] = {}, ev_in_ready = nullptr, ev_out_done = nullptr;
   bool out_pending = false;
 
-  // scatter tile range [g_lo, g_hi) (flat over local ranks; the CE exchange scatters in passes)
-  uint64_t g_lo = 0, g_hi = ~0ull;
-  // RAFI_EXCHANGE_CE: destination table (own incoming queue for the self run,
-  // the local send batch for every peer), pass bounds, copy streams
-  static constexpr int kMaxPasses = 16;
-  uint8_t** ce_table_dev = nullptr;   // [R]
-  uint32_t* bounds_dev = nullptr;     // [(kMaxPasses+1) * R] items of dest d before pass k's first block
-  uint32_t* bounds_host = nullptr;    // pinned mirror
-  uint64_t* off_host = nullptr;       // [R] pinned: per-destination bases uploaded to off_dev
-  int ce_passes = 0;                  // RAFI_OPT_CE_PASSES (0 = automatic)
-  std::vector<cudaStream_t> ce_streams;  // [R] one copy stream per peer
-  std::vector<cudaEvent_t> ce_done;      // [R]
-  cudaEvent_t ce_pass[kMaxPasses] = {};
   // blocking FUSED forward replayed as one cached CUDA graph (RAFI_OPT_FORWARD_GRAPH)
   bool fwd_graph = true;
   bool fwd_dirty = true;            // options / buffers changed since the graph was captured
@@ -184,9 +176,9 @@ inline size_t ctrl_c_bytes(const Ctx* c) { return sizeof(CtrlDev) * c->L + sizeo
 
 // kernels.cu
 uint32_t choose_tile(uint64_t item_bytes);
-uint32_t choose_tile_perm(int mode, uint64_t item_bytes, int R);
+uint32_t choose_tile_perm(uint64_t item_bytes, int R);
 bool perm_supported(uint64_t item_bytes);
-size_t perm_smem_bytes(int mode, uint32_t tile, uint64_t item_bytes, int R);
+size_t perm_smem_bytes(uint32_t tile, uint64_t item_bytes, int R);
 int launch_emit_bulk(Ctx* c, int local, const uint8_t* items, const int32_t* dests, uint64_t n);
 int launch_hist(Ctx* c);
 int launch_scan(Ctx* c, int plan_mode, unsigned long long* G_out = nullptr, bool ctl = false);
@@ -194,9 +186,8 @@ int launch_scatter(Ctx* c, bool fused, bool wrap);
 int launch_plan(Ctx* c, bool fused, unsigned long long* G_out = nullptr);
 int launch_copy(Ctx* c, int nruns_per_dest);
 int launch_wrapup(Ctx* c);
-int launch_pass_bounds(Ctx* c, int K);
-int launch_ctl_counts(Ctx* c);
-int launch_ctl_barrier(Ctx* c);
+int launch_ctl_selftest(unsigned long long* const* mbox, uint64_t* Cs, int P, int L, int rounds, int absent,
+                        unsigned long long timeout_ns, unsigned long long* err, unsigned long long* bad);
 size_t scatter_smem_bytes(uint32_t tile, uint64_t item_bytes, int R);
 
 }  // namespace rafi_impl

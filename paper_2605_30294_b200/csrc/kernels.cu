@@ -405,6 +405,8 @@ __device__ __forceinline__ bool last_block(unsigned* done) {
 struct PeerCtl {
   unsigned long long* const* mbox;  // [P] mailboxes (local or IPC-mapped), nullptr = off
   int proc, P;
+  unsigned long long timeout_ns;    // give up a wait after this long (0 = never)
+  unsigned long long* err;          // set to 1 when a wait gave up (CtrlDev::status of local rank 0)
 };
 
 __device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
@@ -420,22 +422,26 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// Wait until *flag >= e; a peer that never arrives is a hang: trap after 20 s.
-__device__ void spin_until(const unsigned long long* flag, unsigned long long e) {
+// Wait until *flag >= e.  A peer that never arrives would be a hang: after
+// pc.timeout_ns (0 = never) give up, flag the error for the host and return
+// false -- no trap, so the CUDA context stays usable for cleanup.
+__device__ bool spin_until(const PeerCtl& pc, const unsigned long long* flag, unsigned long long e) {
   const unsigned long long t0 = globaltimer_ns();
   for (uint32_t i = 1; ld_acquire_sys(flag) < e; ++i) {
-    if ((i & 1023) == 0 && globaltimer_ns() - t0 > 20000000000ull) {
-      printf("rafi: peer control flag timed out (epoch %llu)\n", e);
-      __trap();
+    if (pc.timeout_ns && (i & 1023) == 0 && globaltimer_ns() - t0 > pc.timeout_ns) {
+      atomicExch(pc.err, 1ull);
+      return false;
     }
   }
+  return true;
 }
 
 // Count exchange by one whole block: push this process's L count rows
 // (Cdev rows proc*L ..) into every process's mailbox, raise this process's
 // count flag there, wait for every process's flag, then copy the whole R x R
-// matrix into Cdev (where the plan and the host read it).
-__device__ void ctl_counts_block(const PeerCtl& pc, uint64_t* Cdev, int L, int R) {
+// matrix into Cdev (where the plan and the host read it).  Returns false
+// (for every thread) if some wait timed out; Cdev is then incomplete.
+__device__ bool ctl_counts_block(const PeerCtl& pc, uint64_t* Cdev, int L, int R) {
   __shared__ unsigned long long se;
   unsigned long long* mine = pc.mbox[pc.proc];
   const int tid = threadIdx.x, P = pc.P;
@@ -452,17 +458,20 @@ __device__ void ctl_counts_block(const PeerCtl& pc, uint64_t* Cdev, int L, int R
     __threadfence_system();  // the rows before the flags, at every peer
     for (int p = 0; p < P; ++p) st_relaxed_sys(&pc.mbox[p][8 + pc.proc], e);
   }
-  for (int p = tid; p < P; p += blockDim.x) spin_until(&mine[8 + p], e);
-  __syncthreads();
+  bool ok = true;
+  for (int p = tid; p < P; p += blockDim.x) ok = spin_until(pc, &mine[8 + p], e) && ok;
+  if (!__syncthreads_and(ok)) return false;
   asm volatile("fence.acq_rel.sys;" ::: "memory");
   for (size_t x = tid; x < (size_t)R * R; x += blockDim.x)
     Cdev[x] = *reinterpret_cast<volatile unsigned long long*>(&mine[C0 + x]);
   __syncthreads();
+  return true;
 }
 
 // Completion barrier by one whole block: this process's pushes of the round
 // (made visible system-wide before the call) precede its flag in every
-// mailbox; return once every process's flag is up.
+// mailbox; return once every process's flag is up (or a wait timed out,
+// which sets *pc.err).
 __device__ void ctl_barrier_block(const PeerCtl& pc) {
   unsigned long long* mine = pc.mbox[pc.proc];
   const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&mine[0]);
@@ -470,16 +479,46 @@ __device__ void ctl_barrier_block(const PeerCtl& pc) {
     __threadfence_system();
     for (int p = 0; p < pc.P; ++p) st_relaxed_sys(&pc.mbox[p][8 + pc.P + pc.proc], e);
   }
-  for (int p = threadIdx.x; p < pc.P; p += blockDim.x) spin_until(&mine[8 + pc.P + p], e);
+  for (int p = threadIdx.x; p < pc.P; p += blockDim.x) spin_until(pc, &mine[8 + pc.P + p], e);
   __syncthreads();
   asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
 
-__global__ void __launch_bounds__(256) k_ctl_counts(PeerCtl pc, uint64_t* Cdev, int L, int R) {
-  ctl_counts_block(pc, Cdev, L, R);
+// Self-test of the peer-control protocol on ONE device: the P blocks of one
+// cooperative launch (co-resident by construction, so their spins cannot
+// deadlock) each play one process with its own mailbox and its own copy of
+// the count matrix.  Every round, block p writes its L rows, runs the count
+// exchange, checks that the whole matrix arrived (a mismatch bumps *bad),
+// then runs the completion barrier.  Block `absent` (or -1) never shows up:
+// the others must give up after timeout_ns and flag err[p].
+__device__ __forceinline__ uint64_t ctl_tag(int rnd, int row, int d) {
+  return ((uint64_t)rnd << 40) ^ ((uint64_t)row << 20) ^ (uint64_t)d ^ 0x5EEDull;
 }
 
-__global__ void k_ctl_barrier(PeerCtl pc) { ctl_barrier_block(pc); }
+__global__ void __launch_bounds__(256) k_ctl_selftest(unsigned long long* const* mbox, uint64_t* Cs, int P, int L,
+                                                      int rounds, int absent, unsigned long long timeout_ns,
+                                                      unsigned long long* err, unsigned long long* bad) {
+  const int p = blockIdx.x;
+  if (p == absent) return;
+  const int R = P * L;
+  PeerCtl pc;
+  pc.mbox = mbox; pc.proc = p; pc.P = P; pc.timeout_ns = timeout_ns; pc.err = err + p;
+  uint64_t* C = Cs + (size_t)p * R * R;
+  for (int rnd = 1; rnd <= rounds; ++rnd) {
+    for (int x = threadIdx.x; x < R * R; x += blockDim.x) {
+      const int row = x / R, d = x % R;
+      C[x] = row / L == p ? ctl_tag(rnd, row, d) : ~0ull;  // other processes' rows must arrive
+    }
+    __syncthreads();
+    if (!ctl_counts_block(pc, C, L, R)) return;
+    unsigned long long nbad = 0;
+    for (int x = threadIdx.x; x < R * R; x += blockDim.x) nbad += C[x] != ctl_tag(rnd, x / R, x % R);
+    if (nbad) atomicAdd(bad, nbad);
+    __threadfence_system();
+    ctl_barrier_block(pc);
+    if (*reinterpret_cast<volatile unsigned long long*>(pc.err)) return;
+  }
+}
 
 // ---------------------------------------------------------------- a3 scan
 
@@ -563,7 +602,14 @@ k_scan(const RankDev* __restrict__ rk, CtrlDev* __restrict__ ctrl, uint64_t* __r
   // into Cmat); then, plan_mode 1 (staged) / 2 (FUSED), every local rank's
   // plan -- one launch instead of three
   if ((plan_mode || pc.mbox) && last_block(done)) {
-    if (pc.mbox) ctl_counts_block(pc, Cmat, L, R);
+    if (pc.mbox && !ctl_counts_block(pc, Cmat, L, R)) {
+      // a peer never arrived: move nothing this round (the host reports RAFI_ERR_TIMEOUT)
+      if (threadIdx.x == 0) {
+        *ovf = 2;
+        if (G_out) *G_out = ~0ull;
+      }
+      return;
+    }
     if (plan_mode) plan_all(Cmat, grank0, L, R, cap, plan_mode == 2, dst_off, num_in, ovf, G_out);
   }
 }
@@ -665,7 +711,7 @@ __global__ void __launch_bounds__(kThreads, kMinB)
 k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint8_t* const* __restrict__ dst_table,
           const uint64_t* __restrict__ dst_off, const int* __restrict__ ovf, int L, int R, uint64_t cap, uint32_t T,
           int cur, uint32_t B, uint32_t UPI, FastDiv divU, FastDiv divB, ScatterLayout lay, unsigned* __restrict__ wrap_done,
-          CtrlDev* __restrict__ ctrl_w, const uint64_t* __restrict__ wrap_num_in, uint64_t g_lo, uint64_t g_hi,
+          CtrlDev* __restrict__ ctrl_w, const uint64_t* __restrict__ wrap_num_in,
           PeerCtl pc) {
   if (ovf && *ovf) return;  // collective receive overflow: move nothing (Z3)
   extern __shared__ __align__(128) uint8_t smem[];
@@ -680,10 +726,10 @@ k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint
   constexpr uint32_t K = kK;  // items per thread per tile (T = 256 * kK)
 
   auto issue = [&](uint32_t it) {  // thread 0: start loading iteration it's tile into stage it&1
-    const uint64_t g = g_lo + blockIdx.x + (uint64_t)it * gridDim.x;
+    const uint64_t g = blockIdx.x + (uint64_t)it * gridDim.x;
     int l;
     uint64_t t, n, tiles;
-    if (g >= g_hi || !tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) return;
+    if (!tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) return;
     const uint64_t t0 = t * T;
     const uint32_t nt = (uint32_t)umin64(T, n - t0);
     uint8_t* st = smem + (it & 1) * lay.stage_stride;
@@ -703,10 +749,10 @@ k_scatter(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint
   if (tid == 0) { issue(0); issue(1); }
 
   for (uint32_t it = 0;; ++it) {
-    const uint64_t g = g_lo + blockIdx.x + (uint64_t)it * gridDim.x;
+    const uint64_t g = blockIdx.x + (uint64_t)it * gridDim.x;
     int l;
     uint64_t t, n, tiles;
-    if (g >= g_hi || !tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) break;
+    if (!tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) break;
     const uint64_t t0 = t * T;
     const uint32_t nt = (uint32_t)umin64(T, n - t0);
     const uint8_t* st = smem + (it & 1) * lay.stage_stride;
@@ -922,21 +968,18 @@ __host__ __device__ inline BulkLayout bulk_layout(uint32_t T, uint64_t B, int R,
 //     memory.  Run d starts at an offset congruent to its global byte address
 //     modulo 16, so the body of every run is one 16-byte-aligned span on both
 //     sides whatever the item size;
-//   * stores, kTma (RAFI_SCATTER_BULK): one elected thread issues a TMA bulk
-//     store (cp.async.bulk shared -> global) per run body, straight into the
-//     destination queue (the local send batch, the local incoming queue, or a
-//     peer's incoming queue over NVLink under FUSED), double-buffered output
-//     tiles when they fit; threads write the unaligned heads and tails (< 16 B);
-//   * stores, !kTma (RAFI_SCATTER_ALIGNED): all threads write the output tile
-//     as consecutive 16-byte-aligned vector stores (4 in flight per thread),
-//     so a 44-B item costs 2.75 vector stores instead of 11 word stores.
+//   * stores: one elected thread issues a TMA bulk store (cp.async.bulk
+//     shared -> global) per run body, straight into the destination queue (the
+//     local send batch, the local incoming queue, or a peer's incoming queue
+//     over NVLink under FUSED), double-buffered output tiles when they fit;
+//     threads write the unaligned heads and tails (< 16 B).
 // The stage is released to the next TMA load as soon as it is permuted.
-template <typename U, int kK, int kMinB, bool kTma>
+template <typename U, int kK, int kMinB>
 __global__ void __launch_bounds__(kThreads, kMinB)
 k_scatter_perm(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint8_t* const* __restrict__ dst_table,
                const uint64_t* __restrict__ dst_off, const int* __restrict__ ovf, int L, int R, uint64_t cap, uint32_t T,
                int cur, uint32_t B, uint32_t UPI, BulkLayout lay, unsigned* __restrict__ wrap_done,
-               CtrlDev* __restrict__ ctrl_w, const uint64_t* __restrict__ wrap_num_in, uint64_t g_lo, uint64_t g_hi,
+               CtrlDev* __restrict__ ctrl_w, const uint64_t* __restrict__ wrap_num_in,
           PeerCtl pc) {
   if (ovf && *ovf) return;  // collective receive overflow: move nothing (Z3)
   extern __shared__ __align__(128) uint8_t smem[];
@@ -949,10 +992,10 @@ k_scatter_perm(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl,
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
 
   auto issue = [&](uint32_t it) {  // thread 0: start loading iteration it's tile into stage it&1
-    const uint64_t g = g_lo + blockIdx.x + (uint64_t)it * gridDim.x;
+    const uint64_t g = blockIdx.x + (uint64_t)it * gridDim.x;
     int l;
     uint64_t t, n, tiles;
-    if (g >= g_hi || !tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) return;
+    if (!tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) return;
     const uint64_t t0 = t * T;
     const uint32_t nt = (uint32_t)umin64(T, n - t0);
     uint8_t* st = smem + (it & 1) * lay.stage_stride;
@@ -967,10 +1010,10 @@ k_scatter_perm(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl,
   // destination base + (tile prefix O + block prefix H + per-destination
   // base) * B; 0 past the last tile
   auto run_addr = [&](uint32_t it, int d) -> uintptr_t {
-    const uint64_t g = g_lo + blockIdx.x + (uint64_t)it * gridDim.x;
+    const uint64_t g = blockIdx.x + (uint64_t)it * gridDim.x;
     int l;
     uint64_t t, n, tiles;
-    if (g >= g_hi || !tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) return 0;
+    if (!tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) return 0;
     const uint64_t nblk = (tiles + kHistTilesPerCta - 1) / kHistTilesPerCta;
     const uint64_t first = (uint64_t)rk[l].O[(uint64_t)d * tiles + t] +
                            rk[l].H[(uint64_t)d * nblk + t / kHistTilesPerCta] + dst_off[(uint64_t)l * R + d];
@@ -987,10 +1030,10 @@ k_scatter_perm(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl,
   uintptr_t pf_addr = (R <= kThreads && tid < R) ? run_addr(0, tid) : 0;
 
   for (uint32_t it = 0;; ++it) {
-    const uint64_t g = g_lo + blockIdx.x + (uint64_t)it * gridDim.x;
+    const uint64_t g = blockIdx.x + (uint64_t)it * gridDim.x;
     int l;
     uint64_t t, n, tiles;
-    if (g >= g_hi || !tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) break;
+    if (!tile_of(g, ctrl, L, cap, T, &l, &t, &n, &tiles)) break;
     const uint64_t t0 = t * T;
     const uint32_t nt = (uint32_t)umin64(T, n - t0);
     const uint8_t* st = smem + (it & 1) * lay.stage_stride;
@@ -1028,9 +1071,7 @@ k_scatter_perm(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl,
         o += tcnt[d] * B;
       }
       // this output buffer's stores (two tiles ago, or the last tile's with one buffer) have read it
-      if (kTma) {
-        if (lay.nobuf == 2) bulk_wait_read<1>(); else bulk_wait_read<0>();
-      }
+      if (lay.nobuf == 2) bulk_wait_read<1>(); else bulk_wait_read<0>();
     }
     __syncthreads();
     // permutation: item il (slot order) -> position rank in run d of the output
@@ -1062,71 +1103,34 @@ k_scatter_perm(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl,
         }
       }
     }
-    if constexpr (kTma) {
-      fence_proxy_async();  // this thread's generic smem writes -> visible to the bulk stores
-      __syncthreads();
-      if (tid == 0) {
-        issue(it + 2);  // the stage is consumed: refill it
-        for (int d = 0; d < R; ++d) {
-          const uint64_t len = (uint64_t)tcnt[d] * B;
-          const uintptr_t a = dbase[d], e = a + len;
-          const uintptr_t b0 = (a + 15) & ~(uintptr_t)15, b1 = e & ~(uintptr_t)15;
-          if (b1 > b0) bulk_s2g(reinterpret_cast<void*>(b0), ob + ooff[d] + (b0 - a), (uint32_t)(b1 - b0));
-        }
-        bulk_commit();
-      }
-      // heads and tails (< 16 B each, or the whole run when it has no aligned body)
-      for (int d = tid; d < R; d += kThreads) {
+    fence_proxy_async();  // this thread's generic smem writes -> visible to the bulk stores
+    __syncthreads();
+    if (tid == 0) {
+      issue(it + 2);  // the stage is consumed: refill it
+      for (int d = 0; d < R; ++d) {
         const uint64_t len = (uint64_t)tcnt[d] * B;
-        if (!len) continue;
         const uintptr_t a = dbase[d], e = a + len;
-        uintptr_t b0 = (a + 15) & ~(uintptr_t)15, b1 = e & ~(uintptr_t)15;
-        if (b1 <= b0) b0 = b1 = e;  // no body: threads write the whole run
-        const uint8_t* o = ob + ooff[d];
-        for (uintptr_t x = a; x < b0; x += sizeof(U))
-          *reinterpret_cast<U*>(x) = *reinterpret_cast<const U*>(o + (x - a));
-        for (uintptr_t x = b1; x < e; x += sizeof(U))
-          *reinterpret_cast<U*>(x) = *reinterpret_cast<const U*>(o + (x - a));
+        const uintptr_t b0 = (a + 15) & ~(uintptr_t)15, b1 = e & ~(uintptr_t)15;
+        if (b1 > b0) bulk_s2g(reinterpret_cast<void*>(b0), ob + ooff[d] + (b0 - a), (uint32_t)(b1 - b0));
       }
-    } else {
-      __syncthreads();
-      if (tid == 0) {
-        fence_proxy_async();  // order the generic-proxy reads of the stage before the async refill
-        issue(it + 2);
-      }
-      // every thread stores consecutive 16-byte chunks of the output tile; a
-      // chunk inside run d lands at a 16-byte-aligned global address (runs are
-      // placed congruent mod 16), chunks at a run's ends are written in
-      // item-unit pieces; the run a thread is in only moves forward
-      const uint32_t oend = ooff[R - 1] + tcnt[R - 1] * B;
-      int d = 0;
-      uint32_t rs = ooff[0], re = rs + tcnt[0] * B;
-      constexpr uint32_t kStep = kThreads * 16;
-      for (uint32_t c0 = tid * 16; c0 < oend; c0 += 4 * kStep) {
-        uint4 v[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (c0 + q * kStep < oend) v[q] = *reinterpret_cast<const uint4*>(ob + c0 + q * kStep);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t c = c0 + q * kStep;
-          if (c < oend) {
-            while (c >= re) { ++d; rs = ooff[d]; re = rs + tcnt[d] * B; }
-            uint8_t* gp = reinterpret_cast<uint8_t*>(dbase[d]);
-            if (c >= rs && c + 16 <= re) {
-              *reinterpret_cast<uint4*>(gp + (c - rs)) = v[q];
-            } else {
-              const uint32_t x1 = c + 16 < re ? c + 16 : re;
-              for (uint32_t x = c > rs ? c : rs; x < x1; x += sizeof(U))
-                *reinterpret_cast<U*>(gp + (x - rs)) = *reinterpret_cast<const U*>(ob + x);
-            }
-          }
-        }
-      }
+      bulk_commit();
+    }
+    // heads and tails (< 16 B each, or the whole run when it has no aligned body)
+    for (int d = tid; d < R; d += kThreads) {
+      const uint64_t len = (uint64_t)tcnt[d] * B;
+      if (!len) continue;
+      const uintptr_t a = dbase[d], e = a + len;
+      uintptr_t b0 = (a + 15) & ~(uintptr_t)15, b1 = e & ~(uintptr_t)15;
+      if (b1 <= b0) b0 = b1 = e;  // no body: threads write the whole run
+      const uint8_t* o = ob + ooff[d];
+      for (uintptr_t x = a; x < b0; x += sizeof(U))
+        *reinterpret_cast<U*>(x) = *reinterpret_cast<const U*>(o + (x - a));
+      for (uintptr_t x = b1; x < e; x += sizeof(U))
+        *reinterpret_cast<U*>(x) = *reinterpret_cast<const U*>(o + (x - a));
     }
     __syncthreads();  // tcnt / ooff / dbase / the output tile are rewritten by the next tile
   }
-  if (kTma && tid == 0) bulk_wait_all();  // every bulk store has completed its writes
+  if (tid == 0) bulk_wait_all();  // every bulk store has completed its writes
   if (dst_table) __threadfence_system();
   if (wrap_done && last_block(wrap_done)) {
     for (int l2 = threadIdx.x; l2 < L; l2 += blockDim.x) {
@@ -1183,53 +1187,21 @@ k_copy(const CopyRun* __restrict__ runs, const RankDev* __restrict__ rk, int R, 
   }
 }
 
-// ---------------------------------------------------------------- a6 CE exchange: pass bounds
-
-// Items of destination d in blocks 0 .. b_k-1 of (single) local rank 0, for the
-// K+1 pass boundaries b_k = k * nblk / K (blocks of kHistTilesPerCta tiles;
-// b_K = nblk gives the row total).  After k_scan, H holds exactly these
-// exclusive block prefixes.  The host derives the same b_k from the item
-// count, so pass k of the scatter covers tiles [8 b_k, 8 b_{k+1}).
-__global__ void k_pass_bounds(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl,
-                              const uint64_t* __restrict__ Cmat, int grank, int R, uint64_t cap, uint32_t T, int K,
-                              uint32_t* __restrict__ out) {
-  const uint64_t n = n_items(ctrl[0], cap);
-  const uint64_t tiles = (n + T - 1) / T;
-  const uint64_t nblk = (tiles + kHistTilesPerCta - 1) / kHistTilesPerCta;
-  for (int x = threadIdx.x; x < (K + 1) * R; x += blockDim.x) {
-    const int k = x / R, d = x % R;
-    const uint64_t b = (uint64_t)k * nblk / K;
-    out[x] = b >= nblk ? (uint32_t)Cmat[(uint64_t)grank * R + d] : rk[0].H[(uint64_t)d * nblk + b];
-  }
-}
-
-int launch_pass_bounds(Ctx* c, int K) {
-  k_pass_bounds<<<1, 256, 0, c->stream>>>(rank_table(c), c->ctrl, c->Cdev, c->proc, c->R, c->cap, c->tile, K,
-                                          c->bounds_dev);
-  RAFI_CK_CUDA(cudaGetLastError());
-  c->launches += 1; c->fwd_launches += 1;
-  return RAFI_OK;
-}
-
 static PeerCtl peer_ctl(Ctx* c, bool on) {
   PeerCtl pc;
   pc.mbox = on ? c->mbox_table_dev : nullptr;
   pc.proc = c->proc;
   pc.P = c->nprocs;
+  pc.timeout_ns = c->peer_timeout_ns;
+  pc.err = &c->ctrl[0].status;
   return pc;
 }
 
-int launch_ctl_counts(Ctx* c) {
-  k_ctl_counts<<<1, 256, 0, c->stream>>>(peer_ctl(c, true), c->Cdev, c->L, c->R);
-  RAFI_CK_CUDA(cudaGetLastError());
-  c->launches += 1; c->fwd_launches += 1;
-  return RAFI_OK;
-}
-
-int launch_ctl_barrier(Ctx* c) {
-  k_ctl_barrier<<<1, 32, 0, c->stream>>>(peer_ctl(c, true));
-  RAFI_CK_CUDA(cudaGetLastError());
-  c->launches += 1; c->fwd_launches += 1;
+int launch_ctl_selftest(unsigned long long* const* mbox, uint64_t* Cs, int P, int L, int rounds, int absent,
+                        unsigned long long timeout_ns, unsigned long long* err, unsigned long long* bad) {
+  void* args[] = {(void*)&mbox, (void*)&Cs, (void*)&P, (void*)&L, (void*)&rounds, (void*)&absent, (void*)&timeout_ns,
+                  (void*)&err, (void*)&bad};
+  RAFI_CK_CUDA(cudaLaunchCooperativeKernel((const void*)k_ctl_selftest, dim3(P), dim3(256), args, 0, nullptr));
   return RAFI_OK;
 }
 
@@ -1316,7 +1288,7 @@ int launch_emit_bulk(Ctx* c, int local, const uint8_t* items, const int32_t* des
 }
 
 static int persistent_grid(Ctx* c, int per_sm) {
-  const uint64_t max_tiles_all = std::min<uint64_t>(c->max_tiles * (uint64_t)c->L, c->g_hi - c->g_lo);
+  const uint64_t max_tiles_all = c->max_tiles * (uint64_t)c->L;
   return (int)std::max<uint64_t>(1, std::min<uint64_t>(max_tiles_all, (uint64_t)num_sms(c->device) * per_sm));
 }
 
@@ -1359,12 +1331,11 @@ static int launch_scatter_kk(Ctx* c, bool fused, bool wrap, uint32_t UPI, int gr
     RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
     granted = (int)lay.total;
   }
-  uint8_t* const* table = fused ? (c->exchange_eff == RAFI_EXCHANGE_CE ? c->ce_table_dev : c->in_table_dev) : nullptr;
-  const int* ovf = fused && c->exchange_eff != RAFI_EXCHANGE_CE ? c->ovf_dev : nullptr;
-  k<<<grid, kThreads, lay.total, c->stream>>>(rank_table(c), c->ctrl, table, c->off_dev, ovf, c->L, c->R, c->cap,
+  k<<<grid, kThreads, lay.total, c->stream>>>(rank_table(c), c->ctrl, fused ? c->in_table_dev : nullptr, c->off_dev,
+                                             fused ? c->ovf_dev : nullptr, c->L, c->R, c->cap,
                                              c->tile, c->cur, (uint32_t)c->B, UPI, FastDiv(UPI),
                                              FastDiv((uint32_t)c->B), lay, wrap ? c->done_dev + 1 : nullptr, c->ctrl,
-                                             c->plan_dev, c->g_lo, c->g_hi, peer_ctl(c, c->scatter_barrier));
+                                             c->plan_dev, peer_ctl(c, c->scatter_barrier));
   RAFI_CK_CUDA(cudaGetLastError());
   return RAFI_OK;
 }
@@ -1372,13 +1343,12 @@ static int launch_scatter_kk(Ctx* c, bool fused, bool wrap, uint32_t UPI, int gr
 // 16-byte chunk gathering (kChunk) for 4-byte units (B % 8 == 4, B >= 16):
 // 44 B goes from 4.43 to 5.41 TB/s.  8-byte units (24, 40 B) stay on unit
 // stores, which measured faster there (profiles/r01_suite_n1_cfg5_chunk.md).
-// RAFI_SCATTER_UNITS keeps unit stores everywhere (comparison).
 template <typename U, int kK, int kMinB>
 static int launch_scatter_k(Ctx* c, bool fused, bool wrap, uint32_t UPI, int grid) {
   const bool si = stage_items(c->tile, c->B);
   const ScatterLayout lay = scatter_layout(c->tile, c->B, c->R, si);
   constexpr bool kCanChunk = sizeof(U) == 4;
-  const bool chunk = kCanChunk && c->B >= 16 && c->B % 16 != 0 && c->scatter_eff != RAFI_SCATTER_UNITS;
+  const bool chunk = kCanChunk && c->B >= 16 && c->B % 16 != 0;
   if (chunk)
     return si ? launch_scatter_kk<U, true, kK, kMinB, kCanChunk>(c, fused, wrap, UPI, grid, lay)
               : launch_scatter_kk<U, false, kK, kMinB, kCanChunk>(c, fused, wrap, UPI, grid, lay);
@@ -1404,86 +1374,77 @@ static int launch_scatter_t(Ctx* c, bool fused, bool wrap, uint32_t UPI, int gri
                                  : launch_scatter_m<U, 2>(c, fused, wrap, UPI, grid);
 }
 
-// ---- permuting scatter (RAFI_SCATTER_BULK: TMA bulk stores; RAFI_SCATTER_ALIGNED: 16-B thread stores)
+// ---- permuting scatter (RAFI_SCATTER_BULK: TMA bulk stores)
 
 bool perm_supported(uint64_t B) { return B % 4 == 0; }
 
-// Output tiles: BULK keeps two (the store of tile i overlaps tile i+1) when
-// that still leaves room for two CTAs per SM; ALIGNED stores synchronously
-// and needs one.
-static uint32_t perm_nobuf(int mode, uint32_t T, uint64_t B, int R) {
-  if (mode != RAFI_SCATTER_BULK) return 1u;
+// Output tiles: two (the store of tile i overlaps tile i+1) when that still
+// leaves room for two CTAs per SM, else one.
+static uint32_t perm_nobuf(uint32_t T, uint64_t B, int R) {
   return bulk_layout(T, B, R, 2).total <= 112u * 1024u ? 2u : 1u;
 }
 
-size_t perm_smem_bytes(int mode, uint32_t T, uint64_t B, int R) {
-  return bulk_layout(T, B, R, perm_nobuf(mode, T, B, R)).total;
-}
+size_t perm_smem_bytes(uint32_t T, uint64_t B, int R) { return bulk_layout(T, B, R, perm_nobuf(T, B, R)).total; }
 
-// Largest tile (256 * 2^k) whose layout fits four CTAs per SM, else two, else
-// one.  BULK starts at two: its NVLink pushes gain 2-9% from 512-item tiles
-// over 256-item ones at N=2 and N=4 (profiles/r01_bulk_tiles_multigpu.md).
-uint32_t choose_tile_perm(int mode, uint64_t B, int R) {
-  for (uint32_t budget : {56u * 1024u, 112u * 1024u, 227u * 1024u}) {
-    if (mode == RAFI_SCATTER_BULK && budget < 112u * 1024u) continue;
+// Largest tile (256 * 2^k) whose layout fits two CTAs per SM, else one.  Its
+// NVLink pushes gain 2-9% from 512-item tiles over 256-item ones at N=2 and
+// N=4 (profiles/r01_bulk_tiles_multigpu.md).
+uint32_t choose_tile_perm(uint64_t B, int R) {
+  for (uint32_t budget : {112u * 1024u, 227u * 1024u}) {
     uint32_t best = 0;
     for (uint32_t T = kThreads; T <= kThreads * kMaxK; T *= 2)
-      if (perm_smem_bytes(mode, T, B, R) <= budget) best = T;
+      if (perm_smem_bytes(T, B, R) <= budget) best = T;
     if (best) return best;
   }
   return kThreads;
 }
 
-template <typename U, int kK, int kMinB, bool kTma>
+template <typename U, int kK, int kMinB>
 static int launch_perm_k(Ctx* c, bool fused, bool wrap, uint32_t UPI, int grid) {
-  const BulkLayout lay = bulk_layout(c->tile, c->B, c->R, perm_nobuf(c->scatter_eff, c->tile, c->B, c->R));
+  const BulkLayout lay = bulk_layout(c->tile, c->B, c->R, perm_nobuf(c->tile, c->B, c->R));
   static int granted = 0;  // per instantiation: the largest smem opt-in already granted
-  auto k = k_scatter_perm<U, kK, kMinB, kTma>;
+  auto k = k_scatter_perm<U, kK, kMinB>;
   if ((int)lay.total > granted) {
     RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
     granted = (int)lay.total;
   }
-  const bool ce = c->exchange_eff == RAFI_EXCHANGE_CE;
-  k<<<grid, kThreads, lay.total, c->stream>>>(rank_table(c), c->ctrl,
-                                             fused ? (ce ? c->ce_table_dev : c->in_table_dev) : nullptr, c->off_dev,
-                                             fused && !ce ? c->ovf_dev : nullptr, c->L, c->R, c->cap, c->tile, c->cur,
+  k<<<grid, kThreads, lay.total, c->stream>>>(rank_table(c), c->ctrl, fused ? c->in_table_dev : nullptr, c->off_dev,
+                                             fused ? c->ovf_dev : nullptr, c->L, c->R, c->cap, c->tile, c->cur,
                                              (uint32_t)c->B, UPI, lay, wrap ? c->done_dev + 1 : nullptr, c->ctrl,
-                                             c->plan_dev, c->g_lo, c->g_hi, peer_ctl(c, c->scatter_barrier));
+                                             c->plan_dev, peer_ctl(c, c->scatter_barrier));
   RAFI_CK_CUDA(cudaGetLastError());
   return RAFI_OK;
 }
 
-template <typename U, int kMinB, bool kTma>
+template <typename U, int kMinB>
 static int launch_perm_m(Ctx* c, bool fused, bool wrap, uint32_t UPI, int grid) {
   switch (c->tile / kThreads) {
-    case 1: return launch_perm_k<U, 1, kMinB, kTma>(c, fused, wrap, UPI, grid);
-    case 2: return launch_perm_k<U, 2, kMinB, kTma>(c, fused, wrap, UPI, grid);
-    case 4: return launch_perm_k<U, 4, kMinB, kTma>(c, fused, wrap, UPI, grid);
-    case 8: return launch_perm_k<U, 8, kMinB, kTma>(c, fused, wrap, UPI, grid);
-    case 16: return launch_perm_k<U, 16, kMinB, kTma>(c, fused, wrap, UPI, grid);
+    case 1: return launch_perm_k<U, 1, kMinB>(c, fused, wrap, UPI, grid);
+    case 2: return launch_perm_k<U, 2, kMinB>(c, fused, wrap, UPI, grid);
+    case 4: return launch_perm_k<U, 4, kMinB>(c, fused, wrap, UPI, grid);
+    case 8: return launch_perm_k<U, 8, kMinB>(c, fused, wrap, UPI, grid);
+    case 16: return launch_perm_k<U, 16, kMinB>(c, fused, wrap, UPI, grid);
     default: set_error("tile must be 256 * 2^k"); return RAFI_ERR_INVALID_ARG;
   }
 }
 
-template <typename U, bool kTma>
+template <typename U>
 static int launch_perm_t(Ctx* c, bool fused, bool wrap, uint32_t UPI, int grid, int per_sm) {
-  return per_sm >= 4 ? launch_perm_m<U, 4, kTma>(c, fused, wrap, UPI, grid)
-                     : launch_perm_m<U, 2, kTma>(c, fused, wrap, UPI, grid);
+  return per_sm >= 4 ? launch_perm_m<U, 4>(c, fused, wrap, UPI, grid) : launch_perm_m<U, 2>(c, fused, wrap, UPI, grid);
 }
 
-template <bool kTma>
 static int launch_scatter_perm(Ctx* c, bool fused, bool wrap) {
   const uint32_t unit = unit_for(c->B, 0);
   const uint32_t UPI = (uint32_t)(c->B / unit);
-  const size_t smem = perm_smem_bytes(c->scatter_eff, c->tile, c->B, c->R);
+  const size_t smem = perm_smem_bytes(c->tile, c->B, c->R);
   const int fit = (int)((228u * 1024u) / (smem + 1024u));
   const int per_sm = std::max(1, std::min(4, fit));
   const int grid = persistent_grid(c, per_sm);
   int rc;
   switch (unit) {
-    case 16: rc = launch_perm_t<uint4, kTma>(c, fused, wrap, UPI, grid, per_sm); break;
-    case 8: rc = launch_perm_t<uint2, kTma>(c, fused, wrap, UPI, grid, per_sm); break;
-    case 4: rc = launch_perm_t<uint32_t, kTma>(c, fused, wrap, UPI, grid, per_sm); break;
+    case 16: rc = launch_perm_t<uint4>(c, fused, wrap, UPI, grid, per_sm); break;
+    case 8: rc = launch_perm_t<uint2>(c, fused, wrap, UPI, grid, per_sm); break;
+    case 4: rc = launch_perm_t<uint32_t>(c, fused, wrap, UPI, grid, per_sm); break;
     default: set_error("permuting scatter needs item_bytes % 4 == 0"); return RAFI_ERR_UNSUPPORTED;
   }
   if (rc == RAFI_OK) { c->launches += 1; c->fwd_launches += 1; }
@@ -1491,8 +1452,7 @@ static int launch_scatter_perm(Ctx* c, bool fused, bool wrap) {
 }
 
 int launch_scatter(Ctx* c, bool fused, bool wrap) {
-  if (c->scatter_eff == RAFI_SCATTER_BULK) return launch_scatter_perm<true>(c, fused, wrap);
-  if (c->scatter_eff == RAFI_SCATTER_ALIGNED) return launch_scatter_perm<false>(c, fused, wrap);
+  if (c->scatter_eff == RAFI_SCATTER_BULK) return launch_scatter_perm(c, fused, wrap);
   const uint32_t unit = unit_for(c->B, 0);
   const uint32_t UPI = (uint32_t)(c->B / unit);
   const size_t smem = scatter_smem_bytes(c->tile, c->B, c->R);

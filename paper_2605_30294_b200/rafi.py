@@ -24,18 +24,20 @@ ERR_NOMEM = -4
 ERR_RECV_OVERFLOW = -5
 ERR_STATE = -6
 ERR_UNSUPPORTED = -7
+ERR_TIMEOUT = -8
+ERR_BOOTSTRAP = -9
 
 OPT_EXCHANGE = 1
 OPT_TIMING = 2
 OPT_TILE = 3
 OPT_SELF_DIRECT = 4
 OPT_SCATTER = 5
-OPT_CE_PASSES = 6
 OPT_CONTROL = 7
 OPT_FORWARD_GRAPH = 8
-CONTROL_AUTO, CONTROL_NCCL, CONTROL_PEER = 0, 1, 2
-SCATTER_AUTO, SCATTER_THREADS, SCATTER_BULK, SCATTER_ALIGNED, SCATTER_UNITS = 0, 1, 2, 3, 4
-EXCHANGE_AUTO, EXCHANGE_NCCL, EXCHANGE_PEER, EXCHANGE_FUSED, EXCHANGE_CE = 0, 1, 2, 3, 4
+OPT_PEER_TIMEOUT_MS = 9
+CONTROL_AUTO, CONTROL_NCCL, CONTROL_PEER, CONTROL_HOST = 0, 1, 2, 3
+SCATTER_AUTO, SCATTER_THREADS, SCATTER_BULK = 0, 1, 2
+EXCHANGE_AUTO, EXCHANGE_NCCL, EXCHANGE_PEER, EXCHANGE_FUSED = 0, 1, 2, 3
 
 
 class DeviceView(C.Structure):
@@ -52,6 +54,38 @@ class CreateParams(C.Structure):
         ("item_bytes", C.c_size_t), ("capacity", C.c_size_t), ("nccl_comm", C.c_void_p),
         ("stream", C.c_void_p), ("local_ranks", C.c_int), ("device", C.c_int),
     ]
+
+
+# int (*rafi_allgather_fn)(void* user, const void* send, void* recv, size_t bytes)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
+
+
+class Bootstrap(C.Structure):
+    _fields_ = [("nprocs", C.c_int), ("proc", C.c_int), ("allgather", ALLGATHER_FN), ("user", C.c_void_p)]
+
+
+def torch_allgather(group=None):
+    """A rafi_allgather_fn over a torch.distributed CPU (gloo) group: plumbing
+    for rafi_create_boot (the host transport the paper uses MPI for)."""
+    import torch
+    import torch.distributed as dist
+
+    def fn(user, send, recv, nbytes):
+        try:
+            world = dist.get_world_size(group)
+            src = torch.zeros(max(nbytes, 1), dtype=torch.uint8)
+            if nbytes:
+                C.memmove(src.data_ptr(), send, nbytes)
+            outs = [torch.empty_like(src) for _ in range(world)]
+            dist.all_gather(outs, src, group=group)
+            for p, o in enumerate(outs):
+                if nbytes:
+                    C.memmove(recv + p * nbytes, o.data_ptr(), nbytes)
+            return 0
+        except Exception:  # noqa: BLE001  (reported to the library as a failed collective)
+            return 1
+
+    return fn
 
 
 class Stats(C.Structure):
@@ -77,6 +111,10 @@ class Stats(C.Structure):
 SIGNATURES = {
     "rafi_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_size_t, C.c_size_t, C.c_void_p, C.c_void_p]),
     "rafi_create_ex": (C.c_int, [C.POINTER(C.c_void_p), C.POINTER(CreateParams)]),
+    "rafi_create_boot": (C.c_int, [C.POINTER(C.c_void_p), C.POINTER(CreateParams), C.POINTER(Bootstrap)]),
+    "rafi_selftest_peer_control": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_longlong,
+                                             C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "rafi_drv_emit_items": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_uint64]),
     "rafi_resize": (C.c_int, [C.c_void_p, C.c_size_t]),
     "rafi_destroy": (None, [C.c_void_p]),
     "rafi_get_device_view": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(DeviceView)]),
@@ -209,6 +247,14 @@ def nccl_comm_destroy(comm: int):
     _check(lib().rafi_nccl_comm_destroy(comm), "rafi_nccl_comm_destroy")
 
 
+def selftest_peer_control(P: int, L: int, rounds: int, absent: int = -1, timeout_ms: int = 0, device: int = -1):
+    """rafi_selftest_peer_control: returns (bad matrix entries, processes that timed out)."""
+    bad, tout = C.c_uint64(), C.c_uint64()
+    _check(lib().rafi_selftest_peer_control(device, P, L, rounds, absent, timeout_ms, C.byref(bad), C.byref(tout)),
+           "rafi_selftest_peer_control")
+    return bad.value, tout.value
+
+
 def plan(C_matrix: np.ndarray, capacity: int, d: int):
     """Host-side plan for destination d from the R x R count matrix (rafi_plan)."""
     Cm = np.ascontiguousarray(C_matrix, dtype=np.uint64)
@@ -263,10 +309,19 @@ class Context:
     """One RaFI host context (HostContext<T>)."""
 
     def __init__(self, item_bytes: int, capacity: int, comm: int | None = None, stream=None,
-                 local_ranks: int = 1, device: int = -1):
+                 local_ranks: int = 1, device: int = -1, bootstrap=None):
+        """bootstrap: (nprocs, proc, allgather) for rafi_create_boot, where
+        allgather is a Python callable (user, send, recv, nbytes) -> int such as
+        torch_allgather(); None = rafi_create_ex (NCCL communicator only)."""
         p = CreateParams(item_bytes, capacity, comm, _stream_ptr(stream), local_ranks, device)
         h = C.c_void_p()
-        _check(lib().rafi_create_ex(C.byref(h), C.byref(p)), "rafi_create_ex")
+        if bootstrap is None:
+            _check(lib().rafi_create_ex(C.byref(h), C.byref(p)), "rafi_create_ex")
+        else:
+            nprocs, proc, fn = bootstrap
+            self._allgather = ALLGATHER_FN(fn)  # kept alive as long as the context
+            b = Bootstrap(nprocs, proc, self._allgather, None)
+            _check(lib().rafi_create_boot(C.byref(h), C.byref(p), C.byref(b)), "rafi_create_boot")
         self._h = h.value
         self.item_bytes = int(item_bytes)
         self.local_ranks = int(local_ranks)
@@ -383,6 +438,12 @@ class Context:
                            invalid_threshold: int = 0, local: int = 0):
         _check(lib().rafi_drv_emit_synthetic(self._h, local, pattern, seed, rnd, n, seq0, target, invalid_threshold),
                "rafi_drv_emit_synthetic")
+
+    def drv_emit_items(self, items, dests, n: int | None = None, local: int = 0):
+        """Device re-emit of a resident batch through rafi::Queue<T>::emitOutgoing."""
+        if n is None:
+            n = len(dests)
+        _check(lib().rafi_drv_emit_items(self._h, local, _ptr(items), _ptr(dests), int(n)), "rafi_drv_emit_items")
 
     def drv_random_walk(self, seed: int, rnd: int, last_round: int):
         _check(lib().rafi_drv_random_walk(self._h, seed, rnd, last_round), "rafi_drv_random_walk")

@@ -51,7 +51,7 @@ def test_library_is_sm100a_and_links_one_nccl(L):
 
 
 def test_status_strings_and_version(L):
-    assert L.rafi_abi_version() == 1
+    assert L.rafi_abi_version() == 2
     assert L.rafi_status_str(0) == b"RAFI_OK"
     assert L.rafi_status_str(rafi.ERR_RECV_OVERFLOW) == b"RAFI_ERR_RECV_OVERFLOW"
 

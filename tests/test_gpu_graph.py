@@ -95,3 +95,79 @@ def test_graph_captured_advection_rounds(R, n):
             assert rounds > 10
         finally:
             rafi.Context.graph_destroy(ex)
+
+
+@pytest.mark.parametrize("path", ["forward_async", "graph"])
+def test_async_read_not_torn_by_a_later_forward(path):
+    """rafi_read_incoming_async copies the incoming queue out on the copy-out
+    stream; a forward enqueued right after it (rafi_forward_async, or a graph
+    replay of one) rewrites that queue.  The library makes the context stream
+    wait for the read first, so the host copy holds exactly the old round."""
+    L, n, B, seed = 2, 4 * 1024 * 1024, 48, 91
+    s = torch.cuda.Stream()
+    G_dev = torch.zeros(1, dtype=torch.int64, device="cuda")
+    with rafi.Context(B, 2 * n, local_ranks=L, stream=s) as ctx:
+        for l in range(L):
+            ctx.drv_emit_synthetic(synth.PATTERNS["uniform"], seed, 0, n, local=l)
+        assert ctx.forward() == L * n
+        expect = [ctx.read_incoming(l) for l in range(L)]
+        pins = [torch.empty((len(e), B), dtype=torch.uint8).pin_memory() for e in expect]
+        ex = None
+        if path == "graph":
+            ctx.capture_begin()
+            ctx.drv_random_walk(seed, 1, 5)
+            ctx.forward_async(G_dev)
+            ex = ctx.capture_end()
+        for l in range(L):
+            ctx.read_incoming_async(pins[l], local=l)
+        if path == "graph":
+            ctx.graph_launch(ex)
+        else:
+            ctx.drv_random_walk(seed, 1, 5)
+            ctx.forward_async(G_dev)
+        s.synchronize()
+        ctx.read_wait()
+        assert int(G_dev.item()) == L * n
+        for l in range(L):
+            assert np.array_equal(pins[l].numpy(), expect[l]), l
+        ctx.sync_host()
+        assert sum(ctx.num_incoming(l) for l in range(L)) == L * n
+        if ex is not None:
+            rafi.Context.graph_destroy(ex)
+
+
+def test_capture_after_blocking_forward_covers_empty_rank():
+    """A graph captured right after a blocking forward that left a local rank
+    with no items must still contain that rank's app-step kernel (sized from
+    the capacity, reading numIncoming on the device): later replays bring it
+    items, and none may be dropped."""
+    L, n, B, seed = 2, 3000, 32, 17
+    s = torch.cuda.Stream()
+    G_dev = torch.zeros(1, dtype=torch.int64, device="cuda")
+    w = oracle.World(L, 2 * n * L, B)
+    with rafi.Context(B, 2 * n * L, local_ranks=L, stream=s) as ctx:
+        for l in range(L):  # everything to rank 0: rank 1 starts empty
+            ctx.drv_emit_synthetic(synth.PATTERNS["all_to_one"], seed, 0, n, local=l, target=0)
+            w.emit_many(l, synth.make_items(l, 0, n, B), synth.make_dests("all_to_one", seed, l, 0, n, L, target=0))
+        assert ctx.forward() == w.forward() == L * n
+        assert ctx.num_incoming(1) == 0
+        ctx.capture_begin()
+        ctx.drv_random_walk(seed, 1, 10 ** 6)
+        ctx.forward_async(G_dev)
+        ex = ctx.capture_end()
+        try:
+            for rnd in range(4):
+                ctx.graph_launch(ex)
+                for l in range(L):
+                    inc = w.incoming(l).copy()
+                    inc[:, 4:8] = np.frombuffer(np.uint32(1).tobytes(), np.uint8)
+                    w.emit_many(l, inc, synth.walk_dests(seed, 1, synth.item_id_of(inc), L))
+                G_o = w.forward()
+                s.synchronize()
+                assert int(G_dev.item()) == G_o == L * n, (rnd, int(G_dev.item()), G_o)
+            ctx.sync_host()
+            assert ctx.num_incoming(1) > 0
+            for l in range(L):
+                assert np.array_equal(canonical(ctx.read_incoming(l)), canonical(w.incoming(l)))
+        finally:
+            rafi.Context.graph_destroy(ex)

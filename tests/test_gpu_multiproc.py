@@ -33,7 +33,10 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, B, n, pattern, exchange, rounds, scatter=1, passes=0, control=0):
+def _worker(rank, world, port, B, n, pattern, exchange, rounds, scatter=1, control=0, comm_mode="nccl"):
+    """comm_mode: "nccl" (rafi_create_ex with an NCCL communicator), "both"
+    (NCCL communicator + gloo bootstrap) or "boot" (gloo bootstrap only, no
+    NCCL in the library)."""
     import torch.distributed as dist
 
     import oracle
@@ -44,16 +47,18 @@ def _worker(rank, world, port, B, n, pattern, exchange, rounds, scatter=1, passe
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(rank)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    obj = [rafi.nccl_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(obj, src=0)
-    comm = rafi.nccl_comm_init(world, rank, obj[0], rank)
+    comm = None
+    if comm_mode in ("nccl", "both"):
+        obj = [rafi.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = rafi.nccl_comm_init(world, rank, obj[0], rank)
+    boot = (world, rank, rafi.torch_allgather()) if comm_mode in ("both", "boot") else None
     cap = n * world
-    ctx = rafi.Context(B, cap, comm=comm, stream=torch.cuda.current_stream())
+    ctx = rafi.Context(B, cap, comm=comm, stream=torch.cuda.current_stream(), bootstrap=boot)
     ctx.set_option(rafi.OPT_EXCHANGE, exchange)
     assert ctx.get_option(rafi.OPT_EXCHANGE) == (exchange or rafi.EXCHANGE_FUSED)
     ctx.set_option(rafi.OPT_SCATTER, scatter)
     assert ctx.get_option(rafi.OPT_SCATTER) == (scatter or rafi.SCATTER_BULK)
-    ctx.set_option(rafi.OPT_CE_PASSES, passes)
     ctx.set_option(rafi.OPT_CONTROL, control)
     if control:
         assert ctx.get_option(rafi.OPT_CONTROL) == control
@@ -81,13 +86,14 @@ def _worker(rank, world, port, B, n, pattern, exchange, rounds, scatter=1, passe
     # termination: nothing emitted anywhere -> 0 on every rank
     assert ctx.forward() == 0
     ctx.close()
-    rafi.nccl_comm_destroy(comm)
+    if comm:
+        rafi.nccl_comm_destroy(comm)
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("scatter", [1, 2, 3])  # THREADS, BULK (TMA bulk stores, to NVLink peers), ALIGNED
+@pytest.mark.parametrize("scatter", [1, 2])  # THREADS, BULK (TMA bulk stores, to NVLink peers)
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("exchange", [1, 2, 3, 4])  # NCCL, PEER, FUSED, CE
+@pytest.mark.parametrize("exchange", [1, 2, 3])  # NCCL, PEER, FUSED
 @pytest.mark.parametrize("B,pattern", [(48, "uniform"), (44, "skewed"), (16, "all_to_one")])
 def test_multigpu_snapshot_parity(world, exchange, B, pattern, scatter):
     _need(world)
@@ -96,26 +102,15 @@ def test_multigpu_snapshot_parity(world, exchange, B, pattern, scatter):
 
 
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("passes", [1, 3, 16])
-@pytest.mark.parametrize("B,n", [(48, 30011), (44, 3000), (16, 200000)])
-def test_multigpu_ce_passes(world, passes, B, n):
-    """CE exchange: any number of scatter passes (more than there are blocks
-    included) gives the bit-exact result; copies of every pass land at the
-    right offsets of the peers' queues."""
-    _need(world)
-    import torch.multiprocessing as mp
-    mp.spawn(_worker, args=(world, _free_port(), B, n, "uniform", 4, 3, 1, passes), nprocs=world, join=True)
-
-
-@pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("control", [1, 2])  # NCCL collectives, PEER mailboxes over NVLink
-@pytest.mark.parametrize("exchange", [3, 4])  # FUSED, CE
+@pytest.mark.parametrize("control", [1, 2, 3])  # NCCL collectives, PEER mailboxes over NVLink, HOST
+@pytest.mark.parametrize("exchange", [3])  # FUSED
 def test_multigpu_control_modes(world, control, exchange):
     """Count exchange + completion barrier through NCCL or through the peer
     mailboxes: same bytes, same G, several rounds (epochs) in a row."""
     _need(world)
     import torch.multiprocessing as mp
-    mp.spawn(_worker, args=(world, _free_port(), 48, 20011, "skewed", exchange, 5, 1, 0, control), nprocs=world,
+    mp.spawn(_worker, args=(world, _free_port(), 48, 20011, "skewed", exchange, 5, 1, control,
+                                  "both" if control == 3 else "nccl"), nprocs=world,
              join=True)
 
 
@@ -125,7 +120,19 @@ def test_multigpu_large_default_path(world):
     control) at 2M x 48-B items per rank, two rounds: P1 bit-exact."""
     _need(world)
     import torch.multiprocessing as mp
-    mp.spawn(_worker, args=(world, _free_port(), 48, 2 * 1024 * 1024, "uniform", 0, 2, 0, 0, 0), nprocs=world,
+    mp.spawn(_worker, args=(world, _free_port(), 48, 2 * 1024 * 1024, "uniform", 0, 2, 0, 0), nprocs=world,
+             join=True)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("exchange", [2, 3])  # PEER (staged pull), FUSED
+def test_multigpu_bootstrap_without_nccl(world, exchange):
+    """rafi_create_boot with a gloo bootstrap and no NCCL communicator: CUDA-IPC
+    handles travel through the host all-gather; AUTO control is PEER (mailboxes
+    over NVLink) for FUSED, the host all-gather for the staged counts."""
+    _need(world)
+    import torch.multiprocessing as mp
+    mp.spawn(_worker, args=(world, _free_port(), 44, 20011, "uniform", exchange, 3, 1, 0, "boot"), nprocs=world,
              join=True)
 
 
@@ -192,7 +199,7 @@ def _worker_hybrid(rank, world, port, L, B, n, graph, scatter=1):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("scatter", [1, 2, 3])
+@pytest.mark.parametrize("scatter", [1, 2])
 @pytest.mark.parametrize("graph", [False, True])
 @pytest.mark.parametrize("world,L", [(2, 2), (2, 4), (4, 2)])
 def test_multigpu_hybrid_local_ranks(world, L, graph, scatter):

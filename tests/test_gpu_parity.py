@@ -81,16 +81,19 @@ CASES = [
 
 
 EXCHANGES = {"fused": 3, "peer": 2}
-SCATTERS = {"threads": rafi.SCATTER_THREADS, "bulk": rafi.SCATTER_BULK, "aligned": rafi.SCATTER_ALIGNED,
-            "units": rafi.SCATTER_UNITS}
+SCATTERS = {"threads": rafi.SCATTER_THREADS, "bulk": rafi.SCATTER_BULK}
 
 
-@pytest.mark.parametrize("scatter", sorted(SCATTERS))
-@pytest.mark.parametrize("exchange", sorted(EXCHANGES))
-@pytest.mark.parametrize("B,L,n,pattern", CASES)
+def _bulk_ok(B):
+    """BULK needs item_bytes % 4 == 0 and a 256-item tile in shared memory
+    (test_bulk_unsupported checks that it is refused otherwise)."""
+    return B % 4 == 0 and B <= 256
+
+
+@pytest.mark.parametrize("scatter,exchange,B,L,n,pattern",
+                         [(sc, ex) + case for sc in sorted(SCATTERS) for ex in sorted(EXCHANGES) for case in CASES
+                          if sc == "threads" or _bulk_ok(case[0])])
 def test_forward_snapshot_parity(B, L, n, pattern, exchange, scatter):
-    if scatter in ("bulk", "aligned") and (B % 4 or B > 256):
-        pytest.skip("bulk scatter needs item_bytes % 4 == 0 and a 256-item tile in shared memory")
     inputs = make_inputs(L, n, B, pattern, 1234 + B, invalid_frac=0.01)
     cap = max(n * L, 1)
     with _ctx(B, cap, L) as ctx:
@@ -117,10 +120,10 @@ def test_tile_sizes(tile):
 
 @pytest.mark.parametrize("B,tile", [(16, 256), (16, 1024), (16, 2048), (48, 256), (48, 512), (44, 1024),
                                     (128, 256), (4, 4096), (36, 512), (256, 256), (200, 256), (64, 1024)])
-@pytest.mark.parametrize("mode", ["bulk", "aligned"])
+@pytest.mark.parametrize("mode", ["bulk"])
 def test_perm_tile_sizes(B, tile, mode):
-    """The permuting scatters at every tile that fits, ragged last tiles and
-    runs whose global start is not 16-byte aligned (B % 16 != 0)."""
+    """The permuting (TMA bulk-store) scatter at every tile that fits, ragged
+    last tiles and runs whose global start is not 16-byte aligned (B % 16 != 0)."""
     L, n = 4, 20011
     inputs = make_inputs(L, n, B, "uniform", 6 + B)
     with _ctx(B, n * L, L) as ctx:
@@ -343,7 +346,7 @@ def test_forward_graph_rounds_with_option_changes(graph):
         ctx.set_option(rafi.OPT_FORWARD_GRAPH, graph)
         assert ctx.get_option(rafi.OPT_FORWARD_GRAPH) == graph
         steps = [(20000, None), (7, None), (15000, (rafi.OPT_TILE, 1024)), (0, None),
-                 (19999, (rafi.OPT_TIMING, 1)), (12345, (rafi.OPT_SCATTER, rafi.SCATTER_UNITS)),
+                 (19999, (rafi.OPT_TIMING, 1)), (12345, (rafi.OPT_SCATTER, rafi.SCATTER_BULK)),
                  (20000, (rafi.OPT_TILE, 0))]
         for rnd, (n, opt) in enumerate(steps):
             if opt:
@@ -355,3 +358,64 @@ def test_forward_graph_rounds_with_option_changes(graph):
                 st = ctx.stats()  # phase events are recorded by the graph replay too
                 assert st["ms_scatter"] > 0 and st["ms_hist"] > 0 and st["ms_total"] > 0, st
         assert ctx.forward() == 0
+
+
+# ------------------------------------------------------------------ device emit: drop rule and re-emit
+
+@pytest.mark.parametrize("pattern", ["uniform", "self"])
+@pytest.mark.parametrize("B", [16, 24, 44, 48, 64, 128])
+@pytest.mark.parametrize("cap", [1, 31, 1000, 4133])
+def test_device_emit_overflow_drop_rule(B, cap, pattern):
+    """Z1/Z2 through rafi::Queue<T>::emitOutgoing (warp-aggregated): more
+    emits than capacity (cap not a multiple of 32, so a warp's slot range
+    straddles it), mixed invalid destinations.  The counter is not clamped and
+    equals the valid emits; invalid ones are counted and take no slot; exactly
+    min(ctr, cap) items are kept, each one a distinct generator item with its
+    own destination; the forward reports the drops and is P1-exact."""
+    L, n, seed = 3, 9001, 23
+    thr = synth.invalid_threshold(0.05)
+    with _ctx(B, cap, L) as ctx:
+        for l in range(L):
+            ctx.drv_emit_synthetic(synth.PATTERNS[pattern], seed, 2, n, local=l, invalid_threshold=thr)
+        ctrs = []
+        for l in range(L):
+            items, dests, ctr, inv = ctx.read_outgoing(l)
+            ctrs.append(int(ctr))
+            exp_it = synth.make_items(l, 2, n, B)
+            exp_d = synth.make_dests(pattern, seed, l, 2, n, L, invalid_frac=0.05)
+            ok = (exp_d >= 0) & (exp_d < L)
+            assert ctr == ok.sum() and inv == (~ok).sum()
+            assert len(items) == min(ctr, cap)
+            seq = (synth.item_id_of(items) & np.uint64((1 << 40) - 1)).astype(np.int64)
+            assert len(np.unique(seq)) == len(seq)               # no item kept twice
+            assert np.all(ok[seq])                               # only valid emits take slots
+            assert np.array_equal(items, exp_it[seq])            # each slot holds a whole generator item
+            assert np.array_equal(dests, exp_d[seq])             # ... with its own destination
+        # uniform: a receiver may get more than cap (Z3, refused alike by both sides);
+        # self: every rank receives its own cap items, and the stats report the drops
+        w, G = p1_forward(ctx, L, B)  # checks dropped == ctr - min(ctr, cap) per rank, then every byte
+        if pattern == "self":
+            assert G == sum(min(cap, c) for c in ctrs)
+
+
+@pytest.mark.parametrize("B", [4, 8, 12, 16, 20, 44, 48, 64, 128])
+def test_device_reemit_of_resident_batch(B):
+    """rafi_drv_emit_items: a resident (items, dests) batch re-emitted through
+    emitOutgoing with vector loads/stores; the queue holds exactly the valid
+    (item, dest) pairs (as a multiset: warp order follows the atomics), then
+    P1."""
+    L, n = 2, 50001
+    inputs = make_inputs(L, n, B, "uniform", 5 + B, invalid_frac=0.02)
+    with _ctx(B, n, L) as ctx:
+        for l, (it, ds) in enumerate(inputs):
+            ctx.drv_emit_items(torch.from_numpy(it).cuda(), torch.from_numpy(ds).cuda(), n, local=l)
+        for l, (it, ds) in enumerate(inputs):
+            items, dests, ctr, inv = ctx.read_outgoing(l)
+            ok = (ds >= 0) & (ds < L)
+            assert ctr == ok.sum() and inv == (~ok).sum()
+            got = np.concatenate([items, dests.view(np.uint8).reshape(-1, 4)], axis=1)
+            exp = np.concatenate([it[ok], ds[ok].view(np.uint8).reshape(-1, 4)], axis=1)
+            gv = np.sort(got.view(np.dtype((np.void, got.shape[1]))).ravel())
+            ev = np.sort(exp.view(np.dtype((np.void, exp.shape[1]))).ravel())
+            assert np.array_equal(gv, ev)
+        p1_forward(ctx, L, B)
