@@ -52,6 +52,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-graph", action="store_true", help="skip the supplementary graph-replay measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-extras", action="store_true", help="skip the binning_r8 and device_emit blocks")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle cpu_baseline sample")
     return p.parse_args()
 
@@ -142,6 +143,38 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- oracle (CPU)
 
+def host_facts():
+    """nproc and CPU model of the host the oracle runs on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+class pinned_to_core0:
+    """Pin the calling thread to core 0 (taskset -c 0) while the single-threaded oracle runs."""
+
+    def __enter__(self):
+        self.old = None
+        try:
+            self.old = os.sched_getaffinity(0)
+            os.sched_setaffinity(0, {min(self.old)})
+            self.core = min(self.old)
+        except Exception:
+            self.core = None
+        return self
+
+    def __exit__(self, *a):
+        if self.old:
+            os.sched_setaffinity(0, self.old)
+
+
 def oracle_step_rate(R, n, B, pattern, seconds, max_reps=50):
     """The oracle as it stands (single-threaded C): one step = sequential
     emit of every rank's batch + forward, on a bounded sample of the
@@ -156,14 +189,15 @@ def oracle_step_rate(R, n, B, pattern, seconds, max_reps=50):
     cap = n + n // 8 + 4096
     w = oracle.World(R, cap, B)
     times = []
-    t_end = time.perf_counter() + seconds
-    while len(times) < max_reps and (time.perf_counter() < t_end or len(times) < 2):
-        t0 = time.perf_counter()
-        for s, (it, ds) in enumerate(batches):
-            w.emit_many(s, it, ds)
-        G = w.forward()
-        times.append(time.perf_counter() - t0)
-        assert G == R * n, G
+    with pinned_to_core0():
+        t_end = time.perf_counter() + seconds
+        while len(times) < max_reps and (time.perf_counter() < t_end or len(times) < 2):
+            t0 = time.perf_counter()
+            for s, (it, ds) in enumerate(batches):
+                w.emit_many(s, it, ds)
+            G = w.forward()
+            times.append(time.perf_counter() - t0)
+            assert G == R * n, G
     w.close()
     med = statistics.median(times)
     return R * n / med, len(times), "R=%d x %d items x %d B (%s), emit+forward per step, median of %d" % (
@@ -195,25 +229,139 @@ def run_reference(args):
             w.emit_many(s, it, ds)
         assert w.forward() == N * n
 
-    for _ in range(args.warmup):
-        step()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        step()
-    dt = time.perf_counter() - t0
+    with pinned_to_core0():
+        for _ in range(args.warmup):
+            step()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            step()
+        dt = time.perf_counter() - t0
     v = N * n * args.steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "items/s", "n_gpus": N, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic (synth/ SplitMix64 recipe)",
         "config": workload_config(args, N),
-        "cpu_baseline": {"value": v, "unit": "items/s", "cores": 1, "kind": "oracle",
-                         "sample": "R=%d x %d items x %d B per step (bounded sample of the workload), "
-                                   "sequential emit + plain forward, single-threaded C oracle"
-                                   % (N, n, args.item_bytes)},
+        "cpu_baseline": dict({"value": v, "unit": "items/s", "cores": 1, "kind": "oracle",
+                              "sample": "R=%d x %d items x %d B per step (bounded sample of the workload), "
+                                        "sequential emit + plain forward, single-threaded C oracle pinned to "
+                                        "one core (sched_setaffinity, as taskset -c 0)" % (N, n, args.item_bytes)},
+                             **host_facts()),
         "e2e": {"value": v, "unit": "items/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- NVLink counters
+
+def nvlink_counters(gpu):
+    """Per-link NVLink transmit / receive byte counters of one GPU (NVML field
+    values NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES / _RCV_BYTES summed over the
+    links), or None where NVML does not expose them."""
+    try:
+        import pynvml as nv
+        nv.nvmlInit()
+        h = nv.nvmlDeviceGetHandleByIndex(gpu)
+        nl = nv.nvmlDeviceGetFieldValues(h, [(nv.NVML_FI_DEV_NVLINK_LINK_COUNT, 0)])[0]
+        links = int(nl.value.uiVal) if nl.nvmlReturn == 0 else 18
+        tx = rx = 0
+        for fid, acc in ((nv.NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES, "tx"), (nv.NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES, "rx")):
+            vals = nv.nvmlDeviceGetFieldValues(h, [(fid, l) for l in range(links)])
+            if any(v.nvmlReturn != 0 for v in vals):
+                return None
+            total = sum(int(v.value.ullVal) for v in vals)
+            if acc == "tx":
+                tx = total
+            else:
+                rx = total
+        return {"tx": tx, "rx": rx, "links": links}
+    except Exception:
+        return None
+
+
+def nvlink_delta(c0, c1, remote_bytes):
+    if not c0 or not c1:
+        return {"available": False, "why": "NVML NVLink byte counters not exposed on this box"}
+    tx, rx = c1["tx"] - c0["tx"], c1["rx"] - c0["rx"]
+    return {"available": True, "tx_bytes": tx, "rx_bytes": rx, "links": c0["links"],
+            "algorithmic_remote_bytes": remote_bytes,
+            "tx_over_algorithmic": tx / remote_bytes if remote_bytes else None,
+            "what": "NVML_FI_DEV_NVLINK_COUNT_XMIT/RCV_BYTES summed over links, read before and after the timed "
+                    "region (all K steps, this GPU); includes protocol overhead"}
+
+
+# ----------------------------------------------------------------------------- supplementary blocks
+
+def bench_binning_r8(rafi, synth, torch, stream, args, hbm_peak):
+    """R=8 binning on one GPU: the whole cfg2 world (8 logical ranks x 16M x
+    48-B items, uniform destinations) forwarded FUSED into local queues; the
+    per-kernel durations of histogram + scan + scatter (CUDA events on the
+    context stream, instrumented forwards) against their algorithmic bytes
+    2B+8 per item."""
+    L, n, B = 8, args.items, args.item_bytes
+    cap = n + n // 8
+    ctx = rafi.Context(B, cap, stream=stream, local_ranks=L)
+    try:
+        ctx.set_option(rafi.OPT_TIMING, 1)
+        for k in range(args.warmup + args.steps):
+            if k == args.warmup:
+                ctx.set_option(rafi.OPT_TIMING, 1)  # resets the accumulated phase sums
+            for l in range(L):
+                ctx.drv_emit_synthetic(synth.PATTERNS["uniform"], synth.CONFIG_SEEDS[2], k, n, local=l)
+            assert ctx.forward() == L * n
+        st = ctx.stats()
+        K = st["acc_forwards"]
+        ms = {p: st["acc_ms_" + p] / K for p in ("hist", "scan", "count_exchange", "scatter")}
+        tot = ms["hist"] + ms["scan"] + ms["count_exchange"] + ms["scatter"]
+        byts = L * n * (2 * B + 8)
+        gbs = byts / (tot / 1e3) / 1e9
+        sc_bytes = L * n * (2 * B + 4)
+        return {"workload": "cfg2 world on one GPU: %d logical ranks x %d x %d-B items, uniform over R=%d, FUSED "
+                            "into local incoming queues" % (L, n, B, L),
+                "items": L * n, "ms": tot, "ms_phases": ms, "algorithmic_bytes": byts, "achieved_gbs": gbs,
+                "frac": gbs / hbm_peak, "frac_of_8tbs": gbs / 8000.0, "peak": hbm_peak,
+                "scatter_gbs": sc_bytes / (ms["scatter"] / 1e3) / 1e9,
+                "scatter_frac": sc_bytes / (ms["scatter"] / 1e3) / 1e9 / hbm_peak,
+                "tile": ctx.get_option(rafi.OPT_TILE), "forwards_timed": K,
+                "what": "histogram + scan(+plan) + stable scatter of one forward; bytes = (2B+8) per item: hist "
+                        "reads 4, scatter reads B+4 and writes B"}
+    finally:
+        ctx.close()
+
+
+def bench_device_emit(rafi, torch, stream, items_d, dests_d, args, hbm_peak):
+    """The app-facing emit (rafi::Queue<T>::emitOutgoing, warp-aggregated
+    atomics, vector stores) re-emitting the resident batch: algorithmic bytes
+    2(B+4) per item (read item + dest, write item + dest)."""
+    n, B = args.items, args.item_bytes
+    ctx = rafi.Context(B, n, stream=stream)
+    out = {}
+    try:
+        for batch in (8, 1):
+            evs = []
+            for k in range(args.warmup + args.steps):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                ctx.drv_emit_items(items_d, dests_d, n, batch=batch)
+                b.record(stream)
+                if k >= args.warmup:
+                    evs.append((a, b))
+                assert ctx.forward() == n  # empties the queue (untimed)
+            stream.synchronize()
+            ms = sum(a.elapsed_time(b) for a, b in evs) / len(evs)
+            byts = n * 2 * (B + 4)
+            gbs = byts / (ms / 1e3) / 1e9
+            out["batch%d" % batch] = {"ms": ms, "achieved_gbs": gbs, "frac": gbs / hbm_peak,
+                                      "items_per_s": n / (ms / 1e3)}
+        best = out["batch8"]
+        return dict(best, items=n, algorithmic_bytes=n * 2 * (B + 4), single=out["batch1"],
+                    what="rafi_drv_emit_items, the app-facing device emit: threads load items (16-B vectors) "
+                         "and emit through rafi::Queue<T> (16-B vector stores); top level = batched "
+                         "emitOutgoing<8> (one warp atomicAdd per 256 items), 'single' = one emitOutgoing per "
+                         "item (one warp atomicAdd per 32 items: bounded by the emit counter's per-address L2 "
+                         "atomic rate); CUDA events around each launch")
+    finally:
+        ctx.close()
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -306,13 +454,19 @@ def main():
     clocks.start()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
+    f_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    nvl0 = nvlink_counters(local) if N > 1 else None
     t_start.record(stream)
     for k in range(args.steps):
         ctx.emit_bulk(items_d, dests_d, n)
+        f_ev[k][0].record(stream)     # forward only (a2-a8): events around each rafi_forward
         G = ctx.forward()
+        f_ev[k][1].record(stream)
     t_end.record(stream)
     barrier()
+    nvl1 = nvlink_counters(local) if N > 1 else None
     clk = clocks.stop()
+    ms_fwd = max_over_ranks(sum(a.elapsed_time(b) for a, b in f_ev))
     st = ctx.stats()
     launches = st["kernel_launches"] - l0
     remote = st["bytes_sent_remote"] * args.steps  # same plan every step
@@ -339,6 +493,10 @@ def main():
     assert st["acc_forwards"] == K and st["acc_emits"] == K, (st["acc_forwards"], st["acc_emits"])
     value = N * n * K / (ms_max / 1e3)
     ms_step = ms_max / K
+    forward_only = {"value": N * n * K / (ms_fwd / 1e3), "unit": "items/s", "ms_per_forward": ms_fwd / K,
+                    "what": "rafi_forward alone (hist, scan, count exchange, scatter/payload exchange, wrap-up, "
+                            "termination count), emission excluded: the paper's sort-and-send (PAPER:449); CUDA "
+                            "events around each forward inside the timed region, max over ranks"}
     ph = {k: st["acc_ms_" + k] / K for k in ("emit", "hist", "scan", "scatter", "count_exchange",
                                             "payload_exchange", "wrapup")}
 
@@ -358,17 +516,20 @@ def main():
         gbs = byts / (ph[k] / 1e3) / 1e9
         kern[k] = {"ms": ph[k], "bytes": byts, "achieved_gbs": gbs, "frac": gbs / hbm_peak}
     dom = max(kern, key=lambda k: kern[k]["ms"])
-    traffic = None
+    traffic, traffic_src = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f)
         key = "%s/B%d/n%d/R%d" % (dom, B, n, N)
         traffic = tr.get(key)
+        if traffic is not None:
+            traffic_src = "STORED, not measured in this run: dram__bytes_read.sum + dram__bytes_write.sum of " \
+                          "one ncu --set full capture, %s" % tr.get("_capture", tr.get("_about", "")[:160])
     except Exception:
         pass
     roofline = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["achieved_gbs"], "peak": hbm_peak,
-                "unit": "GB/s", "frac": kern[dom]["frac"], "traffic": traffic, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": kern[dom]["bytes"]}
+                "unit": "GB/s", "frac": kern[dom]["frac"], "traffic": traffic, "traffic_source": traffic_src,
+                "peak_source": peak_src, "algorithmic_bytes_per_launch": kern[dom]["bytes"]}
     exch = None
     xfer_ms = ph["scatter"] if exchange == "fused" else ph["payload_exchange"]
     if N > 1 and xfer_ms > 0:
@@ -378,7 +539,7 @@ def main():
         ceil = nvlink_ceilings(N)
         exch = {"gbs_per_gpu": gbs, "frac_of_900": gbs / 900.0, "frac_of_770_measured_p2p": gbs / 770.0,
                 "transport": exchange, "remote_bytes_per_step": remote / K, "kernel_ms": xfer_ms,
-                "ceilings_gbs": ceil}
+                "ceilings_gbs": ceil, "nvlink_counters": nvlink_delta(nvl0, nvl1, remote)}
         if exchange == "fused" and xfer_ms >= max(v["ms"] for v in kern.values()):
             # the step's dominant phase moves bytes over NVLink: that is its roofline
             # (peak: the profiling guide's measured 770 GB/s peer copy per direction)
@@ -452,13 +613,23 @@ def main():
         graph = {"value": N * n * K / (ms_g / 1e3), "unit": "items/s", "ms_per_step": ms_g / K,
                  "what": "[emit_bulk + rafi_forward_async] captured as one CUDA graph, replayed K times"}
 
+    # ---- supplementary single-GPU blocks: R=8 binning and the device-side emit
+    binning_r8 = device_emit = None
+    if N == 1 and not args.no_extras:
+        ctx.close()
+        ctx = None
+        torch.cuda.empty_cache()
+        binning_r8 = bench_binning_r8(rafi, synth, torch, stream, args, hbm_peak)
+        device_emit = bench_device_emit(rafi, torch, stream, items_d, dests_d, args, hbm_peak)
+
     # ---- cpu baseline: the oracle on the host, rank 0 at N=1 only
     cpu = None
     if N == 1 and rank == 0 and not args.no_cpu_baseline:
         ns = cpu_sample_size(args, 1)
         v, reps, desc = oracle_step_rate(1, ns, B, args.pattern, args.cpu_seconds)
-        cpu = {"value": v, "unit": "items/s", "cores": 1, "kind": "oracle",
-               "sample": desc + " (single-threaded C oracle on the GPU box host)"}
+        cpu = dict({"value": v, "unit": "items/s", "cores": 1, "kind": "oracle",
+                    "sample": desc + " (single-threaded C oracle on the GPU box host, pinned to one core "
+                                     "with sched_setaffinity as taskset -c 0)"}, **host_facts())
 
     line = {
         "metric": METRIC, "value": value, "unit": "items/s", "n_gpus": N, "steps": K, "warmup": args.warmup,
@@ -468,10 +639,12 @@ def main():
         "clocks": clk, "phases_ms": ph, "phases_source": "instrumented pass of the same K steps (CUDA events "
         "between launches); its ms_per_step: %.4f" % ms_instr, "kernels": kern, "exchange": exch, "exchange_transport": exchange,
         "graph_replay": graph, "scatter_write": scatter, "tile": ctx_tile, "control": control, "per_gpu_items_per_s": value / N,
+        "forward_only": forward_only, "binning_r8": binning_r8, "device_emit": device_emit,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
-    ctx.close()
+    if ctx is not None:
+        ctx.close()
     if comm:
         rafi.nccl_comm_destroy(comm)
     if world > 1:

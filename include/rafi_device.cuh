@@ -124,6 +124,52 @@ struct Queue {
     return true;
   }
 
+  /* Batched emitOutgoing: this thread emits items[0..count) to dests[0..count)
+     (count <= K), with the same accept / drop / reject rules as K single
+     calls.  The warp takes ONE atomicAdd for all its lanes' items (instead of
+     one per emitOutgoing call): under full-GPU load the single emit counter's
+     atomic unit serialises per address, and this is what lifts emission to
+     the HBM write roofline.  Slots are item-major within the warp (item k of
+     every lane, then item k+1), so the stores of each k are coalesced.
+     Returns how many of this thread's items were stored. */
+  template <int K>
+  __device__ int emitOutgoing(const T (&items)[K], const int (&dests)[K], int count = K) const {
+    const unsigned active = __activemask();
+    const unsigned lane = lane_id();
+    unsigned vm[K];
+    unsigned total = 0, ninv = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const bool in_batch = k < count;
+      const bool valid = in_batch && (unsigned)dests[k] < (unsigned)v.num_ranks;
+      vm[k] = __ballot_sync(active, valid);
+      ninv += __popc(__ballot_sync(active, in_batch && !valid));
+      total += __popc(vm[k]);
+    }
+    const unsigned leader = __ffs(active) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) {
+      if (total) base = atomicAdd(v.ctr, (unsigned long long)total);
+      if (ninv) atomicAdd(v.invalid, (unsigned long long)ninv);
+    }
+    base = __shfl_sync(active, base, leader);
+    const unsigned lt = lanemask_lt();
+    int stored = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (vm[k] & (1u << lane)) {
+        const unsigned long long slot = base + __popc(vm[k] & lt);
+        if (slot < v.capacity) {
+          store_item<T>(static_cast<char*>(v.out) + slot * sizeof(T), items[k]);
+          v.dest[slot] = dests[k];
+          ++stored;
+        }
+      }
+      base += __popc(vm[k]);
+    }
+    return stored;
+  }
+
   __host__ __device__ int numRanks() const { return v.num_ranks; }
   __host__ __device__ int myRank() const { return v.my_rank; }
 };

@@ -42,14 +42,16 @@ int rafi_drv_emit_synthetic(rafi_ctx* ctx, int local, int pattern, uint64_t seed
                             uint64_t seq0, int target, uint64_t invalid_threshold);
 
 /* Device re-emit of a resident batch (the app-facing emit path, PAPER:70-71,
- * 98): thread i loads items[i] (item_bytes, packed; a device pointer aligned
- * to 16 bytes) and dests[i] (int32, device) and calls
- * rafi::Queue<T>::emitOutgoing on local rank `local`'s queue -- one
- * warp-aggregated atomicAdd per warp, vector item stores.  Same accept / drop /
- * reject rules as every emit.  For item sizes of rafi_drv_emit_synthetic plus
- * 4, 8 and 12 bytes (RAFI_ERR_UNSUPPORTED otherwise).  Used to time the device
- * emit against its 2 * (item_bytes + 4) bytes-per-item roofline. */
-int rafi_drv_emit_items(rafi_ctx* ctx, int local, const void* items, const int32_t* dests, uint64_t n);
+ * 98): threads load items (item_bytes, packed; a device pointer aligned to 16
+ * bytes) and their dests (int32, device) and emit them through
+ * rafi::Queue<T> on local rank `local`'s queue, with vector item loads and
+ * stores.  batch = 1: one emitOutgoing(item, dest) per item (one warp
+ * atomicAdd per 32 items); batch = 8: the batched emitOutgoing<8> (one warp
+ * atomicAdd per 256 items).  Same accept / drop / reject rules as every emit.
+ * For item sizes of rafi_drv_emit_synthetic plus 4, 8 and 12 bytes
+ * (RAFI_ERR_UNSUPPORTED otherwise).  Used to time the device emit against its
+ * 2 * (item_bytes + 4) bytes-per-item roofline. */
+int rafi_drv_emit_items(rafi_ctx* ctx, int local, const void* items, const int32_t* dests, uint64_t n, int batch);
 
 /* Random-walk step (cfg1 app kernel): every incoming item of every local
  * rank gets round field = rnd and is re-emitted to

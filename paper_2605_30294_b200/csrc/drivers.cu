@@ -84,12 +84,36 @@ __global__ void k_drv_walk(rafi_device_view v, uint64_t seed, uint32_t rnd, uint
   }
 }
 
-template <int B>
-__global__ void k_drv_emit_items(rafi_device_view v, const uint8_t* __restrict__ items,
-                                 const int32_t* __restrict__ dests, uint64_t n) {
+// Device re-emit of a resident batch.  kBatch == 1: one emitOutgoing(item,
+// dest) per item (one warp atomic per 32 items); kBatch > 1: each thread
+// emits kBatch items with the batched emitOutgoing (one warp atomic per
+// 32 * kBatch items).  Thread t of a block-chunk handles items t, t + blockDim,
+// ... so the loads of each k are coalesced.
+template <int B, int kBatch>
+__global__ void __launch_bounds__(256) k_drv_emit_items(rafi_device_view v, const uint8_t* __restrict__ items,
+                                                        const int32_t* __restrict__ dests, uint64_t n) {
   rafi::Queue<Item<B>> q(v);
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    q.emitOutgoing(rafi::load_item<Item<B>>(items + i * B), dests[i]);
+  const uint64_t chunk = (uint64_t)blockDim.x * kBatch;
+  for (uint64_t c0 = blockIdx.x * chunk; c0 < n; c0 += (uint64_t)gridDim.x * chunk) {
+    if (kBatch == 1) {
+      const uint64_t i = c0 + threadIdx.x;
+      if (i < n) q.emitOutgoing(rafi::load_item<Item<B>>(items + i * B), dests[i]);
+      continue;
+    }
+    Item<B> it[kBatch];
+    int d[kBatch];
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k) {
+      const uint64_t i = c0 + (uint64_t)k * blockDim.x + threadIdx.x;
+      if (i < n) {
+        it[k] = rafi::load_item<Item<B>>(items + i * B);
+        d[k] = dests[i];
+        cnt = k + 1;
+      }
+    }
+    q.emitOutgoing<kBatch>(it, d, cnt);
+  }
 }
 
 // Threads to launch for an app step over the incoming queue: the host-known
@@ -319,20 +343,23 @@ extern "C" int rafi_drv_emit_synthetic(rafi_ctx* ctx, int local, int pattern, ui
   }
 }
 
-extern "C" int rafi_drv_emit_items(rafi_ctx* ctx, int local, const void* items, const int32_t* dests, uint64_t n) {
+extern "C" int rafi_drv_emit_items(rafi_ctx* ctx, int local, const void* items, const int32_t* dests, uint64_t n,
+                                   int batch) {
   auto* c = reinterpret_cast<rafi_impl::Ctx*>(ctx);
   rafi_device_view v;
   int rc = rafi_get_device_view(ctx, local, &v);
   if (rc != RAFI_OK) return rc;
   if (n == 0) return RAFI_OK;
-  if (!items || !dests || ((uintptr_t)items & 15)) return RAFI_ERR_INVALID_ARG;
+  if (!items || !dests || ((uintptr_t)items & 15) || (batch != 1 && batch != 8)) return RAFI_ERR_INVALID_ARG;
   if (cudaSetDevice(c->device) != cudaSuccess) return RAFI_ERR_CUDA;
-  const uint64_t blocks = (n + 255) / 256;
-  const int grid = (int)(blocks < 148 * 16 ? blocks : 148 * 16);
+  const uint64_t blocks = (n + 256ull * batch - 1) / (256ull * batch);
+  const int grid = (int)(blocks < 148 * 8 ? blocks : 148 * 8);
+  const uint8_t* it = static_cast<const uint8_t*>(items);
   switch (v.item_bytes) {
-#define CASE(B)                                                                                          \
-  case B:                                                                                                \
-    k_drv_emit_items<B><<<grid, 256, 0, c->stream>>>(v, static_cast<const uint8_t*>(items), dests, n); \
+#define CASE(B)                                                                                        \
+  case B:                                                                                              \
+    if (batch == 1) k_drv_emit_items<B, 1><<<grid, 256, 0, c->stream>>>(v, it, dests, n);            \
+    else k_drv_emit_items<B, 8><<<grid, 256, 0, c->stream>>>(v, it, dests, n);                       \
     break;
     RAFI_DRV_ITEM_SIZES(CASE)
 #undef CASE

@@ -114,7 +114,7 @@ SIGNATURES = {
     "rafi_create_boot": (C.c_int, [C.POINTER(C.c_void_p), C.POINTER(CreateParams), C.POINTER(Bootstrap)]),
     "rafi_selftest_peer_control": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_longlong,
                                              C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
-    "rafi_drv_emit_items": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_uint64]),
+    "rafi_drv_emit_items": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int]),
     "rafi_resize": (C.c_int, [C.c_void_p, C.c_size_t]),
     "rafi_destroy": (None, [C.c_void_p]),
     "rafi_get_device_view": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(DeviceView)]),
@@ -439,11 +439,13 @@ class Context:
         _check(lib().rafi_drv_emit_synthetic(self._h, local, pattern, seed, rnd, n, seq0, target, invalid_threshold),
                "rafi_drv_emit_synthetic")
 
-    def drv_emit_items(self, items, dests, n: int | None = None, local: int = 0):
-        """Device re-emit of a resident batch through rafi::Queue<T>::emitOutgoing."""
+    def drv_emit_items(self, items, dests, n: int | None = None, local: int = 0, batch: int = 1):
+        """Device re-emit of a resident batch through rafi::Queue<T>::emitOutgoing
+        (batch = 1) or the batched emitOutgoing<8> (batch = 8)."""
         if n is None:
             n = len(dests)
-        _check(lib().rafi_drv_emit_items(self._h, local, _ptr(items), _ptr(dests), int(n)), "rafi_drv_emit_items")
+        _check(lib().rafi_drv_emit_items(self._h, local, _ptr(items), _ptr(dests), int(n), int(batch)),
+               "rafi_drv_emit_items")
 
     def drv_random_walk(self, seed: int, rnd: int, last_round: int):
         _check(lib().rafi_drv_random_walk(self._h, seed, rnd, last_round), "rafi_drv_random_walk")

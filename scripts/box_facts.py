@@ -32,12 +32,12 @@ try:
     N.nvmlInit()
     h = N.nvmlDeviceGetHandleByIndex(0)
     out = {}
-    for name in ("NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX", "NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX",
-                 "NVML_FI_DEV_NVLINK_THROUGHPUT_RAW_TX", "NVML_FI_DEV_NVLINK_THROUGHPUT_RAW_RX",
+    for name in ("NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES", "NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES",
+                 "NVML_FI_DEV_NVLINK_COUNT_XMIT_PACKETS", "NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX",
                  "NVML_FI_DEV_NVLINK_LINK_COUNT"):
         fid = getattr(N, name)
         res = []
-        for scope in (0xFFFFFFFF, 0, 1):
+        for scope in (0xFFFFFFFF, 0, 1, 17):
             try:
                 v = N.nvmlDeviceGetFieldValues(h, [(fid, scope)])[0]
                 res.append({"scope": scope, "ret": int(v.nvmlReturn), "type": int(v.valueType),

@@ -398,17 +398,18 @@ def test_device_emit_overflow_drop_rule(B, cap, pattern):
             assert G == sum(min(cap, c) for c in ctrs)
 
 
+@pytest.mark.parametrize("batch", [1, 8])
 @pytest.mark.parametrize("B", [4, 8, 12, 16, 20, 44, 48, 64, 128])
-def test_device_reemit_of_resident_batch(B):
+def test_device_reemit_of_resident_batch(B, batch):
     """rafi_drv_emit_items: a resident (items, dests) batch re-emitted through
-    emitOutgoing with vector loads/stores; the queue holds exactly the valid
-    (item, dest) pairs (as a multiset: warp order follows the atomics), then
-    P1."""
+    emitOutgoing (single or batched) with vector loads/stores; the queue holds
+    exactly the valid (item, dest) pairs (as a multiset: warp order follows
+    the atomics), then P1."""
     L, n = 2, 50001
     inputs = make_inputs(L, n, B, "uniform", 5 + B, invalid_frac=0.02)
     with _ctx(B, n, L) as ctx:
         for l, (it, ds) in enumerate(inputs):
-            ctx.drv_emit_items(torch.from_numpy(it).cuda(), torch.from_numpy(ds).cuda(), n, local=l)
+            ctx.drv_emit_items(torch.from_numpy(it).cuda(), torch.from_numpy(ds).cuda(), n, local=l, batch=batch)
         for l, (it, ds) in enumerate(inputs):
             items, dests, ctr, inv = ctx.read_outgoing(l)
             ok = (ds >= 0) & (ds < L)
@@ -419,3 +420,24 @@ def test_device_reemit_of_resident_batch(B):
             ev = np.sort(exp.view(np.dtype((np.void, exp.shape[1]))).ravel())
             assert np.array_equal(gv, ev)
         p1_forward(ctx, L, B)
+
+
+@pytest.mark.parametrize("batch", [1, 8])
+@pytest.mark.parametrize("cap", [1, 1000, 30001])
+def test_device_reemit_drop_rule(batch, cap):
+    """Z1/Z2 for the single and the batched device emit: over capacity (cap
+    not a multiple of the 32- or 256-item warp reservation), with invalid
+    destinations.  ctr = valid emits, invalid counted, min(ctr, cap) kept,
+    every kept slot a distinct input pair with its own destination."""
+    B, n = 48, 50001
+    (it, ds), = make_inputs(1, n, B, "self", 77, invalid_frac=0.03)
+    with _ctx(B, cap, 1) as ctx:
+        ctx.drv_emit_items(torch.from_numpy(it).cuda(), torch.from_numpy(ds).cuda(), n, batch=batch)
+        items, dests, ctr, inv = ctx.read_outgoing(0)
+        ok = (ds >= 0) & (ds < 1)
+        assert ctr == ok.sum() and inv == (~ok).sum() and len(items) == min(ctr, cap)
+        seq = (synth.item_id_of(items) & np.uint64((1 << 40) - 1)).astype(np.int64)
+        assert len(np.unique(seq)) == len(seq) and np.all(ok[seq])
+        assert np.array_equal(items, it[seq]) and np.array_equal(dests, ds[seq])
+        w, G = p1_forward(ctx, 1, B)
+        assert G == min(ctr, cap)

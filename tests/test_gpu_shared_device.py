@@ -39,7 +39,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, B, L, n, pattern, exchange, rounds, resize_to):
+def _worker(rank, world, port, B, L, n, pattern, exchange, rounds, resize_round):
     import torch.distributed as dist
 
     import oracle
@@ -51,7 +51,7 @@ def _worker(rank, world, port, B, L, n, pattern, exchange, rounds, resize_to):
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     R = world * L
-    cap = 2 * n
+    cap = R * n  # any pattern fits (all_to_one sends everything to one rank)
     stream = torch.cuda.Stream()
     ctx = rafi.Context(B, cap, stream=stream, local_ranks=L, bootstrap=(world, rank, rafi.torch_allgather()))
     assert ctx.num_ranks == R and ctx.rank_of(0) == rank * L
@@ -65,8 +65,8 @@ def _worker(rank, world, port, B, L, n, pattern, exchange, rounds, resize_to):
     with pytest.raises(rafi.RafiError):        # HOST control synchronises with the host: not capturable
         ctx.forward_async(torch.zeros(1, dtype=torch.int64, device="cuda"))
     for rnd in range(rounds):
-        if rnd == resize_to[0]:
-            cap = resize_to[1]
+        if rnd == resize_round:
+            cap = R * n + 1000
             ctx.resize(cap)                    # collective; old queues freed after every process unmapped them
             assert ctx.capacity == cap
         m = n if rnd % 2 == 0 else n // 3 + rnd
@@ -103,7 +103,7 @@ def _worker(rank, world, port, B, L, n, pattern, exchange, rounds, resize_to):
                                            (16, 3, 5000, "all_to_one")])
 def test_two_processes_one_gpu_host_control(B, L, n, pattern, exchange):
     import torch.multiprocessing as mp
-    mp.spawn(_worker, args=(2, _free_port(), B, L, n, pattern, exchange, 4, (2, 3 * n)), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), B, L, n, pattern, exchange, 4, 2), nprocs=2, join=True)
 
 
 def _worker_mismatch(rank, world, port):

@@ -164,6 +164,67 @@ def test_ray_march_straight_line_exit():
     assert rounds <= 3 + 1   # a straight line crosses at most 3 brick faces of a 2x2x2 grid
 
 
+def _march_once(w, R, g, seed, p_thr, max_bounces, max_steps, n):
+    res = np.full(R * n, -1.0, np.float32)
+    for r in range(R):
+        w.march_step(r, seed, p_thr, max_bounces, max_steps, g, res)
+    return res, w.forward()
+
+
+def _dist_to_boundary(o):
+    return float(min(min(o), min(1.0 - np.asarray(o, np.float64))))
+
+
+def test_ray_march_always_scatter_bounce_count_and_time():
+    """p_thr = 2^32 - 1 (a scatter event at every step, barring hash value
+    2^32-1) and max_steps = max_bounces = k on one brick: a ray whose origin
+    is farther than k/256 from the domain boundary cannot leave it, so it
+    takes exactly k steps -- t == k/256 exactly (dyadic sums), bounces == k,
+    a unit direction after every redirect, displacement <= k/256 -- and is
+    re-emitted to its own rank.  One more step makes bounces = k+1 > k: each
+    of them retires on that step with 0 < integral <= t + 1/256."""
+    R, n, k, seed = 1, 4000, 6, 11
+    w, g = _seed_world(R, n, 48, "march", seed)
+    start = {int(y["id"]): y["o"].astype(np.float64) for y in _rays(w.incoming(0))}
+    deep = {i for i, o in start.items() if _dist_to_boundary(o) > (k + 1) / 256.0}
+    assert len(deep) > 0.8 * n
+    res, G = _march_once(w, R, g, seed, 2**32 - 1, k, k, n)
+    rays = {int(y["id"]): y for y in _rays(w.incoming(0))}
+    assert deep <= set(rays)                       # every deep ray survives the k steps
+    for i in deep:
+        y = rays[i]
+        assert float(y["t"]) == k / 256.0 and int(y["bounces"]) == k
+        assert abs(np.linalg.norm(y["d"].astype(np.float64)) - 1.0) < 4e-7
+        assert np.linalg.norm(y["o"].astype(np.float64) - start[i]) <= k / 256.0 + 1e-6
+        assert 0.0 < float(y["integral"]) <= k / 256.0
+        assert res[i] == -1.0                      # not retired
+    before = {i: float(rays[i]["integral"]) for i in deep}
+    res, G = _march_once(w, R, g, seed, 2**32 - 1, k, 10**6, n)
+    assert G == 0                                  # everything retired (bounce limit or domain exit)
+    for i in deep:
+        assert before[i] < res[i] <= before[i] + 1.0 / 256.0
+
+
+@pytest.mark.parametrize("p_log2", [1, 2, 3])
+def test_ray_march_scatter_probability(p_log2):
+    """p_thr = 2^(32-p) scatters with probability 2^-p per step: over m steps
+    deep inside one brick the mean bounce count is m * 2^-p (binomial; a
+    reversed comparison would give m * (1 - 2^-p)), and redirected
+    directions are isotropic (mean direction ~ 0)."""
+    R, n, m, seed = 1, 20000, 8, 7
+    w, g = _seed_world(R, n, 48, "march", seed)
+    deep = {int(y["id"]) for y in _rays(w.incoming(0)) if _dist_to_boundary(y["o"]) > (m + 1) / 256.0}
+    res, G = _march_once(w, R, g, seed, 2 ** (32 - p_log2), 10**6, m, n)
+    rays = [y for y in _rays(w.incoming(0)) if int(y["id"]) in deep]
+    b = np.array([int(y["bounces"]) for y in rays], np.float64)
+    p = 2.0 ** -p_log2
+    sd = np.sqrt(m * p * (1 - p) / len(b))
+    assert abs(b.mean() - m * p) < 6 * sd
+    moved = np.array([y["d"] for y in rays if int(y["bounces"]) > 0], np.float64)
+    assert len(moved) > 1000 and np.all(np.abs(moved.mean(axis=0)) < 0.05)
+    assert np.all(np.abs(np.linalg.norm(moved, axis=1) - 1.0) < 4e-7)
+
+
 # ------------------------------------------------------------------ GPU parity
 
 def _gpu():
