@@ -108,18 +108,22 @@ def build_tools() -> list:
 VARIANTS = {  # scatter tuning experiments: name -> defines (build with --variants)
     "ilp2": ["RAFI_SCATTER_ILP=2"],
     "ilp8": ["RAFI_SCATTER_ILP=8"],
+    "w3": ["RAFI_W_STAGES=3"],
+    "u4": ["RAFI_W_UNROLL=4"],
     "debug": ["RAFI_DEBUG_BOUNDS=1"],  # device-side bounds checks (scripts/sanitize_cases.py)
 }
 
 
-def build_variants():
+def build_variants(names=None):
     os.makedirs(os.path.join(PKG, "_variants"), exist_ok=True)
     return [build(force=True, defines=d, out=os.path.join(PKG, "_variants", "librafi_%s.so" % n))
-            for n, d in VARIANTS.items()]
+            for n, d in VARIANTS.items() if not names or n in names]
 
 
 if __name__ == "__main__":
     if "--variants" in sys.argv:
-        print(build_variants())
+        i = sys.argv.index("--variants")
+        names = sys.argv[i + 1].split(",") if i + 1 < len(sys.argv) and not sys.argv[i + 1].startswith("-") else None
+        print(build_variants(names))
     else:
         print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -308,7 +308,7 @@ static int resolve_scatter(Ctx* c) {
 }
 
 static uint32_t auto_tile(const Ctx* c) {
-  return c->scatter_eff == RAFI_SCATTER_BULK ? choose_tile_perm(c->B, c->R) : choose_tile(c->B);
+  return c->scatter_eff == RAFI_SCATTER_BULK ? choose_tile_perm(c->B, c->R) : choose_tile(c->B, c->R, c->L);
 }
 
 // Binning tile (between rounds); grows H/O when the tile count grows.

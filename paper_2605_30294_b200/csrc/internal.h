@@ -175,7 +175,7 @@ inline RankDev* rank_table(Ctx* c) { return c->rank_dev; }
 inline size_t ctrl_c_bytes(const Ctx* c) { return sizeof(CtrlDev) * c->L + sizeof(uint64_t) * c->R * c->R; }
 
 // kernels.cu
-uint32_t choose_tile(uint64_t item_bytes);
+uint32_t choose_tile(uint64_t item_bytes, int R, int L);
 uint32_t choose_tile_perm(uint64_t item_bytes, int R);
 bool perm_supported(uint64_t item_bytes);
 size_t perm_smem_bytes(uint32_t tile, uint64_t item_bytes, int R);

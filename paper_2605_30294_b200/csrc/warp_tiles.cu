@@ -1,0 +1,446 @@
+// warp_tiles.cu -- the warp-tile binning path (a2 histogram + a4 stable
+// scatter) for R <= 8 destinations and item sizes that are a multiple of 8 B.
+//
+// The binning tile is 256 items and ONE WARP owns a whole tile, from the TMA
+// load to the last store, so the scatter needs no block-level barrier at all:
+//
+//   k_hist_w     a2  persistent; one warp counts one scan block (8 tiles,
+//                    2048 dests) at a time, streamed through a private
+//                    three-stage ring of 8-KiB TMA bulk loads: per-lane byte
+//                    counters, a 31-shuffle butterfly reduce-scatter that
+//                    leaves lane j with word j of the 8 x 8 count table, and
+//                    the in-block prefix (O) and block total (H) -- the same
+//                    two-level layout k_scan and both scatters read.
+//   k_scatter_w  a4  persistent, one CTA per SM of up to 16 independent warps.
+//                    Each warp streams its tiles through a private two-stage
+//                    ring of 1-D TMA bulk loads (items + dests, mbarrier
+//                    completion), ranks the tile's items among same-destination
+//                    items in slot order (__match_any_sync), and
+//                    writes every destination run with coalesced 16/8-byte
+//                    unit stores straight into the destination queue (the local
+//                    send batch, the local incoming queue, or -- FUSED -- a
+//                    peer's incoming queue over NVLink).
+//
+// Why (profiles/r02_binning_r8.md): the block-tile scatter of kernels.cu pays
+// ~6 __syncthreads per tile; at R = 8 its warps spend a third of their time
+// in barriers and the kernel reaches 0.65 of HBM.  Here a warp only ever waits
+// for its own data.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "devcommon.cuh"
+#include "internal.h"
+
+namespace rafi_impl {
+
+constexpr int kWK = (int)kWarpTile / 32;  // items per lane of a warp tile
+// tuning (build-time; paper_2605_30294_b200/build.py variants)
+#ifndef RAFI_W_STAGES
+#define RAFI_W_STAGES 2
+#endif
+#ifndef RAFI_W_UNROLL
+#define RAFI_W_UNROLL 8
+#endif
+constexpr int kWStages = RAFI_W_STAGES;   // TMA ring depth per warp
+constexpr int kWMaxWarps = 16;
+constexpr int kWUnroll = RAFI_W_UNROLL;   // independent unit moves in flight per lane
+constexpr uint32_t kWSmemMax = 227u * 1024u;
+
+// ---------------------------------------------------------------- a2 histogram
+
+constexpr int kHWarps = 8;      // warps per CTA (one CTA per SM)
+constexpr int kHStages = 3;     // TMA ring depth per warp
+constexpr uint32_t kHBlk = kWarpTile * kHistTilesPerCta;  // dests per scan block (2048 = 8 KiB)
+
+__host__ __device__ constexpr uint32_t hist_w_smem(int L) { return kHWarps * (kHStages * kHBlk * 4 + 64) + 8 * (2 * L + 1); }
+
+// Persistent: warp w of CTA x takes scan blocks gw, gw + stride, ... (flat
+// over the local ranks), each streamed into its private kHStages-deep ring by
+// one 8-KiB TMA bulk load.  Scan block b of local rank l = tiles 8b .. 8b+7.
+__global__ void __launch_bounds__(kHWarps * 32, 1) k_hist_w(const RankDev* __restrict__ rk,
+                                                             const CtrlDev* __restrict__ ctrl, int L, int R,
+                                                             uint64_t cap) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* my = smem + (size_t)w * (kHStages * kHBlk * 4 + 64);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(my + kHStages * kHBlk * 4);
+  uint64_t* bpre = reinterpret_cast<uint64_t*>(smem + kHWarps * (kHStages * kHBlk * 4 + 64));  // [L + 1]
+  uint64_t* nl = bpre + (L + 1);
+  if (threadIdx.x == 0) {
+    uint64_t acc = 0;
+    for (int l = 0; l < L; ++l) {
+      const uint64_t n = n_items(ctrl[l], cap);
+      nl[l] = n;
+      bpre[l] = acc;
+      acc += (n + kHBlk - 1) / kHBlk;
+    }
+    bpre[L] = acc;
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kHStages; ++s) mbar_init(&mbar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t total = bpre[L];
+  const uint64_t gw = (uint64_t)blockIdx.x * kHWarps + w, stride = (uint64_t)gridDim.x * kHWarps;
+  auto locate = [&](uint64_t g, int* l) {
+    int x = 0;
+    while (g >= bpre[x + 1]) ++x;
+    *l = x;
+    return g - bpre[x];
+  };
+  auto issue = [&](uint32_t it) {
+    const uint64_t g = gw + (uint64_t)it * stride;
+    if (g >= total) return;
+    int l;
+    const uint64_t i0 = locate(g, &l) * kHBlk;
+    const uint32_t bytes = ((uint32_t)umin64(kHBlk, nl[l] - i0) * 4 + 15) & ~15u;  // queues carry >= 16 B of slack
+    uint64_t* bar = &mbar[it % kHStages];
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(my + (it % kHStages) * kHBlk * 4, rk[l].dest + i0, bytes, bar);
+  };
+  if (lane == 0)
+    for (int s = 0; s < kHStages; ++s) issue(s);
+  for (uint32_t it = 0;; ++it) {
+    const uint64_t g = gw + (uint64_t)it * stride;
+    if (g >= total) break;
+    int l;
+    const uint64_t b = locate(g, &l);
+    const uint64_t n = nl[l];
+    const uint64_t tiles = (n + kWarpTile - 1) / kWarpTile;
+    const uint64_t nblk = (tiles + kHistTilesPerCta - 1) / kHistTilesPerCta;
+    const uint64_t i0 = b * kHBlk;
+    const bool full = i0 + kHBlk <= n;
+    mbar_wait(&mbar[it % kHStages], (it / kHStages) & 1);
+    const int4* d4 = reinterpret_cast<const int4*>(my + (it % kHStages) * kHBlk * 4);
+    // int4 q = 32 i + lane holds dests 4q .. 4q+3, in tile q / 64 = i / 2.
+    // Per tile, byte d of c counts destination d among this lane's 8 dests
+    // (every queued dest is in [0, R), R <= 8: invalid ones were rejected at
+    // emit); then widened to 16-bit fields, even and odd destinations apart:
+    //   word 4t+0: dests 0, 2   4t+1: 4, 6   4t+2: 1, 3   4t+3: 5, 7
+    uint32_t a[32];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      uint64_t c = 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = 2 * t + h;
+        const int4 v = d4[i * 32 + lane];
+        const int e[4] = {v.x, v.y, v.z, v.w};
+        const uint64_t e0 = i0 + (uint64_t)(i * 32 + lane) * 4;
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+          if (full || e0 + m < n) c += 1ull << ((unsigned)e[m] << 3);
+      }
+      const uint64_t ev = c & 0x00FF00FF00FF00FFull, od = (c >> 8) & 0x00FF00FF00FF00FFull;
+      a[4 * t + 0] = (uint32_t)ev;
+      a[4 * t + 1] = (uint32_t)(ev >> 32);
+      a[4 * t + 2] = (uint32_t)od;
+      a[4 * t + 3] = (uint32_t)(od >> 32);
+    }
+    __syncwarp();  // every lane has read the stage
+    if (lane == 0) {
+      fence_proxy_async();
+      issue(it + kHStages);
+    }
+    // butterfly reduce-scatter: at distance s a lane keeps one half of its
+    // words (the upper one if bit s of its lane id is set) and adds its
+    // partner's copy of that half; after s = 16 .. 1, lane j holds the warp
+    // sum of word j
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+      const bool up = (lane & s) != 0;
+#pragma unroll
+      for (int j = 0; j < s; ++j) {
+        const uint32_t send = up ? a[j] : a[j + s];
+        const uint32_t keep = up ? a[j + s] : a[j];
+        a[j] = keep + __shfl_xor_sync(kFull, send, s);
+      }
+    }
+    const uint32_t x = a[0];  // tile 8b + (lane >> 2), word lane & 3: two 16-bit counts (<= 256 each)
+    // prefix over the block's tiles (lanes k, k+4, ..., k+28 share a word)
+    uint32_t inc = x;
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const uint32_t excl = inc - x;  // <= 2048 per field: no carry
+    const uint32_t tot = __shfl_sync(kFull, inc, 28 + (lane & 3));
+    const int k = lane & 3;
+    const uint64_t t = b * kHistTilesPerCta + (lane >> 2);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int d = (k & 1) * 4 + (k >> 1) + 2 * h;
+      if (d < R) {
+        if (t < tiles) rk[l].O[(uint64_t)d * tiles + t] = (excl >> (16 * h)) & 0xffffu;
+        if ((lane >> 2) == kHistTilesPerCta - 1) rk[l].H[(uint64_t)d * nblk + b] = (tot >> (16 * h)) & 0xffffu;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- a4 scatter
+
+// Shared memory of k_scatter_w: `warps` private warp regions, then the CTA's
+// tile map.  Warp region: kWStages x (items, dests), src_of[256] (u16), cnt[R],
+// rs[R + 1] (u32), gb[R] (u64), mbarriers.
+struct WarpLayout {
+  uint32_t stage_items, stage_stride;
+  uint32_t off_src, off_cnt, off_rs, off_gb, off_mbar, per_warp;
+  uint32_t off_cta, total;
+};
+
+static WarpLayout warp_layout(uint64_t B, int R, int L, int warps) {
+  auto al = [](uint64_t x, uint64_t a) { return (uint32_t)((x + a - 1) / a * a); };
+  WarpLayout s;
+  s.stage_items = al((uint64_t)kWarpTile * B, 16);
+  s.stage_stride = al((uint64_t)s.stage_items + 4ull * kWarpTile, 128);
+  uint32_t o = kWStages * s.stage_stride;
+  s.off_src = o; o += 2 * kWarpTile;
+  s.off_cnt = o; o += 4 * R;
+  s.off_rs = o; o = al(o + 4ull * (R + 1), 8);
+  s.off_gb = o; o += 8 * R;
+  s.off_mbar = o; o += 8 * kWStages;
+  s.per_warp = al(o, 128);
+  s.off_cta = s.per_warp * warps;
+  s.total = al(s.off_cta + 8ull * (2 * L + 1), 16);
+  return s;
+}
+
+static int warps_that_fit(uint64_t B, int R, int L) {
+  int w = 0;
+  while (w < kWMaxWarps && warp_layout(B, R, L, w + 1).total <= kWSmemMax) ++w;
+  return w;
+}
+
+template <typename U>
+__global__ void __launch_bounds__(kWMaxWarps * 32, 1)
+k_scatter_w(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint8_t* const* __restrict__ dst_table,
+            const uint64_t* __restrict__ dst_off, const int* __restrict__ ovf, int L, int R, uint64_t cap, int cur,
+            uint32_t B, uint32_t UPI, FastDiv divU, WarpLayout lay, unsigned* __restrict__ wrap_done,
+            CtrlDev* __restrict__ ctrl_w, const uint64_t* __restrict__ wrap_num_in, PeerCtl pc) {
+  if (ovf && *ovf) return;  // collective receive overflow: move nothing (Z3)
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5;
+  // tile map: tpre[l] = first flat tile of local rank l (tpre[L] = all), nl[l] = its items
+  uint64_t* tpre = reinterpret_cast<uint64_t*>(smem + lay.off_cta);
+  uint64_t* nl = tpre + (L + 1);
+  uint8_t* my = smem + (size_t)w * lay.per_warp;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(my + lay.off_mbar);
+  uint16_t* src_of = reinterpret_cast<uint16_t*>(my + lay.off_src);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(my + lay.off_cnt);
+  uint32_t* rs = reinterpret_cast<uint32_t*>(my + lay.off_rs);
+  uintptr_t* gb = reinterpret_cast<uintptr_t*>(my + lay.off_gb);
+  if (threadIdx.x == 0) {
+    uint64_t acc = 0;
+    for (int l = 0; l < L; ++l) {
+      const uint64_t n = n_items(ctrl[l], cap);
+      nl[l] = n;
+      tpre[l] = acc;
+      acc += (n + kWarpTile - 1) / kWarpTile;
+    }
+    tpre[L] = acc;
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kWStages; ++s) mbar_init(&mbar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();  // the only CTA barrier before the epilogue
+  const uint64_t total = tpre[L];
+  const uint64_t gw = (uint64_t)blockIdx.x * W + w, stride = (uint64_t)gridDim.x * W;
+  auto locate = [&](uint64_t g, int* l) {
+    int x = 0;
+    while (g >= tpre[x + 1]) ++x;
+    *l = x;
+    return g - tpre[x];
+  };
+  auto issue = [&](uint32_t it) {  // lane 0: start loading the warp's it-th tile into stage it % kWStages
+    const uint64_t g = gw + (uint64_t)it * stride;
+    if (g >= total) return;
+    int l;
+    const uint64_t t0 = locate(g, &l) * kWarpTile;
+    const uint32_t nt = (uint32_t)umin64(kWarpTile, nl[l] - t0);
+    uint8_t* st = my + (it % kWStages) * lay.stage_stride;
+    uint64_t* bar = &mbar[it % kWStages];
+    const uint32_t bi = (nt * B + 15) & ~15u, bd = (nt * 4 + 15) & ~15u;  // queues carry >= 16 B of slack
+    mbar_expect_tx(bar, bi + bd);
+    bulk_g2s(st, rk[l].out + t0 * B, bi, bar);
+    bulk_g2s(st + lay.stage_items, rk[l].dest + t0, bd, bar);
+  };
+  if (lane == 0)
+    for (int s = 0; s < kWStages; ++s) issue(s);
+
+  // lane d < R: global start of destination d's run in the warp's it-th tile
+  // -- prefix over earlier tiles (O within the scan block + H over blocks)
+  // plus the per-destination base from the plan -- and d's queue.  Fetched one
+  // tile ahead, so these dependent global loads are in flight while the
+  // current tile is ranked and written.
+  // (The three terms stay apart until the next iteration adds them: an add
+  // here would stall the warp on the loads right away.)
+  struct RunBase {
+    uint32_t o, h;
+    uint64_t off;
+    uintptr_t db;
+  };
+  auto fetch = [&](uint32_t it, RunBase* r) {
+    const uint64_t g = gw + (uint64_t)it * stride;
+    if (g >= total || lane >= R) return;
+    int l;
+    const uint64_t t = locate(g, &l);
+    const uint64_t tiles = tpre[l + 1] - tpre[l];
+    const uint64_t nblk = (tiles + kHistTilesPerCta - 1) / kHistTilesPerCta;
+    r->o = rk[l].O[(uint64_t)lane * tiles + t];
+    r->h = rk[l].H[(uint64_t)lane * nblk + t / kHistTilesPerCta];
+    r->off = dst_off[(uint64_t)l * R + lane];
+    r->db = reinterpret_cast<uintptr_t>(dst_table ? dst_table[lane] : rk[l].binned[cur]);
+  };
+  RunBase nxt{0u, 0u, 0ull, 0};
+  fetch(0, &nxt);
+
+  for (uint32_t it = 0;; ++it) {
+    const uint64_t g = gw + (uint64_t)it * stride;
+    if (g >= total) break;
+    int l;
+    const uint64_t t = locate(g, &l);
+    const uint32_t nt = (uint32_t)umin64(kWarpTile, nl[l] - t * kWarpTile);
+    const RunBase cur_rb = nxt;
+    fetch(it + 1, &nxt);
+    if (lane < R) cnt[lane] = 0;
+    __syncwarp();
+    const uint32_t s = it % kWStages;
+    mbar_wait(&mbar[s], (it / kWStages) & 1);
+    const uint8_t* st = my + s * lay.stage_stride;
+    const int32_t* dest_s = reinterpret_cast<const int32_t*>(st + lay.stage_items);
+    // rank: item 32k + lane gets its rank among the tile's earlier items with
+    // the same destination (stable in slot order)
+    int dk[kWK];
+    uint32_t rnk[kWK];
+#pragma unroll
+    for (int k = 0; k < kWK; ++k) {
+      const uint32_t il = k * 32 + lane;
+      const int d = il < nt ? dest_s[il] : R;
+      const unsigned m = __match_any_sync(kFull, d);
+      const uint32_t c = d < R ? cnt[d] : 0u;
+      __syncwarp();
+      if (d < R && lane == __ffs(m) - 1) cnt[d] = c + __popc(m);
+      __syncwarp();
+      dk[k] = d;
+      rnk[k] = c + __popc(m & lanemask_lt());
+    }
+    // run starts in the tile (exclusive scan over destinations; rs[R] = nt)
+    // and the run bases: position p of run d goes to gb[d] + p * B
+    const uint32_t mine = lane < R ? cnt[lane] : 0u;
+    uint32_t inc = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const uint32_t excl = inc - mine;
+    if (lane <= R) rs[lane] = excl;
+    if (lane < R) gb[lane] = cur_rb.db + (uintptr_t)((uint64_t)cur_rb.o + cur_rb.h + cur_rb.off - excl) * B;
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kWK; ++k)
+      if (dk[k] < R) src_of[rs[dk[k]] + rnk[k]] = (uint16_t)(k * 32 + lane);
+    __syncwarp();
+    // destination-major unit moves: lane x of 32 consecutive units, so every
+    // run is written with coalesced stores; a lane's position only grows, so
+    // its current run only moves forward
+    const U* sU = reinterpret_cast<const U*>(st);
+    const uint32_t units = nt * UPI;
+    int d = 0;
+    uint32_t nb = rs[1];
+    uintptr_t base = gb[0];
+    for (uint32_t x0 = lane; x0 < units; x0 += 32 * kWUnroll) {
+      U v[kWUnroll];
+      uint32_t p[kWUnroll], u[kWUnroll];
+#pragma unroll
+      for (int j = 0; j < kWUnroll; ++j) {
+        const uint32_t x = x0 + 32 * j;
+        p[j] = divU.div(x);
+        u[j] = x - p[j] * UPI;
+        if (x < units) v[j] = sU[(uint32_t)src_of[p[j]] * UPI + u[j]];
+      }
+#pragma unroll
+      for (int j = 0; j < kWUnroll; ++j) {
+        if (x0 + 32 * j < units) {
+          while (p[j] >= nb) {
+            ++d;
+            nb = rs[d + 1];
+            base = gb[d];
+          }
+          RAFI_DCHECK(d < R, "warp scatter: position beyond the last run");
+          reinterpret_cast<U*>(base + (uintptr_t)p[j] * B)[u[j]] = v[j];
+        }
+      }
+    }
+    __syncwarp();  // every lane is done with this stage
+    if (lane == 0) {
+      fence_proxy_async();  // order the generic-proxy reads before the async refill
+      issue(it + kWStages);
+    }
+  }
+  if (dst_table) __threadfence_system();  // pushes to peer memory complete before the kernel does
+  // wrap-up epilogue by the last CTA: every CTA has finished
+  // reading the emit counters, so they can be reset for the next round
+  if (wrap_done && last_block(wrap_done)) {
+    for (int l2 = threadIdx.x; l2 < L; l2 += blockDim.x) {
+      ctrl_w[l2].ctr = 0;
+      ctrl_w[l2].invalid = 0;
+      ctrl_w[l2].num_in = wrap_num_in[l2];
+    }
+    if (pc.mbox) ctl_barrier_block(pc);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+
+bool warp_tiles_ok(uint64_t B, int R, int L) { return R <= 8 && B % 8 == 0 && warps_that_fit(B, R, L) >= 2; }
+
+int launch_hist_w(Ctx* c, int nsm) {
+  const uint32_t sm = hist_w_smem(c->L);
+  static uint32_t granted = 0;
+  if (sm > granted) {
+    RAFI_CK_CUDA(cudaFuncSetAttribute(k_hist_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    granted = sm;
+  }
+  const uint64_t blocks = (c->max_tiles + kHistTilesPerCta - 1) / kHistTilesPerCta * (uint64_t)c->L;
+  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)nsm, (blocks + kHWarps - 1) / kHWarps));
+  k_hist_w<<<grid, kHWarps * 32, sm, c->stream>>>(c->rank_dev, c->ctrl, c->L, c->R, c->cap);
+  RAFI_CK_CUDA(cudaGetLastError());
+  return RAFI_OK;
+}
+
+template <typename U>
+static int launch_w(Ctx* c, bool fused, bool wrap, PeerCtl pc, int nsm) {
+  const int warps = warps_that_fit(c->B, c->R, c->L);
+  const WarpLayout lay = warp_layout(c->B, c->R, c->L, warps);
+  static int granted = 0;
+  auto k = k_scatter_w<U>;
+  if ((int)lay.total > granted) {
+    RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
+    granted = (int)lay.total;
+  }
+  const uint32_t UPI = (uint32_t)(c->B / sizeof(U));
+  const uint64_t tiles_all = c->max_tiles * (uint64_t)c->L;
+  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)nsm, (tiles_all + warps - 1) / warps));
+  k<<<grid, 32 * warps, lay.total, c->stream>>>(c->rank_dev, c->ctrl, fused ? c->in_table_dev : nullptr, c->off_dev,
+                                               fused ? c->ovf_dev : nullptr, c->L, c->R, c->cap, c->cur,
+                                               (uint32_t)c->B, UPI, FastDiv(UPI), lay, wrap ? c->done_dev + 1 : nullptr,
+                                               c->ctrl, c->plan_dev, pc);
+  RAFI_CK_CUDA(cudaGetLastError());
+  return RAFI_OK;
+}
+
+int launch_scatter_w(Ctx* c, bool fused, bool wrap, PeerCtl pc, int nsm) {
+  if (c->B % 16 == 0) return launch_w<uint4>(c, fused, wrap, pc, nsm);
+  return launch_w<uint2>(c, fused, wrap, pc, nsm);
+}
+
+}  // namespace rafi_impl
