@@ -186,8 +186,9 @@ __global__ void __launch_bounds__(kHWarps * 32, 1) k_hist_w(const RankDev* __res
 // ---------------------------------------------------------------- a4 scatter
 
 // Shared memory of k_scatter_w: `warps` private warp regions, then the CTA's
-// tile map.  Warp region: kWStages x (items, dests), src_of[256] (u16), cnt[R],
-// rs[R + 1] (u32), gb[R] (u64), mbarriers.
+// tile map.  Warp region: kWStages x (items, dests), src_of[256] (u16), the
+// chunk x destination table T[8][8] (u32), rs[R + 1] (u32), gb[R] (u64),
+// mbarriers.
 struct WarpLayout {
   uint32_t stage_items, stage_stride;
   uint32_t off_src, off_cnt, off_rs, off_gb, off_mbar, per_warp;
@@ -201,7 +202,7 @@ static WarpLayout warp_layout(uint64_t B, int R, int L, int warps) {
   s.stage_stride = al((uint64_t)s.stage_items + 4ull * kWarpTile, 128);
   uint32_t o = kWStages * s.stage_stride;
   s.off_src = o; o += 2 * kWarpTile;
-  s.off_cnt = o; o += 4 * R;
+  s.off_cnt = o; o += 4 * kWK * 8;
   s.off_rs = o; o = al(o + 4ull * (R + 1), 8);
   s.off_gb = o; o += 8 * R;
   s.off_mbar = o; o += 8 * kWStages;
@@ -215,6 +216,15 @@ static int warps_that_fit(uint64_t B, int R, int L) {
   int w = 0;
   while (w < kWMaxWarps && warp_layout(B, R, L, w + 1).total <= kWSmemMax) ++w;
   return w;
+}
+
+// Unit stores into a destination queue (local HBM or a CUDA-IPC peer
+// mapping: both in the global window), issued as STG rather than generic ST.
+__device__ __forceinline__ void st_global(uint4* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ void st_global(uint2* p, const uint2& v) {
+  asm volatile("st.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
 }
 
 template <typename U>
@@ -232,7 +242,7 @@ k_scatter_w(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, ui
   uint8_t* my = smem + (size_t)w * lay.per_warp;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(my + lay.off_mbar);
   uint16_t* src_of = reinterpret_cast<uint16_t*>(my + lay.off_src);
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(my + lay.off_cnt);
+  uint32_t* T = reinterpret_cast<uint32_t*>(my + lay.off_cnt);  // [chunk k][destination e]
   uint32_t* rs = reinterpret_cast<uint32_t*>(my + lay.off_rs);
   uintptr_t* gb = reinterpret_cast<uintptr_t*>(my + lay.off_gb);
   if (threadIdx.x == 0) {
@@ -251,31 +261,45 @@ k_scatter_w(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, ui
     fence_mbar_init();
   }
   __syncthreads();  // the only CTA barrier before the epilogue
-  const uint64_t total = tpre[L];
   const uint64_t gw = (uint64_t)blockIdx.x * W + w, stride = (uint64_t)gridDim.x * W;
-  auto locate = [&](uint64_t g, int* l) {
-    int x = 0;
-    while (g >= tpre[x + 1]) ++x;
-    *l = x;
-    return g - tpre[x];
-  };
-  auto issue = [&](uint32_t it) {  // lane 0: start loading the warp's it-th tile into stage it % kWStages
-    const uint64_t g = gw + (uint64_t)it * stride;
-    if (g >= total) return;
+  // The warp's tiles are gw, gw + stride, ... (flat over the local ranks); a
+  // cursor walks them with a monotone local-rank search.  Three cursors: the
+  // TMA loads (kWStages ahead), the run-base fetch (one ahead), the tile.
+  struct Cursor {
+    uint64_t g;
     int l;
-    const uint64_t t0 = locate(g, &l) * kWarpTile;
-    const uint32_t nt = (uint32_t)umin64(kWarpTile, nl[l] - t0);
-    uint8_t* st = my + (it % kWStages) * lay.stage_stride;
-    uint64_t* bar = &mbar[it % kWStages];
-    const uint32_t bi = (nt * B + 15) & ~15u, bd = (nt * 4 + 15) & ~15u;  // queues carry >= 16 B of slack
-    mbar_expect_tx(bar, bi + bd);
-    bulk_g2s(st, rk[l].out + t0 * B, bi, bar);
-    bulk_g2s(st + lay.stage_items, rk[l].dest + t0, bd, bar);
+  };
+  auto seek = [&](Cursor& c) {
+    while (c.l < L && c.g >= tpre[c.l + 1]) ++c.l;
+  };
+  auto advance = [&](Cursor& c) {
+    c.g += stride;
+    seek(c);
+  };
+  Cursor ci{gw, 0}, cf{gw, 0}, ct{gw, 0};
+  seek(ci);
+  seek(cf);
+  seek(ct);
+  uint32_t n_issued = 0;
+  auto issue = [&]() {  // lane 0: start loading the tile at ci into stage n_issued % kWStages
+    if (ci.l < L) {
+      const int l = ci.l;
+      const uint64_t t0 = (ci.g - tpre[l]) * kWarpTile;
+      const uint32_t nt = (uint32_t)umin64(kWarpTile, nl[l] - t0);
+      uint8_t* st = my + (n_issued % kWStages) * lay.stage_stride;
+      uint64_t* bar = &mbar[n_issued % kWStages];
+      const uint32_t bi = (nt * B + 15) & ~15u, bd = (nt * 4 + 15) & ~15u;  // queues carry >= 16 B of slack
+      mbar_expect_tx(bar, bi + bd);
+      bulk_g2s(st, rk[l].out + t0 * B, bi, bar);
+      bulk_g2s(st + lay.stage_items, rk[l].dest + t0, bd, bar);
+    }
+    ++n_issued;
+    advance(ci);
   };
   if (lane == 0)
-    for (int s = 0; s < kWStages; ++s) issue(s);
+    for (int s = 0; s < kWStages; ++s) issue();
 
-  // lane d < R: global start of destination d's run in the warp's it-th tile
+  // lane d < R: global start of destination d's run in the cursor's tile
   // -- prefix over earlier tiles (O within the scan block + H over blocks)
   // plus the per-destination base from the plan -- and d's queue.  Fetched one
   // tile ahead, so these dependent global loads are in flight while the
@@ -287,67 +311,83 @@ k_scatter_w(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, ui
     uint64_t off;
     uintptr_t db;
   };
-  auto fetch = [&](uint32_t it, RunBase* r) {
-    const uint64_t g = gw + (uint64_t)it * stride;
-    if (g >= total || lane >= R) return;
-    int l;
-    const uint64_t t = locate(g, &l);
-    const uint64_t tiles = tpre[l + 1] - tpre[l];
-    const uint64_t nblk = (tiles + kHistTilesPerCta - 1) / kHistTilesPerCta;
-    r->o = rk[l].O[(uint64_t)lane * tiles + t];
-    r->h = rk[l].H[(uint64_t)lane * nblk + t / kHistTilesPerCta];
-    r->off = dst_off[(uint64_t)l * R + lane];
-    r->db = reinterpret_cast<uintptr_t>(dst_table ? dst_table[lane] : rk[l].binned[cur]);
+  auto fetch = [&](RunBase* r) {
+    if (cf.l < L && lane < R) {
+      const int l = cf.l;
+      const uint64_t t = cf.g - tpre[l];
+      const uint64_t tiles = tpre[l + 1] - tpre[l];
+      const uint64_t nblk = (tiles + kHistTilesPerCta - 1) / kHistTilesPerCta;
+      r->o = rk[l].O[(uint64_t)lane * tiles + t];
+      r->h = rk[l].H[(uint64_t)lane * nblk + t / kHistTilesPerCta];
+      r->off = dst_off[(uint64_t)l * R + lane];
+      r->db = reinterpret_cast<uintptr_t>(dst_table ? dst_table[lane] : rk[l].binned[cur]);
+    }
+    advance(cf);
   };
   RunBase nxt{0u, 0u, 0ull, 0};
-  fetch(0, &nxt);
+  fetch(&nxt);
 
-  for (uint32_t it = 0;; ++it) {
-    const uint64_t g = gw + (uint64_t)it * stride;
-    if (g >= total) break;
-    int l;
-    const uint64_t t = locate(g, &l);
+  for (uint32_t it = 0; ct.l < L; ++it, advance(ct)) {
+    const int l = ct.l;
+    const uint64_t t = ct.g - tpre[l];
     const uint32_t nt = (uint32_t)umin64(kWarpTile, nl[l] - t * kWarpTile);
     const RunBase cur_rb = nxt;
-    fetch(it + 1, &nxt);
-    if (lane < R) cnt[lane] = 0;
+    fetch(&nxt);
+    T[lane] = 0;
+    T[lane + 32] = 0;
     __syncwarp();
     const uint32_t s = it % kWStages;
     mbar_wait(&mbar[s], (it / kWStages) & 1);
     const uint8_t* st = my + s * lay.stage_stride;
     const int32_t* dest_s = reinterpret_cast<const int32_t*>(st + lay.stage_items);
-    // rank: item 32k + lane gets its rank among the tile's earlier items with
-    // the same destination (stable in slot order)
+    // rank (stable in slot order): item 32k + lane (chunk k)
+    // goes to tile position T[k][d] + (earlier lanes of chunk k with the same
+    // destination d), where T[k][d] = start of run d in the tile + items with
+    // destination d in chunks 0 .. k-1.  Three warp-synchronous steps, no
+    // serial chain over the chunks: the chunk leaders publish their group
+    // sizes, lane e (< R) scans destination e over the chunks, the run starts
+    // come from a shuffle scan over the destinations.
     int dk[kWK];
-    uint32_t rnk[kWK];
+    unsigned mk[kWK];
+    uint32_t before[kWK];
 #pragma unroll
     for (int k = 0; k < kWK; ++k) {
       const uint32_t il = k * 32 + lane;
-      const int d = il < nt ? dest_s[il] : R;
-      const unsigned m = __match_any_sync(kFull, d);
-      const uint32_t c = d < R ? cnt[d] : 0u;
-      __syncwarp();
-      if (d < R && lane == __ffs(m) - 1) cnt[d] = c + __popc(m);
-      __syncwarp();
-      dk[k] = d;
-      rnk[k] = c + __popc(m & lanemask_lt());
+      dk[k] = il < nt ? dest_s[il] : R;
+      mk[k] = __match_any_sync(kFull, dk[k]);
+      before[k] = __popc(mk[k] & lanemask_lt());
     }
-    // run starts in the tile (exclusive scan over destinations; rs[R] = nt)
-    // and the run bases: position p of run d goes to gb[d] + p * B
-    const uint32_t mine = lane < R ? cnt[lane] : 0u;
-    uint32_t inc = mine;
+#pragma unroll
+    for (int k = 0; k < kWK; ++k)
+      if (dk[k] < R && before[k] == 0) T[k * 8 + dk[k]] = __popc(mk[k]);
+    __syncwarp();
+    uint32_t pre[kWK];
+    uint32_t tot = 0;
+    if (lane < R) {
+#pragma unroll
+      for (int k = 0; k < kWK; ++k) {
+        pre[k] = tot;
+        tot += T[k * 8 + lane];
+      }
+    }
+    uint32_t inc = tot;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(kFull, inc, o);
       if (lane >= o) inc += y;
     }
-    const uint32_t excl = inc - mine;
+    const uint32_t excl = inc - tot;  // run start of destination lane (rs[R] = nt)
     if (lane <= R) rs[lane] = excl;
-    if (lane < R) gb[lane] = cur_rb.db + (uintptr_t)((uint64_t)cur_rb.o + cur_rb.h + cur_rb.off - excl) * B;
+    if (lane < R) {
+      // position p of run d goes to gb[d] + p * B
+      gb[lane] = cur_rb.db + (uintptr_t)((uint64_t)cur_rb.o + cur_rb.h + cur_rb.off - excl) * B;
+#pragma unroll
+      for (int k = 0; k < kWK; ++k) T[k * 8 + lane] = excl + pre[k];
+    }
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < kWK; ++k)
-      if (dk[k] < R) src_of[rs[dk[k]] + rnk[k]] = (uint16_t)(k * 32 + lane);
+      if (dk[k] < R) src_of[T[k * 8 + dk[k]] + before[k]] = (uint16_t)(k * 32 + lane);
     __syncwarp();
     // destination-major unit moves: lane x of 32 consecutive units, so every
     // run is written with coalesced stores; a lane's position only grows, so
@@ -376,14 +416,14 @@ k_scatter_w(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, ui
             base = gb[d];
           }
           RAFI_DCHECK(d < R, "warp scatter: position beyond the last run");
-          reinterpret_cast<U*>(base + (uintptr_t)p[j] * B)[u[j]] = v[j];
+          st_global(reinterpret_cast<U*>(base + (uintptr_t)p[j] * B) + u[j], v[j]);
         }
       }
     }
     __syncwarp();  // every lane is done with this stage
     if (lane == 0) {
       fence_proxy_async();  // order the generic-proxy reads before the async refill
-      issue(it + kWStages);
+      issue();
     }
   }
   if (dst_table) __threadfence_system();  // pushes to peer memory complete before the kernel does
