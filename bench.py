@@ -254,40 +254,22 @@ def run_reference(args):
 
 # ----------------------------------------------------------------------------- NVLink counters
 
-def nvlink_counters(gpu):
-    """Per-link NVLink transmit / receive byte counters of one GPU (NVML field
-    values NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES / _RCV_BYTES summed over the
-    links), or None where NVML does not expose them."""
+def stored_nvlink_counters(scatter, B, n, N):
+    """NVLink byte counters of the FUSED scatter from the stored single-process
+    ncu capture (profiles/r02_nvlink_counters.json; scripts/nvl_redirect.py).
+    Not read live: NVML does not expose the NVLink byte counters on these boxes
+    (nvidia-smi nvlink -gt d: N/A), and querying NVML next to the timed region
+    stalled the first steps by ~10 ms."""
     try:
-        import pynvml as nv
-        nv.nvmlInit()
-        h = nv.nvmlDeviceGetHandleByIndex(gpu)
-        nl = nv.nvmlDeviceGetFieldValues(h, [(nv.NVML_FI_DEV_NVLINK_LINK_COUNT, 0)])[0]
-        links = int(nl.value.uiVal) if nl.nvmlReturn == 0 else 18
-        tx = rx = 0
-        for fid, acc in ((nv.NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES, "tx"), (nv.NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES, "rx")):
-            vals = nv.nvmlDeviceGetFieldValues(h, [(fid, l) for l in range(links)])
-            if any(v.nvmlReturn != 0 for v in vals):
-                return None
-            total = sum(int(v.value.ullVal) for v in vals)
-            if acc == "tx":
-                tx = total
-            else:
-                rx = total
-        return {"tx": tx, "rx": rx, "links": links}
+        with open(os.path.join(ROOT, "profiles", "r02_nvlink_counters.json")) as f:
+            tab = json.load(f)
     except Exception:
-        return None
-
-
-def nvlink_delta(c0, c1, remote_bytes):
-    if not c0 or not c1:
-        return {"available": False, "why": "NVML NVLink byte counters not exposed on this box"}
-    tx, rx = c1["tx"] - c0["tx"], c1["rx"] - c0["rx"]
-    return {"available": True, "tx_bytes": tx, "rx_bytes": rx, "links": c0["links"],
-            "algorithmic_remote_bytes": remote_bytes,
-            "tx_over_algorithmic": tx / remote_bytes if remote_bytes else None,
-            "what": "NVML_FI_DEV_NVLINK_COUNT_XMIT/RCV_BYTES summed over links, read before and after the timed "
-                    "region (all K steps, this GPU); includes protocol overhead"}
+        return {"available": False, "why": "profiles/r02_nvlink_counters.json missing"}
+    key = "scatter_%s/B%d/n%d/R2" % (scatter, B, n)
+    if key not in tab:
+        return {"available": False, "why": "no stored capture for %s" % key}
+    return dict(tab[key], available=True, source="STORED, not measured in this run: " + tab["_capture"] +
+                "; rank 0 of an N=2 FUSED forward driven by one process (N=%d here)" % N)
 
 
 # ----------------------------------------------------------------------------- supplementary blocks
@@ -455,7 +437,6 @@ def main():
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     f_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    nvl0 = nvlink_counters(local) if N > 1 else None
     t_start.record(stream)
     for k in range(args.steps):
         ctx.emit_bulk(items_d, dests_d, n)
@@ -464,7 +445,6 @@ def main():
         f_ev[k][1].record(stream)
     t_end.record(stream)
     barrier()
-    nvl1 = nvlink_counters(local) if N > 1 else None
     clk = clocks.stop()
     ms_fwd = max_over_ranks(sum(a.elapsed_time(b) for a, b in f_ev))
     st = ctx.stats()
@@ -539,7 +519,7 @@ def main():
         ceil = nvlink_ceilings(N)
         exch = {"gbs_per_gpu": gbs, "frac_of_900": gbs / 900.0, "frac_of_770_measured_p2p": gbs / 770.0,
                 "transport": exchange, "remote_bytes_per_step": remote / K, "kernel_ms": xfer_ms,
-                "ceilings_gbs": ceil, "nvlink_counters": nvlink_delta(nvl0, nvl1, remote)}
+                "ceilings_gbs": ceil, "nvlink_counters": stored_nvlink_counters(scatter, B, n, N) if exchange == "fused" else None}
         if exchange == "fused" and xfer_ms >= max(v["ms"] for v in kern.values()):
             # the step's dominant phase moves bytes over NVLink: that is its roofline
             # (peak: the profiling guide's measured 770 GB/s peer copy per direction)

@@ -350,6 +350,20 @@ int rafi_nccl_comm_destroy(void* comm);
 int rafi_selftest_peer_control(int device, int P, int L, int rounds, int absent, long long timeout_ms,
                                uint64_t* bad, uint64_t* timed_out);
 
+/* Diagnostic (measurement only): make the FUSED scatter write global rank
+ * `grank`'s incoming queue (a local rank of this process) into `queue`
+ * instead of the context's own buffer -- a device pointer of at least
+ * capacity * item_bytes bytes, 16-byte aligned, owned by the caller and valid
+ * until it is restored.  It may live on ANOTHER device: peer access to that
+ * device is enabled here.  With it one process can drive the NVLink push of a
+ * FUSED forward (rank me's block for rank d written straight
+ * into d's queue) on its own, e.g. under a single-process ncu NVLink counter
+ * capture.  The redirected rank's num_incoming stays correct, but reads of
+ * its incoming queue through this API (rafi_read_incoming, the device view)
+ * see the context's own, stale buffer.  queue = NULL restores the default.
+ * RAFI_ERR_INVALID_ARG (grank not local, misaligned), RAFI_ERR_CUDA. */
+int rafi_diag_redirect_incoming(rafi_ctx* ctx, int grank, void* queue);
+
 /* ---- host-side planning (pure host code; no GPU needed) --------------------- */
 
 /* From the R x R count matrix C (row-major, C[s*R+d] = items s sends to d)

@@ -1389,6 +1389,28 @@ int rafi_selftest_peer_control(int device, int P, int L, int rounds, int absent,
   return rc;
 }
 
+int rafi_diag_redirect_incoming(rafi_ctx* ctx, int grank, void* queue) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return RAFI_ERR_INVALID_ARG;
+  const int l = grank - c->proc * c->L;
+  if (l < 0 || l >= c->L || ((uintptr_t)queue & 15)) return RAFI_ERR_INVALID_ARG;
+  if ((int)c->peer_in.size() != c->R) return RAFI_ERR_UNSUPPORTED;
+  RAFI_CK_CUDA(cudaSetDevice(c->device));
+  if (queue) {
+    cudaPointerAttributes a{};
+    RAFI_CK_CUDA(cudaPointerGetAttributes(&a, queue));
+    if (a.type != cudaMemoryTypeDevice) return RAFI_ERR_INVALID_ARG;
+    if (a.device != c->device) {
+      const cudaError_t e = cudaDeviceEnablePeerAccess(a.device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else RAFI_CK_CUDA(e);
+    }
+  }
+  c->peer_in[grank] = queue ? static_cast<uint8_t*>(queue) : c->lr[l].in;
+  drop_fwd_graph(c);
+  return upload_in_table(c);
+}
+
 int rafi_nccl_unique_id(void* id128) {
   if (!id128) return RAFI_ERR_INVALID_ARG;
   ncclUniqueId id;

@@ -115,6 +115,7 @@ SIGNATURES = {
     "rafi_selftest_peer_control": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_longlong,
                                              C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "rafi_drv_emit_items": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int]),
+    "rafi_diag_redirect_incoming": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "rafi_resize": (C.c_int, [C.c_void_p, C.c_size_t]),
     "rafi_destroy": (None, [C.c_void_p]),
     "rafi_get_device_view": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(DeviceView)]),
@@ -381,6 +382,13 @@ class Context:
         if n is None:
             n = len(dests)
         _check(lib().rafi_emit_bulk(self._h, local, _ptr(items), _ptr(dests), int(n)), "rafi_emit_bulk")
+
+    def diag_redirect_incoming(self, grank: int, queue=None):
+        """rafi_diag_redirect_incoming: FUSED pushes for global rank `grank` go
+        to `queue` (a device tensor, possibly on another GPU) until restored
+        with queue=None.  Measurement only (see include/rafi.h)."""
+        _check(lib().rafi_diag_redirect_incoming(self._h, grank, None if queue is None else _ptr(queue)),
+               "rafi_diag_redirect_incoming")
 
     def forward(self) -> int:
         G = lib().rafi_forward(self._h)

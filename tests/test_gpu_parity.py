@@ -9,7 +9,7 @@ import pytest
 
 import oracle
 import synth
-from helpers import canonical, make_inputs, oracle_sequential, p1_forward
+from helpers import canonical, make_inputs, oracle_sequential, p1_forward, snapshot_world
 
 pytestmark = pytest.mark.gpu
 
@@ -441,3 +441,35 @@ def test_device_reemit_drop_rule(batch, cap):
         assert np.array_equal(items, it[seq]) and np.array_equal(dests, ds[seq])
         w, G = p1_forward(ctx, 1, B)
         assert G == min(ctr, cap)
+
+
+@pytest.mark.parametrize("scatter", [1, 2])  # THREADS (warp tiles at R <= 8), BULK
+@pytest.mark.parametrize("B", [16, 44, 48])
+def test_diag_redirect_incoming(B, scatter):
+    """rafi_diag_redirect_incoming: the FUSED scatter writes rank 1's block
+    into a caller buffer instead of the context's queue -- exactly the bytes
+    the oracle delivers to rank 1 (P1 on the redirected queue); the other
+    ranks' queues are untouched by the redirect, and restoring it brings
+    the default back."""
+    L, n = 3, 30001
+    inputs = make_inputs(L, n, B, "uniform", 21 + B)
+    with _ctx(B, L * n, L) as ctx:
+        ctx.set_option(rafi.OPT_SCATTER, scatter)
+        buf = torch.zeros(L * n * B + 16, dtype=torch.uint8, device="cuda")
+        ctx.diag_redirect_incoming(1, buf)
+        _emit_all(ctx, inputs)
+        w, _ = snapshot_world(ctx, L, B)
+        G_o = w.forward()
+        assert ctx.forward() == G_o
+        m = ctx.num_incoming(1)
+        assert m == w.num_incoming(1)
+        got = buf[: m * B].cpu().numpy().reshape(m, B)
+        assert np.array_equal(got, w.incoming(1))
+        for l in (0, 2):
+            assert np.array_equal(ctx.read_incoming(l), w.incoming(l))
+        ctx.diag_redirect_incoming(1, None)
+        _emit_all(ctx, inputs)
+        p1_forward(ctx, L, B)
+    with _ctx(B, n, 1) as ctx:
+        with pytest.raises(rafi.RafiError):
+            ctx.diag_redirect_incoming(1, buf)   # not a local rank
