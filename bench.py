@@ -4,17 +4,20 @@
     (N > 1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N)
 
 One STEP = one pass of the whole hot path over one batch per rank:
-  a1 emit (rafi_emit_bulk of the rank's resident batch), then rafi_forward:
+  a1 emit (rafi_emit_bulk of every rank's resident batch), then rafi_forward:
   a2 histogram, a3 scan, a4 stable scatter, a5 count exchange, a6 payload
   exchange, a7 wrap-up, a8 termination count.
-Workload (BASELINE.json configs[1] per-rank shape, weak scaling): every rank
-holds 16,777,216 synthetic 48-byte items (the FWDRay shape)
-with uniformly random destinations over R = N ranks.  Inputs are resident in
-HBM before the timed region (768 MiB per rank > 126 MB L2, so no L2 reuse
-between steps).  value = items all ranks forwarded / max-over-ranks device
-time.  e2e = the same metric through the C ABI with HOST buffers: each step
-copies the batch in from pinned memory (inside rafi_emit_bulk) and reads the
-incoming queue back to pinned memory.
+Workload: BASELINE.json configs[1] itself -- 8 ranks, 16,777,216 synthetic
+48-byte items per rank (the FWDRay shape), uniformly random
+destinations over the 8 ranks, one forward.  On N GPUs each GPU hosts 8/N of
+the ranks as logical ranks of one context (N=1: the whole 8-rank world on
+one B200; N=8: one rank per GPU), so the total work is fixed (strong
+scaling).  Inputs are resident in HBM before the timed region (805 MB of
+items per rank > 126 MB L2, so no L2 reuse between steps).  value = items
+all ranks forwarded / max-over-ranks device time.  e2e = the same metric
+through the C ABI with HOST buffers: each step copies the batches in from
+pinned memory (inside rafi_emit_bulk) and reads the incoming queues back to
+pinned memory.
 """
 from __future__ import annotations
 
@@ -34,6 +37,7 @@ import numpy as np  # noqa: E402
 
 DEF_N = 16 * 1024 * 1024
 DEF_B = 48
+DEF_R = 8  # configs[1]: 8 ranks
 METRIC = "forwarded work items/sec"
 
 
@@ -44,6 +48,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="rafi", choices=["rafi", "reference"])
     p.add_argument("--items", type=int, default=DEF_N, help="items per rank per step")
+    p.add_argument("--ranks", type=int, default=DEF_R, help="ranks R of the world (split evenly over the GPUs)")
     p.add_argument("--item-bytes", type=int, default=DEF_B)
     p.add_argument("--pattern", default="uniform")
     p.add_argument("--exchange", default="auto", choices=["auto", "nccl", "peer", "fused"])
@@ -52,7 +57,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-graph", action="store_true", help="skip the supplementary graph-replay measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--no-extras", action="store_true", help="skip the binning_r8 and device_emit blocks")
+    p.add_argument("--no-extras", action="store_true", help="skip the device_emit block")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle cpu_baseline sample")
     return p.parse_args()
 
@@ -76,20 +81,29 @@ def nvlink_ceilings(N):
 
 
 def workload_config(args, N):
+    R = args.ranks
     return {
-        "workload": "cfg2 per-rank shape: %d x %d-B items/rank, %s dest over R=%d ranks, 1 forward/step"
-                    % (args.items, args.item_bytes, args.pattern, N),
-        "items_per_rank": args.items, "item_bytes": args.item_bytes, "ranks": N, "pattern": args.pattern,
-        "l2": "inputs larger than L2 (%.0f MiB/rank resident)" % (args.items * (args.item_bytes + 4) / 2**20),
-        "step": "emit_bulk + forward (hist, scan, scatter, count exchange, payload exchange, wrap-up)",
-        "parallelism": "one rank per GPU" if N > 1 else "single GPU",
+        "workload": "configs[1]%s: %d ranks x %d x %d-B items/rank, %s dest over the %d ranks, 1 forward/step"
+                    % ("" if (R, args.items, args.item_bytes, args.pattern) == (DEF_R, DEF_N, DEF_B, "uniform")
+                       else " (modified)", R, args.items, args.item_bytes, args.pattern, R),
+        "items_per_rank": args.items, "item_bytes": args.item_bytes, "ranks": R, "pattern": args.pattern,
+        "ranks_per_gpu": R // N,
+        "l2": "inputs larger than L2 (%.0f MiB per rank resident)" % (args.items * (args.item_bytes + 4) / 2**20),
+        "step": "emit_bulk of every rank + forward (hist, scan, scatter, count exchange, payload exchange, wrap-up)",
+        "parallelism": "%d GPU%s x %d logical rank%s" % (N, "s" if N > 1 else "", R // N, "s" if R // N > 1 else ""),
     }
 
 
 # ----------------------------------------------------------------------------- clocks
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle sampling during the timed region."""
+    """nvidia-smi clocks/throttle sampling during the timed region.
+
+    Started before the warm-up: nvidia-smi's start-up (NVML init) takes the
+    driver's locks for ~0.1-0.3 s, and when it overlapped the ~15-ms timed
+    region it stalled every rank's CUDA calls (N=4: 1.41 vs 1.32 ms per step).
+    Samples are taken every 100 ms and kept when they fall within 150 ms of
+    the timed region (the nearest one if none does)."""
     FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.active", "clocks_event_reasons.hw_slowdown",
               "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
               "clocks_event_reasons.sw_power_cap"]
@@ -98,6 +112,11 @@ class ClockSampler:
         self.gpu = gpu_index
         self.proc = None
         self.lines = []
+        self.window = None
+
+    def mark(self, t0, t1):
+        """Wall-clock bounds (time.perf_counter) of the timed region."""
+        self.window = (t0, t1)
 
     def start(self):
         try:
@@ -107,12 +126,15 @@ class ClockSampler:
                 text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t_end = time.perf_counter() + 5.0  # the first sample = nvidia-smi is past its start-up
+            while not self.lines and time.perf_counter() < t_end and self.proc.poll() is None:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
 
     def stop(self):
         if not self.proc:
@@ -125,7 +147,12 @@ class ClockSampler:
             self.proc.kill()
         sms, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        if self.window and lines:
+            t0, t1 = self.window
+            near = [(t, ln) for t, ln in lines if t0 - 0.15 <= t <= t1 + 0.15]
+            lines = near or [min(lines, key=lambda x: abs(x[0] - t0))]
+        for _, ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -213,21 +240,21 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    N = args.gpus
-    n = cpu_sample_size(args, N)
+    N, R = args.gpus, args.ranks
+    n = cpu_sample_size(args, R)
     import oracle
     import synth
     batches = []
-    for s in range(N):
+    for s in range(R):
         it = synth.make_items(s, 0, n, max(args.item_bytes, 16))[:, :args.item_bytes].copy()
-        ds = synth.make_dests(args.pattern, synth.CONFIG_SEEDS[2], s, 0, n, N)
+        ds = synth.make_dests(args.pattern, synth.CONFIG_SEEDS[2], s, 0, n, R)
         batches.append((it, ds))
-    w = oracle.World(N, n + n // 8 + 4096, args.item_bytes)
+    w = oracle.World(R, n + n // 8 + 4096, args.item_bytes)
 
     def step():
         for s, (it, ds) in enumerate(batches):
             w.emit_many(s, it, ds)
-        assert w.forward() == N * n
+        assert w.forward() == R * n
 
     with pinned_to_core0():
         for _ in range(args.warmup):
@@ -236,16 +263,16 @@ def run_reference(args):
         for _ in range(args.steps):
             step()
         dt = time.perf_counter() - t0
-    v = N * n * args.steps / dt
+    v = R * n * args.steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "items/s", "n_gpus": N, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic (synth/ SplitMix64 recipe)",
         "config": workload_config(args, N),
         "cpu_baseline": dict({"value": v, "unit": "items/s", "cores": 1, "kind": "oracle",
                               "sample": "R=%d x %d items x %d B per step (bounded sample of the workload), "
                                         "sequential emit + plain forward, single-threaded C oracle pinned to "
-                                        "one core (sched_setaffinity, as taskset -c 0)" % (N, n, args.item_bytes)},
+                                        "one core (sched_setaffinity, as taskset -c 0)" % (R, n, args.item_bytes)},
                              **host_facts()),
         "e2e": {"value": v, "unit": "items/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -273,43 +300,6 @@ def stored_nvlink_counters(scatter, B, n, N):
 
 
 # ----------------------------------------------------------------------------- supplementary blocks
-
-def bench_binning_r8(rafi, synth, torch, stream, args, hbm_peak):
-    """R=8 binning on one GPU: the whole cfg2 world (8 logical ranks x 16M x
-    48-B items, uniform destinations) forwarded FUSED into local queues; the
-    per-kernel durations of histogram + scan + scatter (CUDA events on the
-    context stream, instrumented forwards) against their algorithmic bytes
-    2B+8 per item."""
-    L, n, B = 8, args.items, args.item_bytes
-    cap = n + n // 8
-    ctx = rafi.Context(B, cap, stream=stream, local_ranks=L)
-    try:
-        ctx.set_option(rafi.OPT_TIMING, 1)
-        for k in range(args.warmup + args.steps):
-            if k == args.warmup:
-                ctx.set_option(rafi.OPT_TIMING, 1)  # resets the accumulated phase sums
-            for l in range(L):
-                ctx.drv_emit_synthetic(synth.PATTERNS["uniform"], synth.CONFIG_SEEDS[2], k, n, local=l)
-            assert ctx.forward() == L * n
-        st = ctx.stats()
-        K = st["acc_forwards"]
-        ms = {p: st["acc_ms_" + p] / K for p in ("hist", "scan", "count_exchange", "scatter")}
-        tot = ms["hist"] + ms["scan"] + ms["count_exchange"] + ms["scatter"]
-        byts = L * n * (2 * B + 8)
-        gbs = byts / (tot / 1e3) / 1e9
-        sc_bytes = L * n * (2 * B + 4)
-        return {"workload": "cfg2 world on one GPU: %d logical ranks x %d x %d-B items, uniform over R=%d, FUSED "
-                            "into local incoming queues" % (L, n, B, L),
-                "items": L * n, "ms": tot, "ms_phases": ms, "algorithmic_bytes": byts, "achieved_gbs": gbs,
-                "frac": gbs / hbm_peak, "frac_of_8tbs": gbs / 8000.0, "peak": hbm_peak,
-                "scatter_gbs": sc_bytes / (ms["scatter"] / 1e3) / 1e9,
-                "scatter_frac": sc_bytes / (ms["scatter"] / 1e3) / 1e9 / hbm_peak,
-                "tile": ctx.get_option(rafi.OPT_TILE), "forwards_timed": K,
-                "what": "histogram + scan(+plan) + stable scatter of one forward; bytes = (2B+8) per item: hist "
-                        "reads 4, scatter reads B+4 and writes B"}
-    finally:
-        ctx.close()
-
 
 def bench_device_emit(rafi, torch, stream, items_d, dests_d, args, hbm_peak):
     """The app-facing emit (rafi::Queue<T>::emitOutgoing, warp-aggregated
@@ -374,13 +364,16 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         comm = rafi.nccl_comm_init(world, rank, obj[0], local)
 
-    B, n = args.item_bytes, args.items
+    B, n, R = args.item_bytes, args.items, args.ranks
+    if R % N:
+        raise SystemExit("--ranks %d must be a multiple of the GPU count %d" % (R, N))
+    L = R // N  # logical ranks per GPU (global ranks rank*L .. rank*L+L-1)
     # the context's own (non-default) stream: everything below is ordered on
     # it, and it can be captured into a CUDA graph
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.synchronize()
     cap = n + n // 8 + 4096
-    ctx = rafi.Context(B, cap, comm=comm, stream=stream, device=local)
+    ctx = rafi.Context(B, cap, comm=comm, stream=stream, device=local, local_ranks=L)
     if args.exchange != "auto":
         ctx.set_option(rafi.OPT_EXCHANGE, {"nccl": rafi.EXCHANGE_NCCL, "peer": rafi.EXCHANGE_PEER,
                                            "fused": rafi.EXCHANGE_FUSED}[args.exchange])
@@ -393,11 +386,18 @@ def main():
         ctx.set_option(rafi.OPT_CONTROL, {"nccl": rafi.CONTROL_NCCL, "peer": rafi.CONTROL_PEER}[args.control])
     control = {1: "nccl", 2: "peer", 3: "host"}[ctx.get_option(rafi.OPT_CONTROL)] if N > 1 else None
 
-    # resident inputs (generated on the host by the shared generator, uploaded once)
-    items_h = synth.make_items(rank, 0, n, max(B, 16))[:, :B].copy()
-    dests_h = synth.make_dests(args.pattern, synth.CONFIG_SEEDS[2], rank, 0, n, N)
+    # resident inputs (generated on the host by the shared generator, uploaded
+    # once).  The item payload is generated once per GPU and shared by its
+    # logical ranks (16M x 48 B takes seconds to generate on the host); every
+    # rank has its own destinations.
+    items_h = synth.make_items(rank * L, 0, n, max(B, 16))[:, :B].copy()
+    dests_h = [synth.make_dests(args.pattern, synth.CONFIG_SEEDS[2], rank * L + l, 0, n, R) for l in range(L)]
     items_d = torch.from_numpy(items_h).to(dev)
-    dests_d = torch.from_numpy(dests_h).to(dev)
+    dests_d = [torch.from_numpy(d).to(dev) for d in dests_h]
+
+    def emit_all(items, dests):
+        for l in range(L):
+            ctx.emit_bulk(items, dests[l], n, local=l)
 
     def barrier():
         torch.cuda.synchronize()
@@ -419,37 +419,39 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
-    # ---- warm-up
+    # ---- warm-up (the clock sampler starts first: its start-up must not overlap the timed region)
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(args.warmup):
-        ctx.emit_bulk(items_d, dests_d, n)
+        emit_all(items_d, dests_d)
         G = ctx.forward()
-    assert G == N * n, (G, N * n)
+    assert G == R * n, (G, R * n)
 
     # ---- timed region (device-timed: CUDA events on the context stream,
     # barrier + synchronize on both sides, max over ranks).  The library runs
     # un-instrumented here (RAFI_OPT_TIMING is off by default): every blocking
     # forward replays the CUDA graph the warm-up steps captured.
     assert ctx.get_option(rafi.OPT_TIMING) == 0
-    clocks = ClockSampler(local)
     l0 = ctx.stats()["kernel_launches"]
     barrier()
-    clocks.start()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     f_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    w0 = time.perf_counter()
     t_start.record(stream)
     for k in range(args.steps):
-        ctx.emit_bulk(items_d, dests_d, n)
+        emit_all(items_d, dests_d)
         f_ev[k][0].record(stream)     # forward only (a2-a8): events around each rafi_forward
         G = ctx.forward()
         f_ev[k][1].record(stream)
     t_end.record(stream)
     barrier()
+    clocks.mark(w0, time.perf_counter())
     clk = clocks.stop()
     ms_fwd = max_over_ranks(sum(a.elapsed_time(b) for a, b in f_ev))
     st = ctx.stats()
     launches = st["kernel_launches"] - l0
-    remote = st["bytes_sent_remote"] * args.steps  # same plan every step
+    remote = sum(ctx.stats(l)["bytes_sent_remote"] for l in range(L)) * args.steps  # same plan every step
     ms_total = t_start.elapsed_time(t_end)
     ms_max = max_over_ranks(ms_total)
     K = args.steps
@@ -464,43 +466,45 @@ def main():
     i_end = torch.cuda.Event(enable_timing=True)
     i_start.record(stream)
     for k in range(args.steps):
-        ctx.emit_bulk(items_d, dests_d, n)
+        emit_all(items_d, dests_d)
         ctx.forward()
     i_end.record(stream)
     barrier()
     st = ctx.stats()
     ms_instr = max_over_ranks(i_start.elapsed_time(i_end)) / K
-    assert st["acc_forwards"] == K and st["acc_emits"] == K, (st["acc_forwards"], st["acc_emits"])
-    value = N * n * K / (ms_max / 1e3)
+    assert st["acc_forwards"] == K and st["acc_emits"] == K * L, (st["acc_forwards"], st["acc_emits"])
+    value = R * n * K / (ms_max / 1e3)
     ms_step = ms_max / K
-    forward_only = {"value": N * n * K / (ms_fwd / 1e3), "unit": "items/s", "ms_per_forward": ms_fwd / K,
+    forward_only = {"value": R * n * K / (ms_fwd / 1e3), "unit": "items/s", "ms_per_forward": ms_fwd / K,
                     "what": "rafi_forward alone (hist, scan, count exchange, scatter/payload exchange, wrap-up, "
                             "termination count), emission excluded: the paper's sort-and-send (PAPER:449); CUDA "
                             "events around each forward inside the timed region, max over ranks"}
     ph = {k: st["acc_ms_" + k] / K for k in ("emit", "hist", "scan", "scatter", "count_exchange",
-                                            "payload_exchange", "wrapup")}
+                                            "payload_exchange", "wrapup")}  # per step (emit: all L launches)
+    per_launch = dict(ph, emit=ph["emit"] / L)
 
     # ---- rooflines: algorithmic bytes per launch / average launch duration
     hbm_peak, peak_src = load_peaks()
-    nin = ctx.num_incoming()
-    alg = {  # bytes per launch (per rank); DESIGN.md "Rooflines"
+    nin = sum(ctx.num_incoming(l) for l in range(L))
+    alg = {  # bytes per launch; DESIGN.md "Rooflines" (one emit launch per rank; hist/scatter cover all L)
         "emit": n * 2 * (B + 4),
-        "hist": n * 4,
-        "scatter": n * (B + 4 + B),
+        "hist": L * n * 4,
+        "scatter": L * n * (B + 4 + B),
         "payload_exchange": nin * 2 * B if (N == 1 and exchange != "fused") else None,
     }
     kern = {}
     for k, byts in alg.items():
-        if byts is None or ph[k] <= 0:
+        if byts is None or per_launch[k] <= 0:
             continue
-        gbs = byts / (ph[k] / 1e3) / 1e9
-        kern[k] = {"ms": ph[k], "bytes": byts, "achieved_gbs": gbs, "frac": gbs / hbm_peak}
+        gbs = byts / (per_launch[k] / 1e3) / 1e9
+        kern[k] = {"ms": per_launch[k], "bytes": byts, "achieved_gbs": gbs, "frac": gbs / hbm_peak,
+                   "launches_per_step": L if k == "emit" else 1}
     dom = max(kern, key=lambda k: kern[k]["ms"])
     traffic, traffic_src = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f)
-        key = "%s/B%d/n%d/R%d" % (dom, B, n, N)
+        key = "%s/B%d/n%d/R%d/N%d" % (dom, B, n, R, N)
         traffic = tr.get(key)
         if traffic is not None:
             traffic_src = "STORED, not measured in this run: dram__bytes_read.sum + dram__bytes_write.sum of " \
@@ -534,18 +538,20 @@ def main():
     if not args.no_e2e:
         ctx.set_option(rafi.OPT_TIMING, 0)
         items_p = torch.from_numpy(items_h).pin_memory()
-        dests_p = torch.from_numpy(dests_h).pin_memory()
-        # two pinned result buffers: step k's read-back (copy-out stream) overlaps
-        # step k+1's host-to-device copy (copy-in stream) over full-duplex PCIe
-        outs = [torch.empty((cap, B), dtype=torch.uint8).pin_memory() for _ in range(2)]
+        dests_p = [torch.from_numpy(d).pin_memory() for d in dests_h]
+        # two pinned result buffers per rank: step k's read-back (copy-out
+        # stream) overlaps step k+1's host-to-device copy (copy-in stream) over
+        # full-duplex PCIe
+        outs = [[torch.empty((cap, B), dtype=torch.uint8).pin_memory() for _ in range(2)] for _ in range(L)]
         # as many steps as the device-resident measurement: the pipeline's
         # one-time fill (first upload) and drain (last read-back) are inside
         # the timed region and amortise over K steps
         Ke = max(3, K)
         for k in range(2):
-            ctx.emit_bulk(items_p, dests_p, n)
+            emit_all(items_p, dests_p)
             ctx.forward()
-            ctx.read_incoming_async(outs[k % 2][: ctx.num_incoming()])
+            for l in range(L):
+                ctx.read_incoming_async(outs[l][k % 2][: ctx.num_incoming(l)], local=l)
         ctx.read_wait()
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -553,16 +559,17 @@ def main():
         d2h = 0
         e0.record(stream)
         for k in range(Ke):
-            ctx.emit_bulk(items_p, dests_p, n)             # H2D inside the call (host pointers)
+            emit_all(items_p, dests_p)                      # H2D inside the calls (host pointers)
             ctx.forward()
-            m = ctx.num_incoming()
-            ctx.read_incoming_async(outs[k % 2][:m])       # D2H of the result
-            d2h += m * B
+            for l in range(L):
+                m = ctx.num_incoming(l)
+                ctx.read_incoming_async(outs[l][k % 2][:m], local=l)  # D2H of the result
+                d2h += m * B
         ctx.read_wait()                                    # every result is in host memory
         e1.record(stream)
         barrier()
         ms_e = max_over_ranks(e0.elapsed_time(e1))
-        e2e = {"value": N * n * Ke / (ms_e / 1e3), "unit": "items/s", "h2d_bytes_per_step": n * (B + 4),
+        e2e = {"value": R * n * Ke / (ms_e / 1e3), "unit": "items/s", "h2d_bytes_per_step": L * n * (B + 4),
                "d2h_bytes_per_step": int(d2h / Ke), "steps": Ke}
 
     # ---- the same step as an application-side CUDA graph (NEXT-3): [emit_bulk +
@@ -573,7 +580,7 @@ def main():
         ctx.set_option(rafi.OPT_TIMING, 0)
         G_dev = torch.zeros(1, dtype=torch.int64, device=dev)
         ctx.capture_begin()
-        ctx.emit_bulk(items_d, dests_d, n)
+        emit_all(items_d, dests_d)
         ctx.forward_async(G_dev)
         ex = ctx.capture_end()
         for _ in range(args.warmup):
@@ -587,39 +594,54 @@ def main():
         g1.record(stream)
         barrier()
         ms_g = max_over_ranks(g0.elapsed_time(g1))
-        assert int(G_dev.item()) == N * n
+        assert int(G_dev.item()) == R * n
         ctx.sync_host()
         rafi.Context.graph_destroy(ex)
-        graph = {"value": N * n * K / (ms_g / 1e3), "unit": "items/s", "ms_per_step": ms_g / K,
+        graph = {"value": R * n * K / (ms_g / 1e3), "unit": "items/s", "ms_per_step": ms_g / K,
                  "what": "[emit_bulk + rafi_forward_async] captured as one CUDA graph, replayed K times"}
 
-    # ---- supplementary single-GPU blocks: R=8 binning and the device-side emit
-    binning_r8 = device_emit = None
+    # ---- binning at N=1: the whole R-rank world's histogram + scan + scatter
+    # (the instrumented phases of the headline steps), against (2B+8) bytes per item
+    binning = None
+    if N == 1:
+        bms = ph["hist"] + ph["scan"] + ph["count_exchange"] + ph["scatter"]
+        byts = R * n * (2 * B + 8)
+        binning = {"workload": "the headline world: %d ranks x %d x %d-B items on one GPU, FUSED into local queues"
+                               % (R, n, B), "ranks": R, "items": R * n, "ms": bms,
+                   "ms_phases": {k: ph[k] for k in ("hist", "scan", "count_exchange", "scatter")},
+                   "algorithmic_bytes": byts, "achieved_gbs": byts / (bms / 1e3) / 1e9,
+                   "frac": byts / (bms / 1e3) / 1e9 / hbm_peak, "frac_of_8tbs": byts / (bms / 1e3) / 1e9 / 8000.0,
+                   "scatter_frac": kern["scatter"]["frac"], "peak": hbm_peak, "tile": ctx_tile,
+                   "what": "histogram + scan(+plan) + stable scatter of one forward; bytes = (2B+8) per item: "
+                           "hist reads 4, scatter reads B+4 and writes B; from the instrumented pass"}
+
+    # ---- supplementary single-GPU block: the device-side emit
+    device_emit = None
     if N == 1 and not args.no_extras:
         ctx.close()
         ctx = None
         torch.cuda.empty_cache()
-        binning_r8 = bench_binning_r8(rafi, synth, torch, stream, args, hbm_peak)
-        device_emit = bench_device_emit(rafi, torch, stream, items_d, dests_d, args, hbm_peak)
+        device_emit = bench_device_emit(rafi, torch, stream, items_d, torch.zeros(n, dtype=torch.int32, device=dev),
+                                        args, hbm_peak)
 
     # ---- cpu baseline: the oracle on the host, rank 0 at N=1 only
     cpu = None
     if N == 1 and rank == 0 and not args.no_cpu_baseline:
-        ns = cpu_sample_size(args, 1)
-        v, reps, desc = oracle_step_rate(1, ns, B, args.pattern, args.cpu_seconds)
+        ns = cpu_sample_size(args, R)
+        v, reps, desc = oracle_step_rate(R, ns, B, args.pattern, args.cpu_seconds)
         cpu = dict({"value": v, "unit": "items/s", "cores": 1, "kind": "oracle",
                     "sample": desc + " (single-threaded C oracle on the GPU box host, pinned to one core "
                                      "with sched_setaffinity as taskset -c 0)"}, **host_facts())
 
     line = {
         "metric": METRIC, "value": value, "unit": "items/s", "n_gpus": N, "steps": K, "warmup": args.warmup,
-        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (synth/ SplitMix64 recipe; resident in HBM)", "config": workload_config(args, N),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clk, "phases_ms": ph, "phases_source": "instrumented pass of the same K steps (CUDA events "
         "between launches); its ms_per_step: %.4f" % ms_instr, "kernels": kern, "exchange": exch, "exchange_transport": exchange,
         "graph_replay": graph, "scatter_write": scatter, "tile": ctx_tile, "control": control, "per_gpu_items_per_s": value / N,
-        "forward_only": forward_only, "binning_r8": binning_r8, "device_emit": device_emit,
+        "forward_only": forward_only, "binning": binning, "device_emit": device_emit,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

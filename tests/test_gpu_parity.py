@@ -473,3 +473,22 @@ def test_diag_redirect_incoming(B, scatter):
     with _ctx(B, n, 1) as ctx:
         with pytest.raises(rafi.RafiError):
             ctx.diag_redirect_incoming(1, buf)   # not a local rank
+
+
+@pytest.mark.parametrize("R", [1, 3, 8])
+def test_warp_tiles_many_rounds_empty_ranks_and_resize(R):
+    """The warp-tile path (256-item tiles, R <= 8: k_hist_w, k_scan,
+    k_scatter_w) over many forwards on one context: sizes that change every
+    round (empty ranks, partial scan blocks and tiles), a resize between
+    rounds (new H/O arrays), every round P1-exact against the oracle."""
+    B = 48
+    sizes = [[5000, 0, 70001], [0, 0, 0], [2048, 2047, 1], [300000, 4096, 0], [1, 0, 123457]]
+    with _ctx(B, 300000, R) as ctx:
+        assert ctx.get_option(rafi.OPT_TILE) == 256
+        for rnd, ns in enumerate(sizes * 2):
+            if rnd == len(sizes):
+                ctx.resize(400000)
+            inputs = [(synth.make_items(s, rnd, ns[s % 3], B)[:, :B].copy(),
+                       synth.make_dests("uniform", 40 + rnd, s, rnd, ns[s % 3], R)) for s in range(R)]
+            _emit_all(ctx, inputs)
+            p1_forward(ctx, R, B)

@@ -372,3 +372,81 @@ def test_ring_walk_rounds(R):
             break
     assert rounds == R + 1 and carrying[:R] == [R] * R and carrying[R] == 0
     # after R hops every item is back at its origin: no premature exit of any rank
+
+
+# ---------------------------------------------------------------- emit_many / load_snapshot / set_incoming
+
+@pytest.mark.parametrize("cap", [0, 1, 7, 64, 500])
+def test_emit_many_is_the_drop_rule(cap):
+    """orc_emit_many against the drop and reject rules written out (Z1, Z2,
+    PAPER:71): the queue holds exactly the first min(cap, #valid) valid
+    (item, dest) pairs in array order, the counter counts every valid
+    attempt, the reject counter every invalid one -- and a world fed by
+    single orc_emit calls ends in the same state and forwards alike."""
+    rng = np.random.default_rng(cap + 3)
+    R, B, n = 3, 12, 300
+    items = rng.integers(0, 256, (n, B), dtype=np.uint8)
+    dests = rng.integers(-2, R + 2, n).astype(np.int32)
+    valid = [i for i in range(n) if 0 <= dests[i] < R]
+    kept = valid[:cap]
+    a, b = oracle.World(R, cap, B), oracle.World(R, cap, B)
+    assert a.emit_many(1, items, dests) == len(kept)
+    for i in range(n):
+        b.emit(1, items[i].tobytes(), int(dests[i]))
+    for w in (a, b):
+        assert w.emitted(1) == len(valid) and w.invalid(1) == n - len(valid)
+        assert np.array_equal(w.out_items(1), items[kept].reshape(len(kept), B))
+        assert np.array_equal(w.out_dests(1), dests[kept])
+    ga, gb = a.forward(), b.forward()
+    if ga == oracle.ERR_RECV_OVERFLOW:
+        assert gb == ga
+        return
+    assert ga == gb == len(kept)
+    for r in range(R):
+        assert np.array_equal(a.incoming(r), b.incoming(r))
+        assert np.array_equal(a.incoming(r), items[[i for i in kept if dests[i] == r]].reshape(-1, B))
+
+
+@pytest.mark.parametrize("literal", [False, True])
+def test_load_snapshot_round_trip(literal):
+    """A queue state read back from one world (items in slot order, dests,
+    raw counters) and loaded into a fresh world with orc_load_snapshot
+    forwards to the same incoming queues, count matrix and G -- including an
+    over-capacity counter (only cap items are loaded, the rest count as
+    dropped) -- and a snapshot with an out-of-range dest is refused."""
+    rng = np.random.default_rng(9)
+    R, cap, B = 4, 50, 20
+    src = oracle.World(R, cap, B)
+    for s in range(R):
+        n = int(rng.integers(0, 70))
+        src.emit_many(s, rng.integers(0, 256, (n, B), dtype=np.uint8), rng.integers(-1, R + 1, n).astype(np.int32))
+    dst = oracle.World(R, cap, B)
+    for s in range(R):
+        dst.load_snapshot(s, src.out_items(s), src.out_dests(s), src.emitted(s), src.invalid(s))
+        assert dst.emitted(s) == src.emitted(s) and dst.invalid(s) == src.invalid(s)
+    g1, g2 = src.forward(literal=literal), dst.forward(literal=literal)
+    assert g1 == g2
+    if g1 == oracle.ERR_RECV_OVERFLOW:
+        return
+    assert np.array_equal(src.C(), dst.C())
+    for r in range(R):
+        assert np.array_equal(src.incoming(r), dst.incoming(r))
+        assert dst.dropped_last(r) == src.dropped_last(r)
+    bad = oracle.World(2, 4, 4)
+    with pytest.raises(ValueError):
+        bad.load_snapshot(0, np.zeros((2, 4), np.uint8), np.array([0, 2], np.int32), 2, 0)
+
+
+def test_set_incoming_is_what_get_incoming_reads():
+    """orc_set_incoming seeds a rank's input queue: numIncoming and
+    getIncoming read back exactly the seeded items; more than
+    capacity is refused; a forward replaces the queue (Z12)."""
+    w = oracle.World(2, 8, 6)
+    seed = np.arange(5 * 6, dtype=np.uint8).reshape(5, 6)
+    w.set_incoming(1, seed)
+    assert w.num_incoming(1) == 5 and np.array_equal(w.incoming(1), seed)
+    with pytest.raises(ValueError):
+        w.set_incoming(0, np.zeros((9, 6), np.uint8))
+    assert w.emit(0, b"abcdef", 1)
+    assert w.forward() == 1
+    assert w.num_incoming(1) == 1 and w.incoming(1)[0].tobytes() == b"abcdef"
