@@ -451,7 +451,11 @@ def main():
     ms_fwd = max_over_ranks(sum(a.elapsed_time(b) for a, b in f_ev))
     st = ctx.stats()
     launches = st["kernel_launches"] - l0
-    remote = sum(ctx.stats(l)["bytes_sent_remote"] for l in range(L)) * args.steps  # same plan every step
+    # bytes this GPU pushes to OTHER GPUs per step (its ranks' rows of the
+    # count matrix, columns of ranks hosted elsewhere), same plan every step
+    Cm = ctx.matrix()
+    mine = slice(rank * L, rank * L + L)
+    remote = (int(Cm[mine, :].sum()) - int(Cm[mine, mine].sum())) * B * args.steps
     ms_total = t_start.elapsed_time(t_end)
     ms_max = max_over_ranks(ms_total)
     K = args.steps

@@ -1291,7 +1291,10 @@ int rafi_set_option(rafi_ctx* ctx, int key, long long v) {
       return RAFI_OK;
     case RAFI_OPT_TILE: {
       // only between rounds with an empty outgoing queue; re-sizes H/O
-      if (v != 0 && (v < 256 || v > 4096 || (v & (v - 1)) != 0)) return RAFI_ERR_INVALID_ARG;  // 256 * 2^k
+      // 256 * 2^k; or 128 on the warp-tile path (THREADS, R <= 8, item_bytes % 8 == 0)
+      if (v != 0 && (v < 128 || v > 4096 || (v & (v - 1)) != 0)) return RAFI_ERR_INVALID_ARG;
+      if (v == 128 && !(c->scatter_eff == RAFI_SCATTER_THREADS && warp_tiles_ok(128, c->B, c->R, c->L)))
+        return RAFI_ERR_INVALID_ARG;
       const uint32_t t = v ? (uint32_t)v : auto_tile(c);
       if (c->scatter_eff == RAFI_SCATTER_BULK && perm_smem_bytes(t, c->B, c->R) > kMaxSmem) {
         set_error("tile too large for the permuting scatter's shared memory");

@@ -156,10 +156,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 
 // ---------------------------------------------------------------- warp-tile path (warp_tiles.cu)
 
-// Binning tile of the warp-tile path: one warp owns one tile.
-constexpr uint32_t kWarpTile = 256;
-// R <= 8, item_bytes % 8 == 0, and at least two warp regions fit per CTA.
-bool warp_tiles_ok(uint64_t item_bytes, int R, int L);
+// The warp-tile histogram serves any 128/256-item tiling with R <= 8.
+inline bool hist_w_ok(uint32_t tile, int R) { return (tile == 128 || tile == 256) && R <= 8; }
 int launch_hist_w(Ctx* c, int nsm);
 int launch_scatter_w(Ctx* c, bool fused, bool wrap, PeerCtl pc, int nsm);
 

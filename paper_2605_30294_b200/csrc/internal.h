@@ -176,6 +176,12 @@ inline size_t ctrl_c_bytes(const Ctx* c) { return sizeof(CtrlDev) * c->L + sizeo
 
 // kernels.cu
 uint32_t choose_tile(uint64_t item_bytes, int R, int L);
+// warp_tiles.cu: binning tiles of the warp-tile path (one warp owns one
+// tile): 128 or 256 items, R <= 8, item_bytes % 8 == 0, and at least two warp
+// regions fit; warp_tile_for = the tile the automatic choice takes (0: the
+// path does not apply).
+bool warp_tiles_ok(uint32_t tile, uint64_t item_bytes, int R, int L);
+uint32_t warp_tile_for(uint64_t item_bytes, int R, int L);
 uint32_t choose_tile_perm(uint64_t item_bytes, int R);
 bool perm_supported(uint64_t item_bytes);
 size_t perm_smem_bytes(uint32_t tile, uint64_t item_bytes, int R);

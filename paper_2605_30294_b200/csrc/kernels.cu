@@ -1117,7 +1117,7 @@ static uint32_t scatter_budget(uint64_t B) {
 
 uint32_t choose_tile(uint64_t item_bytes, int R, int L) {
   // R <= 8 and 8-byte units: the warp-tile path (warp_tiles.cu), 256-item tiles
-  if (warp_tiles_ok(item_bytes, R, L)) return kWarpTile;
+  if (const uint32_t w = warp_tile_for(item_bytes, R, L)) return w;
   // two pipeline stages (items + dests) plus 2 B/item of indices in ~110 KiB,
   // so two CTAs fit on an SM
   const uint64_t t = scatter_budget(item_bytes) / (2 * item_bytes + 10);
@@ -1161,7 +1161,7 @@ static int persistent_grid(Ctx* c, int per_sm) {
 }
 
 int launch_hist(Ctx* c) {
-  if (c->tile == kWarpTile && c->R <= 8) {  // one warp per scan block (same O/H layout)
+  if (hist_w_ok(c->tile, c->R)) {  // one warp per scan block (same O/H layout)
     RAFI_CK(launch_hist_w(c, num_sms(c->device)));
     c->launches += 1; c->fwd_launches += 1;
     return RAFI_OK;
@@ -1326,7 +1326,7 @@ static int launch_scatter_perm(Ctx* c, bool fused, bool wrap) {
 
 int launch_scatter(Ctx* c, bool fused, bool wrap) {
   if (c->scatter_eff == RAFI_SCATTER_BULK) return launch_scatter_perm(c, fused, wrap);
-  if (c->tile == kWarpTile && warp_tiles_ok(c->B, c->R, c->L)) {
+  if (warp_tiles_ok(c->tile, c->B, c->R, c->L)) {
     RAFI_CK(launch_scatter_w(c, fused, wrap, peer_ctl(c, c->scatter_barrier), num_sms(c->device)));
     c->launches += 1; c->fwd_launches += 1;
     return RAFI_OK;

@@ -35,7 +35,6 @@
 
 namespace rafi_impl {
 
-constexpr int kWK = (int)kWarpTile / 32;  // items per lane of a warp tile
 // tuning (build-time; paper_2605_30294_b200/build.py variants)
 #ifndef RAFI_W_STAGES
 #define RAFI_W_STAGES 2
@@ -52,16 +51,28 @@ constexpr uint32_t kWSmemMax = 227u * 1024u;
 
 constexpr int kHWarps = 8;      // warps per CTA (one CTA per SM)
 constexpr int kHStages = 3;     // TMA ring depth per warp
-constexpr uint32_t kHBlk = kWarpTile * kHistTilesPerCta;  // dests per scan block (2048 = 8 KiB)
 
-__host__ __device__ constexpr uint32_t hist_w_smem(int L) { return kHWarps * (kHStages * kHBlk * 4 + 64) + 8 * (2 * L + 1); }
+// dests per scan block: 8 tiles (2048 = 8 KiB at 256-item tiles, 1024 at 128)
+template <int kWT>
+struct HistBlk {
+  static constexpr uint32_t kBlk = kWT * kHistTilesPerCta;
+  static constexpr int kVec = kWT / 16;     // int4 per lane per block
+  static constexpr int kPerTile = kWT / 128;  // int4 per lane per tile
+};
+
+template <int kWT>
+__host__ __device__ constexpr uint32_t hist_w_smem(int L) {
+  return kHWarps * (kHStages * HistBlk<kWT>::kBlk * 4 + 64) + 8 * (2 * L + 1);
+}
 
 // Persistent: warp w of CTA x takes scan blocks gw, gw + stride, ... (flat
 // over the local ranks), each streamed into its private kHStages-deep ring by
 // one 8-KiB TMA bulk load.  Scan block b of local rank l = tiles 8b .. 8b+7.
+template <int kWT>
 __global__ void __launch_bounds__(kHWarps * 32, 1) k_hist_w(const RankDev* __restrict__ rk,
                                                              const CtrlDev* __restrict__ ctrl, int L, int R,
                                                              uint64_t cap) {
+  constexpr uint32_t kHBlk = HistBlk<kWT>::kBlk;
   extern __shared__ __align__(128) uint8_t smem[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* my = smem + (size_t)w * (kHStages * kHBlk * 4 + 64);
@@ -110,14 +121,14 @@ __global__ void __launch_bounds__(kHWarps * 32, 1) k_hist_w(const RankDev* __res
     int l;
     const uint64_t b = locate(g, &l);
     const uint64_t n = nl[l];
-    const uint64_t tiles = (n + kWarpTile - 1) / kWarpTile;
+    const uint64_t tiles = (n + kWT - 1) / kWT;
     const uint64_t nblk = (tiles + kHistTilesPerCta - 1) / kHistTilesPerCta;
     const uint64_t i0 = b * kHBlk;
     const bool full = i0 + kHBlk <= n;
     mbar_wait(&mbar[it % kHStages], (it / kHStages) & 1);
     const int4* d4 = reinterpret_cast<const int4*>(my + (it % kHStages) * kHBlk * 4);
-    // int4 q = 32 i + lane holds dests 4q .. 4q+3, in tile q / 64 = i / 2.
-    // Per tile, byte d of c counts destination d among this lane's 8 dests
+    // int4 q = 32 i + lane holds dests 4q .. 4q+3, in tile 4q / kWT = i / kPerTile.
+    // Per tile, byte d of c counts destination d among this lane's 4 kPerTile dests
     // (every queued dest is in [0, R), R <= 8: invalid ones were rejected at
     // emit); then widened to 16-bit fields, even and odd destinations apart:
     //   word 4t+0: dests 0, 2   4t+1: 4, 6   4t+2: 1, 3   4t+3: 5, 7
@@ -126,8 +137,8 @@ __global__ void __launch_bounds__(kHWarps * 32, 1) k_hist_w(const RankDev* __res
     for (int t = 0; t < 8; ++t) {
       uint64_t c = 0;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int i = 2 * t + h;
+      for (int h = 0; h < HistBlk<kWT>::kPerTile; ++h) {
+        const int i = HistBlk<kWT>::kPerTile * t + h;
         const int4 v = d4[i * 32 + lane];
         const int e[4] = {v.x, v.y, v.z, v.w};
         const uint64_t e0 = i0 + (uint64_t)(i * 32 + lane) * 4;
@@ -195,14 +206,14 @@ struct WarpLayout {
   uint32_t off_cta, total;
 };
 
-static WarpLayout warp_layout(uint64_t B, int R, int L, int warps) {
+static WarpLayout warp_layout(uint32_t kWT, uint64_t B, int R, int L, int warps) {
   auto al = [](uint64_t x, uint64_t a) { return (uint32_t)((x + a - 1) / a * a); };
   WarpLayout s;
-  s.stage_items = al((uint64_t)kWarpTile * B, 16);
-  s.stage_stride = al((uint64_t)s.stage_items + 4ull * kWarpTile, 128);
+  s.stage_items = al((uint64_t)kWT * B, 16);
+  s.stage_stride = al((uint64_t)s.stage_items + 4ull * kWT, 128);
   uint32_t o = kWStages * s.stage_stride;
-  s.off_src = o; o += 2 * kWarpTile;
-  s.off_cnt = o; o += 4 * kWK * 8;
+  s.off_src = o; o += 2 * kWT;
+  s.off_cnt = o; o += 4 * (kWT / 32) * 8;
   s.off_rs = o; o = al(o + 4ull * (R + 1), 8);
   s.off_gb = o; o += 8 * R;
   s.off_mbar = o; o += 8 * kWStages;
@@ -212,9 +223,9 @@ static WarpLayout warp_layout(uint64_t B, int R, int L, int warps) {
   return s;
 }
 
-static int warps_that_fit(uint64_t B, int R, int L) {
+static int warps_that_fit(uint32_t kWT, uint64_t B, int R, int L) {
   int w = 0;
-  while (w < kWMaxWarps && warp_layout(B, R, L, w + 1).total <= kWSmemMax) ++w;
+  while (w < kWMaxWarps && warp_layout(kWT, B, R, L, w + 1).total <= kWSmemMax) ++w;
   return w;
 }
 
@@ -227,13 +238,14 @@ __device__ __forceinline__ void st_global(uint2* p, const uint2& v) {
   asm volatile("st.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
 }
 
-template <typename U>
+template <typename U, int kWT>
 __global__ void __launch_bounds__(kWMaxWarps * 32, 1)
 k_scatter_w(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint8_t* const* __restrict__ dst_table,
             const uint64_t* __restrict__ dst_off, const int* __restrict__ ovf, int L, int R, uint64_t cap, int cur,
             uint32_t B, uint32_t UPI, FastDiv divU, WarpLayout lay, unsigned* __restrict__ wrap_done,
             CtrlDev* __restrict__ ctrl_w, const uint64_t* __restrict__ wrap_num_in, PeerCtl pc) {
   if (ovf && *ovf) return;  // collective receive overflow: move nothing (Z3)
+  constexpr int kWK = kWT / 32;  // items per lane of a warp tile
   extern __shared__ __align__(128) uint8_t smem[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5;
   // tile map: tpre[l] = first flat tile of local rank l (tpre[L] = all), nl[l] = its items
@@ -251,7 +263,7 @@ k_scatter_w(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, ui
       const uint64_t n = n_items(ctrl[l], cap);
       nl[l] = n;
       tpre[l] = acc;
-      acc += (n + kWarpTile - 1) / kWarpTile;
+      acc += (n + kWT - 1) / kWT;
     }
     tpre[L] = acc;
   }
@@ -284,8 +296,8 @@ k_scatter_w(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, ui
   auto issue = [&]() {  // lane 0: start loading the tile at ci into stage n_issued % kWStages
     if (ci.l < L) {
       const int l = ci.l;
-      const uint64_t t0 = (ci.g - tpre[l]) * kWarpTile;
-      const uint32_t nt = (uint32_t)umin64(kWarpTile, nl[l] - t0);
+      const uint64_t t0 = (ci.g - tpre[l]) * kWT;
+      const uint32_t nt = (uint32_t)umin64(kWT, nl[l] - t0);
       uint8_t* st = my + (n_issued % kWStages) * lay.stage_stride;
       uint64_t* bar = &mbar[n_issued % kWStages];
       const uint32_t bi = (nt * B + 15) & ~15u, bd = (nt * 4 + 15) & ~15u;  // queues carry >= 16 B of slack
@@ -330,11 +342,10 @@ k_scatter_w(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, ui
   for (uint32_t it = 0; ct.l < L; ++it, advance(ct)) {
     const int l = ct.l;
     const uint64_t t = ct.g - tpre[l];
-    const uint32_t nt = (uint32_t)umin64(kWarpTile, nl[l] - t * kWarpTile);
+    const uint32_t nt = (uint32_t)umin64(kWT, nl[l] - t * kWT);
     const RunBase cur_rb = nxt;
     fetch(&nxt);
-    T[lane] = 0;
-    T[lane + 32] = 0;
+    for (int x = lane; x < kWK * 8; x += 32) T[x] = 0;  // kWK chunks x 8 destinations
     __syncwarp();
     const uint32_t s = it % kWStages;
     mbar_wait(&mbar[s], (it / kWStages) & 1);
@@ -441,28 +452,47 @@ k_scatter_w(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, ui
 
 // ---------------------------------------------------------------- host side
 
-bool warp_tiles_ok(uint64_t B, int R, int L) { return R <= 8 && B % 8 == 0 && warps_that_fit(B, R, L) >= 2; }
+bool warp_tiles_ok(uint32_t tile, uint64_t B, int R, int L) {
+  return (tile == 128 || tile == 256) && R <= 8 && B % 8 == 0 && warps_that_fit(tile, B, R, L) >= 2;
+}
 
-int launch_hist_w(Ctx* c, int nsm) {
-  const uint32_t sm = hist_w_smem(c->L);
+// 256-item tiles while they leave >= 6 warps per SM (items <= 64 B), else
+// 128 (twice the warps; 96 B: 0.90 vs 0.82 of HBM, 128 B: 0.88 vs 0.72 --
+// at <= 64 B the 256-item tiles win, 0.93-0.95 vs 0.84-0.89, and their
+// histogram streams 8-KiB blocks: 0.71 vs 0.50, gpurun_out/r02n_sweep.jsonl);
+// 0 = the warp-tile path does not apply.
+uint32_t warp_tile_for(uint64_t B, int R, int L) {
+  if (!(R <= 8 && B % 8 == 0)) return 0;
+  if (warps_that_fit(256, B, R, L) >= 6) return 256;
+  if (warps_that_fit(128, B, R, L) >= 2) return 128;
+  return 0;
+}
+
+template <int kWT>
+static int launch_hist_t(Ctx* c, int nsm) {
+  const uint32_t sm = hist_w_smem<kWT>(c->L);
   static uint32_t granted = 0;
   if (sm > granted) {
-    RAFI_CK_CUDA(cudaFuncSetAttribute(k_hist_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    RAFI_CK_CUDA(cudaFuncSetAttribute(k_hist_w<kWT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     granted = sm;
   }
   const uint64_t blocks = (c->max_tiles + kHistTilesPerCta - 1) / kHistTilesPerCta * (uint64_t)c->L;
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)nsm, (blocks + kHWarps - 1) / kHWarps));
-  k_hist_w<<<grid, kHWarps * 32, sm, c->stream>>>(c->rank_dev, c->ctrl, c->L, c->R, c->cap);
+  k_hist_w<kWT><<<grid, kHWarps * 32, sm, c->stream>>>(c->rank_dev, c->ctrl, c->L, c->R, c->cap);
   RAFI_CK_CUDA(cudaGetLastError());
   return RAFI_OK;
 }
 
-template <typename U>
+int launch_hist_w(Ctx* c, int nsm) {
+  return c->tile == 128 ? launch_hist_t<128>(c, nsm) : launch_hist_t<256>(c, nsm);
+}
+
+template <typename U, int kWT>
 static int launch_w(Ctx* c, bool fused, bool wrap, PeerCtl pc, int nsm) {
-  const int warps = warps_that_fit(c->B, c->R, c->L);
-  const WarpLayout lay = warp_layout(c->B, c->R, c->L, warps);
+  const int warps = warps_that_fit(kWT, c->B, c->R, c->L);
+  const WarpLayout lay = warp_layout(kWT, c->B, c->R, c->L, warps);
   static int granted = 0;
-  auto k = k_scatter_w<U>;
+  auto k = k_scatter_w<U, kWT>;
   if ((int)lay.total > granted) {
     RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
     granted = (int)lay.total;
@@ -479,8 +509,9 @@ static int launch_w(Ctx* c, bool fused, bool wrap, PeerCtl pc, int nsm) {
 }
 
 int launch_scatter_w(Ctx* c, bool fused, bool wrap, PeerCtl pc, int nsm) {
-  if (c->B % 16 == 0) return launch_w<uint4>(c, fused, wrap, pc, nsm);
-  return launch_w<uint2>(c, fused, wrap, pc, nsm);
+  if (c->tile == 128)
+    return c->B % 16 == 0 ? launch_w<uint4, 128>(c, fused, wrap, pc, nsm) : launch_w<uint2, 128>(c, fused, wrap, pc, nsm);
+  return c->B % 16 == 0 ? launch_w<uint4, 256>(c, fused, wrap, pc, nsm) : launch_w<uint2, 256>(c, fused, wrap, pc, nsm);
 }
 
 }  // namespace rafi_impl

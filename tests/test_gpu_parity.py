@@ -108,14 +108,33 @@ def test_forward_snapshot_parity(B, L, n, pattern, exchange, scatter):
         p1_forward(ctx, L, B)
 
 
-@pytest.mark.parametrize("tile", [256, 512, 1024, 4096])
-def test_tile_sizes(tile):
-    B, L, n = 48, 4, 20000
-    inputs = make_inputs(L, n, B, "uniform", 5)
+@pytest.mark.parametrize("tile", [128, 256, 512, 1024, 4096])
+@pytest.mark.parametrize("B", [24, 48, 64, 128])
+def test_tile_sizes(tile, B):
+    """Every tile on every path: 128/256 are the warp-tile kernels at R <= 8
+    (8-byte units at 24 B), larger tiles the block-tile ones."""
+    L, n = 4, 20011
+    inputs = make_inputs(L, n, B, "uniform", 5 + B)
     with _ctx(B, n * L, L) as ctx:
         ctx.set_option(rafi.OPT_TILE, tile)
+        assert ctx.get_option(rafi.OPT_TILE) == tile
         _emit_all(ctx, inputs)
         p1_forward(ctx, L, B)
+
+
+def test_tile_128_needs_the_warp_tile_path():
+    """RAFI_OPT_TILE 128 exists only on the warp-tile path (THREADS, R <= 8,
+    item_bytes % 8 == 0)."""
+    with _ctx(44, 1000, 2) as ctx:          # 4-byte units: block tiles only
+        with pytest.raises(rafi.RafiError):
+            ctx.set_option(rafi.OPT_TILE, 128)
+    with _ctx(48, 1000, 9) as ctx:          # R = 9
+        with pytest.raises(rafi.RafiError):
+            ctx.set_option(rafi.OPT_TILE, 128)
+    with _ctx(48, 1000, 2) as ctx:
+        ctx.set_option(rafi.OPT_SCATTER, rafi.SCATTER_BULK)
+        with pytest.raises(rafi.RafiError):
+            ctx.set_option(rafi.OPT_TILE, 128)
 
 
 @pytest.mark.parametrize("B,tile", [(16, 256), (16, 1024), (16, 2048), (48, 256), (48, 512), (44, 1024),
@@ -477,14 +496,14 @@ def test_diag_redirect_incoming(B, scatter):
 
 @pytest.mark.parametrize("R", [1, 3, 8])
 def test_warp_tiles_many_rounds_empty_ranks_and_resize(R):
-    """The warp-tile path (256-item tiles, R <= 8: k_hist_w, k_scan,
+    """The warp-tile path (128/256-item tiles, R <= 8: k_hist_w, k_scan,
     k_scatter_w) over many forwards on one context: sizes that change every
     round (empty ranks, partial scan blocks and tiles), a resize between
     rounds (new H/O arrays), every round P1-exact against the oracle."""
-    B = 48
+    B = 48 if R != 3 else 96   # 256- and 128-item warp tiles
     sizes = [[5000, 0, 70001], [0, 0, 0], [2048, 2047, 1], [300000, 4096, 0], [1, 0, 123457]]
     with _ctx(B, 300000, R) as ctx:
-        assert ctx.get_option(rafi.OPT_TILE) == 256
+        assert ctx.get_option(rafi.OPT_TILE) == (256 if B == 48 else 128)
         for rnd, ns in enumerate(sizes * 2):
             if rnd == len(sizes):
                 ctx.resize(400000)
