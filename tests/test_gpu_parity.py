@@ -109,10 +109,11 @@ def test_forward_snapshot_parity(B, L, n, pattern, exchange, scatter):
 
 
 @pytest.mark.parametrize("tile", [128, 256, 512, 1024, 4096])
-@pytest.mark.parametrize("B", [24, 48, 64, 128])
+@pytest.mark.parametrize("B", [4, 12, 20, 24, 44, 48, 64, 128])
 def test_tile_sizes(tile, B):
     """Every tile on every path: 128/256 are the warp-tile kernels at R <= 8
-    (8-byte units at 24 B), larger tiles the block-tile ones."""
+    (16-byte units, or the 16-byte chunk gather at 4, 12, 20, 24 and 44 B,
+    where a chunk spans up to four items), larger tiles the block-tile ones."""
     L, n = 4, 20011
     inputs = make_inputs(L, n, B, "uniform", 5 + B)
     with _ctx(B, n * L, L) as ctx:
@@ -124,8 +125,8 @@ def test_tile_sizes(tile, B):
 
 def test_tile_128_needs_the_warp_tile_path():
     """RAFI_OPT_TILE 128 exists only on the warp-tile path (THREADS, R <= 8,
-    item_bytes % 8 == 0)."""
-    with _ctx(44, 1000, 2) as ctx:          # 4-byte units: block tiles only
+    item_bytes % 4 == 0)."""
+    with _ctx(42, 1000, 2) as ctx:          # 2-byte units: block tiles only
         with pytest.raises(rafi.RafiError):
             ctx.set_option(rafi.OPT_TILE, 128)
     with _ctx(48, 1000, 9) as ctx:          # R = 9
