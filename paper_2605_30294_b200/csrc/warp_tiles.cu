@@ -241,15 +241,11 @@ __device__ __forceinline__ void st_global(uint32_t* p, const uint32_t& v) {
   asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// kChunk (4-byte-unit items of 32 B and more, e.g. 44 B): instead of 4-byte
-// unit stores, a lane writes one 16-byte-aligned chunk of a run at a time,
-// gathering its four words from the (one or two) items it covers; the run's
-// first and last chunk go word by word.
-template <typename U, int kWT, bool kChunk>
+template <typename U, int kWT>
 __global__ void __launch_bounds__(kWMaxWarps * 32, 1)
 k_scatter_w(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint8_t* const* __restrict__ dst_table,
             const uint64_t* __restrict__ dst_off, const int* __restrict__ ovf, int L, int R, uint64_t cap, int cur,
-            uint32_t B, uint32_t UPI, FastDiv divU, FastDiv divB, WarpLayout lay, unsigned* __restrict__ wrap_done,
+            uint32_t B, uint32_t UPI, FastDiv divU, WarpLayout lay, unsigned* __restrict__ wrap_done,
             CtrlDev* __restrict__ ctrl_w, const uint64_t* __restrict__ wrap_num_in, PeerCtl pc) {
   if (ovf && *ovf) return;  // collective receive overflow: move nothing (Z3)
   constexpr int kWK = kWT / 32;  // items per lane of a warp tile
@@ -405,92 +401,72 @@ k_scatter_w(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, ui
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < kWK; ++k)
-      if (dk[k] < R) src_of[T[k * 8 + dk[k]] + before[k]] = (uint16_t)(k * 32 + lane);
+      if (dk[k] < R) src_of[T[k * 8 + dk[k]] + before[k]] = (uint16_t)((k * 32 + lane) | (dk[k] << 8));
     __syncwarp();
-    if (kChunk) {
-      // per-run chunk ranges: run d covers bytes [A_d, A_d + cnt_d * B) of its
-      // queue, i.e. chunks (A_d >> 4) .. ((A_d + cnt_d * B + 15) >> 4) - 1;
-      // cp[d] = chunks of runs 0 .. d-1 (T is free again: src_of is built)
-      uint32_t nch = 0;
-      if (lane < R) {
-        const uint32_t cnt = rs[lane + 1] - rs[lane];
-        const uintptr_t A = gb[lane] + (uintptr_t)rs[lane] * B;
-        if (cnt) nch = (uint32_t)(((A + (uintptr_t)cnt * B + 15) >> 4) - (A >> 4));
-      }
-      uint32_t cinc = nch;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, cinc, o);
-        if (lane >= o) cinc += y;
-      }
-      uint32_t* cp = T;
-      if (lane <= R) cp[lane] = cinc - nch;  // cp[R] = all chunks
-      __syncwarp();
-      const uint32_t chunks = cp[R];
+    // destination-major unit moves: lane x of 32 consecutive units, so every
+    // run is written with coalesced stores.  src_of[p] carries the source
+    // slot (low 8 bits) and the destination (high bits) of position p, so a
+    // unit needs no run tracking: its address is gb[d] + p * B + u * |U|.
+    const U* sU = reinterpret_cast<const U*>(st);
+    const uint32_t units = nt * UPI;
+    if (sizeof(U) == 16 || UPI <= 3) {
+      // 16-byte units and items of at most three units: a lane's position
+      // only grows, so it tracks its run (one compare per unit) -- cheaper
+      // here than a third shared load per unit (at R = 8: 48 B 0.95 vs 0.91,
+      // 24 B 0.86 vs 0.80 of HBM)
       int d = 0;
-      uint32_t c0 = 0, c1 = cp[1], p0 = rs[0];
-      uintptr_t A = gb[0] + (uintptr_t)rs[0] * B, E = gb[0] + (uintptr_t)rs[1] * B;
-      for (uint32_t x = lane; x < chunks; x += 32) {
-        while (x >= c1) {
-          ++d;
-          c0 = c1;
-          c1 = cp[d + 1];
-          p0 = rs[d];
-          A = gb[d] + (uintptr_t)p0 * B;
-          E = gb[d] + (uintptr_t)rs[d + 1] * B;
-        }
-        RAFI_DCHECK(d < R, "warp scatter: chunk beyond the last run");
-        const uintptr_t g = ((A >> 4) + (x - c0)) << 4;
-        if (g >= A && g + 16 <= E) {
-          uint32_t o = (uint32_t)(g - A), q = divB.div(o), e = o - q * B;
-          uint32_t wv[4];
+      uint32_t nb = rs[1];
+      uintptr_t base = gb[0];
+      for (uint32_t xb = lane; xb < units; xb += 32 * kWUnroll) {
+        U v[kWUnroll];
+        uint32_t p[kWUnroll], u[kWUnroll];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            wv[k] = *reinterpret_cast<const uint32_t*>(st + (uint32_t)src_of[p0 + q] * B + e);
-            e += 4;
-            if (e >= B) { e -= B; ++q; }
-          }
-          st_global(reinterpret_cast<uint4*>(g), make_uint4(wv[0], wv[1], wv[2], wv[3]));
-        } else {  // the run's first or last chunk: word by word
-          const uintptr_t w0 = g > A ? g : A, w1 = g + 16 < E ? g + 16 : E;
-          for (uintptr_t a = w0; a < w1; a += 4) {
-            const uint32_t o = (uint32_t)(a - A), q = divB.div(o), e = o - q * B;
-            st_global(reinterpret_cast<uint32_t*>(a),
-                      *reinterpret_cast<const uint32_t*>(st + (uint32_t)src_of[p0 + q] * B + e));
+        for (int j = 0; j < kWUnroll; ++j) {
+          const uint32_t x = xb + 32 * j;
+          p[j] = divU.div(x);
+          u[j] = x - p[j] * UPI;
+          if (x < units) v[j] = sU[(src_of[p[j]] & 0xffu) * UPI + u[j]];
+        }
+#pragma unroll
+        for (int j = 0; j < kWUnroll; ++j) {
+          if (xb + 32 * j < units) {
+            while (p[j] >= nb) {
+              ++d;
+              nb = rs[d + 1];
+              base = gb[d];
+            }
+            RAFI_DCHECK(d < R, "warp scatter: position beyond the last run");
+            st_global(reinterpret_cast<U*>(base + (uintptr_t)p[j] * B) + u[j], v[j]);
           }
         }
       }
     } else {
-    // destination-major unit moves: lane x of 32 consecutive units, so every
-    // run is written with coalesced stores; a lane's position only grows, so
-    // its current run only moves forward
-    const U* sU = reinterpret_cast<const U*>(st);
-    const uint32_t units = nt * UPI;
-    int d = 0;
-    uint32_t nb = rs[1];
-    uintptr_t base = gb[0];
-    for (uint32_t x0 = lane; x0 < units; x0 += 32 * kWUnroll) {
+    // 8- and 4-byte units, more than three per item: no run tracking, the
+    // destination comes with the source slot (at R = 8: 20 B 0.64 -> 0.87,
+    // 40 B 0.78 -> 0.83, 44 B 0.50 -> 0.76 of HBM)
+    uint32_t x0 = lane;
+    for (; x0 + 32 * (kWUnroll - 1) < units; x0 += 32 * kWUnroll) {  // whole batches: no bounds checks
       U v[kWUnroll];
-      uint32_t p[kWUnroll], u[kWUnroll];
+      uint32_t p[kWUnroll], u[kWUnroll], inf[kWUnroll];
 #pragma unroll
       for (int j = 0; j < kWUnroll; ++j) {
         const uint32_t x = x0 + 32 * j;
         p[j] = divU.div(x);
         u[j] = x - p[j] * UPI;
-        if (x < units) v[j] = sU[(uint32_t)src_of[p[j]] * UPI + u[j]];
+        inf[j] = src_of[p[j]];
+        v[j] = sU[(inf[j] & 0xffu) * UPI + u[j]];
       }
 #pragma unroll
       for (int j = 0; j < kWUnroll; ++j) {
-        if (x0 + 32 * j < units) {
-          while (p[j] >= nb) {
-            ++d;
-            nb = rs[d + 1];
-            base = gb[d];
-          }
-          RAFI_DCHECK(d < R, "warp scatter: position beyond the last run");
-          st_global(reinterpret_cast<U*>(base + (uintptr_t)p[j] * B) + u[j], v[j]);
-        }
+        RAFI_DCHECK((inf[j] >> 8) < (uint32_t)R && p[j] >= rs[inf[j] >> 8] && p[j] < rs[(inf[j] >> 8) + 1],
+                    "warp scatter: position outside its run");
+        st_global(reinterpret_cast<U*>(gb[inf[j] >> 8] + (uintptr_t)p[j] * B) + u[j], v[j]);
       }
+    }
+    for (; x0 < units; x0 += 32) {  // the tile's last units
+      const uint32_t p = divU.div(x0), u = x0 - p * UPI, inf = src_of[p];
+      RAFI_DCHECK((inf >> 8) < (uint32_t)R, "warp scatter: position beyond the last run");
+      st_global(reinterpret_cast<U*>(gb[inf >> 8] + (uintptr_t)p * B) + u, sU[(inf & 0xffu) * UPI + u]);
     }
     }
     __syncwarp();  // every lane is done with this stage
@@ -549,12 +525,12 @@ int launch_hist_w(Ctx* c, int nsm) {
   return c->tile == 128 ? launch_hist_t<128>(c, nsm) : launch_hist_t<256>(c, nsm);
 }
 
-template <typename U, int kWT, bool kChunk>
+template <typename U, int kWT>
 static int launch_w(Ctx* c, bool fused, bool wrap, PeerCtl pc, int nsm) {
   const int warps = warps_that_fit(kWT, c->B, c->R, c->L);
   const WarpLayout lay = warp_layout(kWT, c->B, c->R, c->L, warps);
   static int granted = 0;
-  auto k = k_scatter_w<U, kWT, kChunk>;
+  auto k = k_scatter_w<U, kWT>;
   if ((int)lay.total > granted) {
     RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
     granted = (int)lay.total;
@@ -564,32 +540,24 @@ static int launch_w(Ctx* c, bool fused, bool wrap, PeerCtl pc, int nsm) {
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)nsm, (tiles_all + warps - 1) / warps));
   k<<<grid, 32 * warps, lay.total, c->stream>>>(c->rank_dev, c->ctrl, fused ? c->in_table_dev : nullptr, c->off_dev,
                                                fused ? c->ovf_dev : nullptr, c->L, c->R, c->cap, c->cur,
-                                               (uint32_t)c->B, UPI, FastDiv(UPI), FastDiv((uint32_t)c->B), lay,
-                                               wrap ? c->done_dev + 1 : nullptr,
+                                               (uint32_t)c->B, UPI, FastDiv(UPI), lay, wrap ? c->done_dev + 1 : nullptr,
                                                c->ctrl, c->plan_dev, pc);
   RAFI_CK_CUDA(cudaGetLastError());
   return RAFI_OK;
 }
 
-// Item sizes that are not a multiple of 16 B, measured at R = 8 (scatter
-// fraction of the copy peak, gpurun_out/r02o_*, r02p_*): 8-byte units beat
-// the 16-byte chunk gather (24 B: 0.86 vs 0.63, 40 B: 0.78 vs 0.54); for
-// 4-byte units the chunk gather wins at 44 B (0.53 vs 0.50) and loses at
-// 20 B (0.56 vs 0.65).  (A gather through two 16-byte shared loads per chunk
-// and a word funnel was slower still, 0.43 at 44 B: random 16-byte shared
-// loads cost four times the wavefronts of 4-byte ones.)
-static bool chunk_gather(uint64_t B) { return B % 8 == 4 && B >= 32; }
-
+// Units: the widest of 16 / 8 / 4 bytes dividing the item size.  (A 16-byte
+// chunk gather for 4-byte-unit items -- each lane assembling an aligned chunk
+// from the words of the one or two items it covers -- was measured and
+// dropped: 44 B at R = 8, 0.53 vs 0.76 of HBM with plain 4-byte units.)
 int launch_scatter_w(Ctx* c, bool fused, bool wrap, PeerCtl pc, int nsm) {
   if (c->tile == 128)
-    return c->B % 16 == 0   ? launch_w<uint4, 128, false>(c, fused, wrap, pc, nsm)
-           : c->B % 8 == 0  ? launch_w<uint2, 128, false>(c, fused, wrap, pc, nsm)
-           : chunk_gather(c->B) ? launch_w<uint32_t, 128, true>(c, fused, wrap, pc, nsm)
-                                : launch_w<uint32_t, 128, false>(c, fused, wrap, pc, nsm);
-  return c->B % 16 == 0   ? launch_w<uint4, 256, false>(c, fused, wrap, pc, nsm)
-         : c->B % 8 == 0  ? launch_w<uint2, 256, false>(c, fused, wrap, pc, nsm)
-         : chunk_gather(c->B) ? launch_w<uint32_t, 256, true>(c, fused, wrap, pc, nsm)
-                              : launch_w<uint32_t, 256, false>(c, fused, wrap, pc, nsm);
+    return c->B % 16 == 0  ? launch_w<uint4, 128>(c, fused, wrap, pc, nsm)
+           : c->B % 8 == 0 ? launch_w<uint2, 128>(c, fused, wrap, pc, nsm)
+                           : launch_w<uint32_t, 128>(c, fused, wrap, pc, nsm);
+  return c->B % 16 == 0  ? launch_w<uint4, 256>(c, fused, wrap, pc, nsm)
+         : c->B % 8 == 0 ? launch_w<uint2, 256>(c, fused, wrap, pc, nsm)
+                         : launch_w<uint32_t, 256>(c, fused, wrap, pc, nsm);
 }
 
 }  // namespace rafi_impl
