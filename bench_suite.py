@@ -325,30 +325,40 @@ def run_cfg4(env, args):
 
 # ----------------------------------------------------------------------------- cfg5 / sweep
 
-def fwd_rate(env, B, n, steps=5, warmup=2, pattern="uniform", graph=False):
-    """emit_bulk + forward of n items/rank, R = world (one rank per GPU).
+def fwd_rate(env, B, n, steps=5, warmup=2, pattern="uniform", graph=False, ranks=0):
+    """emit_bulk + forward of n items/rank, R = ranks (default: world, one
+    rank per GPU; otherwise R / world logical ranks per GPU, sharing one item
+    payload per GPU, each with its own destinations).
     With graph=True the step is also captured as a CUDA graph of
     [emit_bulk + rafi_forward_async] and replayed (device-side G, no host
     synchronisation per step): the per-step latency without host overhead."""
     import synth
     torch = env.torch
     N = env.world
+    R = ranks or N
+    L = R // N
     # payload bytes only matter for throughput here (parity is tested elsewhere): device RNG
     gen = torch.Generator(device=env.dev)
     gen.manual_seed(synth.CONFIG_SEEDS[5] + env.rank)
     items = torch.randint(0, 256, (n, B), dtype=torch.uint8, device=env.dev, generator=gen)
-    ds = synth.make_dests(pattern, synth.CONFIG_SEEDS[5], env.rank, 0, n, N)
-    dests = torch.from_numpy(ds).to(env.dev)
+    dests = [torch.from_numpy(synth.make_dests(pattern, synth.CONFIG_SEEDS[5], env.rank * L + l, 0, n, R)).to(env.dev)
+             for l in range(L)]
     side = torch.cuda.Stream(device=env.dev)
-    ctx = env.configure(env.rafi.Context(B, n + n // 8 + 4096, comm=env.comm, stream=side, device=env.local))
+    ctx = env.configure(env.rafi.Context(B, n + n // 8 + 4096, comm=env.comm, stream=side, device=env.local,
+                                         local_ranks=L))
     saved, env.stream = env.stream, side
+
+    def emit_all():
+        for l in range(L):
+            ctx.emit_bulk(items, dests[l], n, local=l)
+
     for _ in range(warmup):
-        ctx.emit_bulk(items, dests, n)
+        emit_all()
         ctx.forward()
 
     def loop():
         for _ in range(steps):
-            ctx.emit_bulk(items, dests, n)
+            emit_all()
             ctx.forward()
 
     ms, _ = env.timed(loop)  # un-instrumented: blocking forwards replay their cached graph
@@ -356,17 +366,23 @@ def fwd_rate(env, B, n, steps=5, warmup=2, pattern="uniform", graph=False):
     ms_instr, _ = env.timed(loop)  # instrumented pass: CUDA events between launches, for scatter_ms
     st = ctx.stats()
     scat = st["acc_ms_scatter"] / max(st["acc_forwards"], 1)
-    remote = st["bytes_sent_remote"]
-    out = {"items_per_rank": n, "item_bytes": B, "ms_per_step": ms / steps, "instrumented_ms_per_step": ms_instr / steps,
-           "value": N * n * steps / (ms / 1e3), "unit": "items/s",
+    Cm = ctx.matrix()  # bytes this GPU pushes to other GPUs per forward
+    mine = slice(env.rank * L, env.rank * L + L)
+    remote = (int(Cm[mine, :].sum()) - int(Cm[mine, mine].sum())) * B
+    out = {"items_per_rank": n, "item_bytes": B, "ranks": R, "local_ranks": L, "ms_per_step": ms / steps,
+           "instrumented_ms_per_step": ms_instr / steps,
+           "value": R * n * steps / (ms / 1e3), "unit": "items/s",
            "scatter": {1: "threads", 2: "bulk"}[ctx.get_option(env.rafi.OPT_SCATTER)],
-           "tile": ctx.get_option(env.rafi.OPT_TILE), "scatter_ms": scat, "scatter_hbm_gbs": n * (2 * B + 4) / (scat / 1e3) / 1e9,
+           "tile": ctx.get_option(env.rafi.OPT_TILE), "scatter_ms": scat,
+           "scatter_hbm_gbs": L * n * (2 * B + 4) / (scat / 1e3) / 1e9,
+           "binning_ms": (st["acc_ms_hist"] + st["acc_ms_scan"] + st["acc_ms_scatter"]) / max(st["acc_forwards"], 1),
            "nvlink_gbs_per_gpu": (remote / (scat / 1e3) / 1e9) if N > 1 else None}
+    out["binning_hbm_frac"] = L * n * (2 * B + 8) / (out["binning_ms"] / 1e3) / 1e9 / 6457.1
     if graph:
         ctx.set_option(env.rafi.OPT_TIMING, 0)
         G_dev = torch.zeros(1, dtype=torch.int64, device=env.dev)
         ctx.capture_begin()
-        ctx.emit_bulk(items, dests, n)
+        emit_all()
         ctx.forward_async(G_dev)
         ex = ctx.capture_end()
         for _ in range(3):
@@ -374,11 +390,11 @@ def fwd_rate(env, B, n, steps=5, warmup=2, pattern="uniform", graph=False):
         K = 50
         msg, _ = env.timed(lambda: [ctx.graph_launch(ex) for _ in range(K)])
         side.synchronize()
-        assert int(G_dev.item()) == N * n
+        assert int(G_dev.item()) == R * n
         ctx.sync_host()
         env.rafi.Context.graph_destroy(ex)
         out["graph_ms_per_step"] = msg / K
-        out["graph_value"] = N * n * K / (msg / 1e3)
+        out["graph_value"] = R * n * K / (msg / 1e3)
     env.stream = saved
     ctx.close()
     del items, dests
@@ -391,11 +407,12 @@ def run_cfg5(env, args):
     sizes = [int(x) for x in args.sizes.split(",")] if args.sizes else [16, 24, 32, 40, 44, 48, 64, 96, 128]
     for B in sizes:
         try:
-            r = fwd_rate(env, B, n)
+            r = fwd_rate(env, B, n, ranks=args.ranks)
         except env.rafi.RafiError as e:  # e.g. a --tile that does not fit this item size
             env.emit({"item_bytes": B, "skipped": str(e)})
             continue
-        r["workload"] = "cfg5: uniform all-to-all over R=%d, %d items/rank, %d-B items" % (env.world, n, B)
+        r["workload"] = "cfg5: uniform all-to-all over R=%d, %d items/rank, %d-B items, %d logical rank(s) per GPU" % (
+            r["ranks"], n, B, r["local_ranks"])
         env.emit(r)
 
 
@@ -415,6 +432,7 @@ def main():
     p.add_argument("--tile", type=int, default=0, help="RAFI_OPT_TILE (0 = automatic)")
     p.add_argument("--control", default="auto", choices=["auto", "nccl", "peer"])
     p.add_argument("--sizes", default="", help="cfg5: comma-separated item sizes (default: the full sweep)")
+    p.add_argument("--ranks", type=int, default=8, help="cfg5: ranks R (configs[4]: 8), R / N logical ranks per GPU")
     args = p.parse_args()
     env = Env(args)
     {"cfg1": run_cfg1, "cfg3": run_cfg3, "cfg4": run_cfg4, "cfg5": run_cfg5, "sweep": run_sweep,
