@@ -5,6 +5,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "internal.h"
 
@@ -152,6 +155,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+// Dynamic shared memory above 48 KiB is opted into per kernel AND per device
+// (every device has its own context): remember the largest grant per pair.
+inline cudaError_t ensure_smem(const void* fn, int bytes, int device) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> granted;
+  std::lock_guard<std::mutex> lock(mu);
+  int& have = granted[{fn, device}];
+  if (bytes <= have) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
 }
 
 // ---------------------------------------------------------------- warp-tile path (warp_tiles.cu)

@@ -1198,12 +1198,8 @@ int launch_scan(Ctx* c, int plan_mode, unsigned long long* G_out, bool ctl) {
 
 template <typename U, bool kSI, int kK, int kMinB, bool kChunk>
 static int launch_scatter_kk(Ctx* c, bool fused, bool wrap, uint32_t UPI, int grid, const ScatterLayout& lay) {
-  static int granted = 0;  // per instantiation: the largest smem opt-in already granted
   auto k = k_scatter<U, kSI, kK, kMinB, kChunk>;
-  if ((int)lay.total > granted) {
-    RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
-    granted = (int)lay.total;
-  }
+  RAFI_CK_CUDA(ensure_smem((const void*)k, (int)lay.total, c->device));
   k<<<grid, kThreads, lay.total, c->stream>>>(rank_table(c), c->ctrl, fused ? c->in_table_dev : nullptr, c->off_dev,
                                              fused ? c->ovf_dev : nullptr, c->L, c->R, c->cap,
                                              c->tile, c->cur, (uint32_t)c->B, UPI, FastDiv(UPI),
@@ -1275,12 +1271,8 @@ uint32_t choose_tile_perm(uint64_t B, int R) {
 template <typename U, int kK, int kMinB>
 static int launch_perm_k(Ctx* c, bool fused, bool wrap, uint32_t UPI, int grid) {
   const BulkLayout lay = bulk_layout(c->tile, c->B, c->R, perm_nobuf(c->tile, c->B, c->R));
-  static int granted = 0;  // per instantiation: the largest smem opt-in already granted
   auto k = k_scatter_perm<U, kK, kMinB>;
-  if ((int)lay.total > granted) {
-    RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
-    granted = (int)lay.total;
-  }
+  RAFI_CK_CUDA(ensure_smem((const void*)k, (int)lay.total, c->device));
   k<<<grid, kThreads, lay.total, c->stream>>>(rank_table(c), c->ctrl, fused ? c->in_table_dev : nullptr, c->off_dev,
                                              fused ? c->ovf_dev : nullptr, c->L, c->R, c->cap, c->tile, c->cur,
                                              (uint32_t)c->B, UPI, lay, wrap ? c->done_dev + 1 : nullptr, c->ctrl,

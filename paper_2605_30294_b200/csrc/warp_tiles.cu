@@ -509,11 +509,7 @@ uint32_t warp_tile_for(uint64_t B, int R, int L) {
 template <int kWT>
 static int launch_hist_t(Ctx* c, int nsm) {
   const uint32_t sm = hist_w_smem<kWT>(c->L);
-  static uint32_t granted = 0;
-  if (sm > granted) {
-    RAFI_CK_CUDA(cudaFuncSetAttribute(k_hist_w<kWT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    granted = sm;
-  }
+  RAFI_CK_CUDA(ensure_smem((const void*)k_hist_w<kWT>, (int)sm, c->device));
   const uint64_t blocks = (c->max_tiles + kHistTilesPerCta - 1) / kHistTilesPerCta * (uint64_t)c->L;
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)nsm, (blocks + kHWarps - 1) / kHWarps));
   k_hist_w<kWT><<<grid, kHWarps * 32, sm, c->stream>>>(c->rank_dev, c->ctrl, c->L, c->R, c->cap);
@@ -529,12 +525,8 @@ template <typename U, int kWT>
 static int launch_w(Ctx* c, bool fused, bool wrap, PeerCtl pc, int nsm) {
   const int warps = warps_that_fit(kWT, c->B, c->R, c->L);
   const WarpLayout lay = warp_layout(kWT, c->B, c->R, c->L, warps);
-  static int granted = 0;
   auto k = k_scatter_w<U, kWT>;
-  if ((int)lay.total > granted) {
-    RAFI_CK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total));
-    granted = (int)lay.total;
-  }
+  RAFI_CK_CUDA(ensure_smem((const void*)k, (int)lay.total, c->device));
   const uint32_t UPI = (uint32_t)(c->B / sizeof(U));
   const uint64_t tiles_all = c->max_tiles * (uint64_t)c->L;
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)nsm, (tiles_all + warps - 1) / warps));
