@@ -292,10 +292,12 @@ static constexpr size_t kMaxSmem = 227u * 1024u;  // opt-in shared memory per CT
 static int resolve_scatter(Ctx* c) {
   int x = c->scatter;
   if (x == RAFI_SCATTER_AUTO) {
-    // BULK where the scatter pushes runs to NVLink peers (measured faster there:
-    // DESIGN.md section 6); THREADS for local HBM (faster at every item size)
+    // BULK where the scatter pushes runs of 24 B and larger items to NVLink
+    // peers (measured faster there at N=2 and N=4 by 0-13%, DESIGN.md section
+    // 6); THREADS for local HBM (faster at every item size) and for 16-B items
+    // (N=2: 87 vs 66 G items/s; N=4: 130 vs 133)
     const bool remote_push = c->nprocs > 1 && c->exchange_eff == RAFI_EXCHANGE_FUSED;
-    x = remote_push && perm_supported(c->B) && perm_smem_bytes(256, c->B, c->R) <= kMaxSmem
+    x = remote_push && c->B >= 24 && perm_supported(c->B) && perm_smem_bytes(256, c->B, c->R) <= kMaxSmem
             ? RAFI_SCATTER_BULK
             : RAFI_SCATTER_THREADS;
   }
