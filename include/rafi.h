@@ -115,7 +115,10 @@ typedef struct {
 #define RAFI_OPT_TIMING 2          /* 1 = record per-phase CUDA events (forward: adds one event sync;
                                       bulk emit: events around the kernel); setting it resets the
                                       accumulated sums in rafi_stats; default 0 */
-#define RAFI_OPT_TILE 3            /* binning tile in items (256 * 2^k, k <= 4); 0 = auto from item size */
+#define RAFI_OPT_TILE 3            /* binning tile in items: 256 * 2^k (k <= 4), or 128 on the warp-tile path
+                                      (THREADS, R <= 8, item_bytes % 4 == 0; RAFI_ERR_INVALID_ARG
+                                      otherwise); 0 = auto from item size and R (warp tiles of 256 or 128
+                                      items at R <= 8, block tiles otherwise) */
 #define RAFI_OPT_SELF_DIRECT 4     /* reserved (self run placement); 0 */
 #define RAFI_OPT_CONTROL 7         /* count exchange and completion barrier of FUSED forwards:
                                       RAFI_CONTROL_* (default AUTO).  Every rank must use the same setting */
@@ -134,11 +137,14 @@ typedef struct {
                                       pinned it.  RAFI_ERR_UNSUPPORTED if BULK is asked for an item size
                                       that is not a multiple of 4 or a tile that does not fit */
 
-#define RAFI_SCATTER_AUTO 0        /* BULK when the scatter pushes runs to NVLink peers (FUSED over several
-                                      processes) and BULK is supported, else THREADS (measured winners) */
-#define RAFI_SCATTER_THREADS 1     /* threads store every run with coalesced stores: 16/8/4/2/1-B item units,
-                                      or, for 4-B units (item_bytes % 8 == 4, >= 16), 16-B-aligned chunks
-                                      gathered from the (at most two) items they cover */
+#define RAFI_SCATTER_AUTO 0        /* BULK when the scatter pushes runs of items of >= 24 B to NVLink peers
+                                      (FUSED over several processes) and BULK is supported, else THREADS
+                                      (measured winners) */
+#define RAFI_SCATTER_THREADS 1     /* threads store every run with coalesced stores.  R <= 8 and
+                                      item_bytes % 4 == 0: one warp per 128/256-item tile, 16/8/4-B item
+                                      units.  Otherwise block tiles: 16/8/4/2/1-B item units, or, for 4-B
+                                      units (item_bytes % 8 == 4, >= 16), 16-B-aligned chunks gathered
+                                      from the (at most two) items they cover */
 #define RAFI_SCATTER_BULK 2        /* runs are permuted in shared memory and written by TMA bulk stores
                                       (cp.async.bulk shared->global, local or NVLink peer); threads write
                                       only the unaligned < 16-B heads and tails; item_bytes % 4 == 0 */
