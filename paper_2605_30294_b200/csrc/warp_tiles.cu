@@ -1,30 +1,32 @@
 // warp_tiles.cu -- the warp-tile binning path (a2 histogram + a4 stable
-// scatter) for R <= 8 destinations and item sizes that are a multiple of 8 B.
+// scatter) for R <= 8 destinations and item sizes that are a multiple of 4 B.
 //
-// The binning tile is 256 items and ONE WARP owns a whole tile, from the TMA
-// load to the last store, so the scatter needs no block-level barrier at all:
+// The binning tile is 256 items (128 for items of 96 B and more) and ONE WARP
+// owns a whole tile, from the TMA load to the last store, so the scatter
+// needs no block-level barrier at all:
 //
-//   k_hist_w     a2  persistent; one warp counts one scan block (8 tiles,
-//                    2048 dests) at a time, streamed through a private
-//                    three-stage ring of 8-KiB TMA bulk loads: per-lane byte
-//                    counters, a 31-shuffle butterfly reduce-scatter that
-//                    leaves lane j with word j of the 8 x 8 count table, and
-//                    the in-block prefix (O) and block total (H) -- the same
+//   k_hist_w     a2  persistent; one warp counts one scan block (8 tiles) at
+//                    a time, streamed through a private three-stage ring of
+//                    TMA bulk loads: per-lane byte counters, a 31-shuffle
+//                    butterfly reduce-scatter that leaves lane j with word j
+//                    of the 8 tiles x 8 destinations count table, and the
+//                    in-block prefix (O) and block total (H) -- the same
 //                    two-level layout k_scan and both scatters read.
 //   k_scatter_w  a4  persistent, one CTA per SM of up to 16 independent warps.
 //                    Each warp streams its tiles through a private two-stage
 //                    ring of 1-D TMA bulk loads (items + dests, mbarrier
 //                    completion), ranks the tile's items among same-destination
-//                    items in slot order (__match_any_sync), and
-//                    writes every destination run with coalesced 16/8-byte
-//                    unit stores straight into the destination queue (the local
-//                    send batch, the local incoming queue, or -- FUSED -- a
-//                    peer's incoming queue over NVLink).
+//                    items in slot order (__match_any_sync and a chunk x
+//                    destination table), and writes every
+//                    destination run with coalesced 16/8/4-byte unit stores
+//                    straight into the destination queue (the local send
+//                    batch, the local incoming queue, or -- FUSED -- a peer's
+//                    incoming queue over NVLink).
 //
 // Why (profiles/r02_binning_r8.md): the block-tile scatter of kernels.cu pays
 // ~6 __syncthreads per tile; at R = 8 its warps spend a third of their time
 // in barriers and the kernel reaches 0.65 of HBM.  Here a warp only ever waits
-// for its own data.
+// for its own data: 0.90-0.96 of HBM for 16-B-multiple items at R = 8.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -56,7 +58,6 @@ constexpr int kHStages = 3;     // TMA ring depth per warp
 template <int kWT>
 struct HistBlk {
   static constexpr uint32_t kBlk = kWT * kHistTilesPerCta;
-  static constexpr int kVec = kWT / 16;     // int4 per lane per block
   static constexpr int kPerTile = kWT / 128;  // int4 per lane per tile
 };
 
