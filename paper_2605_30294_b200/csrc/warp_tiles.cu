@@ -47,6 +47,10 @@ namespace rafi_impl {
 constexpr int kWStages = RAFI_W_STAGES;   // TMA ring depth per warp
 constexpr int kWMaxWarps = 16;
 constexpr int kWUnroll = RAFI_W_UNROLL;   // independent unit moves in flight per lane
+#ifndef RAFI_W_UNROLL_NARROW
+#define RAFI_W_UNROLL_NARROW 8
+#endif
+constexpr int kWUnrollNarrow = RAFI_W_UNROLL_NARROW;  // the same for the untracked 8/4-byte-unit loop
 constexpr uint32_t kWSmemMax = 227u * 1024u;
 
 // ---------------------------------------------------------------- a2 histogram
@@ -446,11 +450,11 @@ k_scatter_w(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, ui
     // destination comes with the source slot (at R = 8: 20 B 0.64 -> 0.87,
     // 40 B 0.78 -> 0.83, 44 B 0.50 -> 0.76 of HBM)
     uint32_t x0 = lane;
-    for (; x0 + 32 * (kWUnroll - 1) < units; x0 += 32 * kWUnroll) {  // whole batches: no bounds checks
-      U v[kWUnroll];
-      uint32_t p[kWUnroll], u[kWUnroll], inf[kWUnroll];
+    for (; x0 + 32 * (kWUnrollNarrow - 1) < units; x0 += 32 * kWUnrollNarrow) {  // whole batches: no bounds checks
+      U v[kWUnrollNarrow];
+      uint32_t p[kWUnrollNarrow], u[kWUnrollNarrow], inf[kWUnrollNarrow];
 #pragma unroll
-      for (int j = 0; j < kWUnroll; ++j) {
+      for (int j = 0; j < kWUnrollNarrow; ++j) {
         const uint32_t x = x0 + 32 * j;
         p[j] = divU.div(x);
         u[j] = x - p[j] * UPI;
@@ -458,7 +462,7 @@ k_scatter_w(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, ui
         v[j] = sU[(inf[j] & 0xffu) * UPI + u[j]];
       }
 #pragma unroll
-      for (int j = 0; j < kWUnroll; ++j) {
+      for (int j = 0; j < kWUnrollNarrow; ++j) {
         RAFI_DCHECK((inf[j] >> 8) < (uint32_t)R && p[j] >= rs[inf[j] >> 8] && p[j] < rs[(inf[j] >> 8) + 1],
                     "warp scatter: position outside its run");
         st_global(reinterpret_cast<U*>(gb[inf[j] >> 8] + (uintptr_t)p[j] * B) + u[j], v[j]);
