@@ -7,7 +7,7 @@
 //
 //   k_hist_w     a2  persistent; one warp counts one scan block (8 tiles) at
 //                    a time, streamed through a private three-stage ring of
-//                    TMA bulk loads: per-lane byte counters, a 31-shuffle
+//                    TMA bulk loads: per-lane 4-bit counters, a 31-shuffle
 //                    butterfly reduce-scatter that leaves lane j with word j
 //                    of the 8 tiles x 8 destinations count table, and the
 //                    in-block prefix (O) and block total (H) -- the same
@@ -133,29 +133,31 @@ __global__ void __launch_bounds__(kHWarps * 32, 1) k_hist_w(const RankDev* __res
     mbar_wait(&mbar[it % kHStages], (it / kHStages) & 1);
     const int4* d4 = reinterpret_cast<const int4*>(my + (it % kHStages) * kHBlk * 4);
     // int4 q = 32 i + lane holds dests 4q .. 4q+3, in tile 4q / kWT = i / kPerTile.
-    // Per tile, byte d of c counts destination d among this lane's 4 kPerTile dests
-    // (every queued dest is in [0, R), R <= 8: invalid ones were rejected at
-    // emit); then widened to 16-bit fields, even and odd destinations apart:
-    //   word 4t+0: dests 0, 2   4t+1: 4, 6   4t+2: 1, 3   4t+3: 5, 7
+    // Per tile, nibble d of c counts destination d among this lane's
+    // 4 kPerTile <= 8 dests (every queued dest is in [0, R), R <= 8: invalid
+    // ones were rejected at emit) -- one shift and one add per dest -- then
+    // widened to 16-bit fields:  word 4t+k holds dests k and k+4
     uint32_t a[32];
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
-      uint64_t c = 0;
+      uint32_t c = 0;
 #pragma unroll
       for (int h = 0; h < HistBlk<kWT>::kPerTile; ++h) {
         const int i = HistBlk<kWT>::kPerTile * t + h;
         const int4 v = d4[i * 32 + lane];
         const int e[4] = {v.x, v.y, v.z, v.w};
-        const uint64_t e0 = i0 + (uint64_t)(i * 32 + lane) * 4;
+        if (full) {
 #pragma unroll
-        for (int m = 0; m < 4; ++m)
-          if (full || e0 + m < n) c += 1ull << ((unsigned)e[m] << 3);
+          for (int m = 0; m < 4; ++m) c += 1u << ((unsigned)e[m] << 2);
+        } else {
+          const uint64_t e0 = i0 + (uint64_t)(i * 32 + lane) * 4;
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+            if (e0 + m < n) c += 1u << ((unsigned)e[m] << 2);
+        }
       }
-      const uint64_t ev = c & 0x00FF00FF00FF00FFull, od = (c >> 8) & 0x00FF00FF00FF00FFull;
-      a[4 * t + 0] = (uint32_t)ev;
-      a[4 * t + 1] = (uint32_t)(ev >> 32);
-      a[4 * t + 2] = (uint32_t)od;
-      a[4 * t + 3] = (uint32_t)(od >> 32);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) a[4 * t + k] = (c >> (4 * k)) & 0x000F000Fu;
     }
     __syncwarp();  // every lane has read the stage
     if (lane == 0) {
@@ -190,7 +192,7 @@ __global__ void __launch_bounds__(kHWarps * 32, 1) k_hist_w(const RankDev* __res
     const uint64_t t = b * kHistTilesPerCta + (lane >> 2);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int d = (k & 1) * 4 + (k >> 1) + 2 * h;
+      const int d = k + 4 * h;
       if (d < R) {
         if (t < tiles) rk[l].O[(uint64_t)d * tiles + t] = (excl >> (16 * h)) & 0xffffu;
         if ((lane >> 2) == kHistTilesPerCta - 1) rk[l].H[(uint64_t)d * nblk + b] = (tot >> (16 * h)) & 0xffffu;

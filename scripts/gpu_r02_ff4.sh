@@ -1,0 +1,10 @@
+# 4 GPUs: final tree -- every GPU test with 4 GPUs visible (single + multi-GPU), smoke, bench N=1/2/4, reference arm
+RUN2="python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29571"
+RUN4="python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29572"
+timeout 3000 python -m pytest tests -x -q -p no:cacheprovider -m gpu --timeout 900 > gpurun_out/r02ff_tests_4gpu.log 2>&1; echo rc=$? >> gpurun_out/r02ff_tests_4gpu.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02ff_smoke.log 2>&1; echo rc=$? >> gpurun_out/r02ff_smoke.log
+timeout 600 python bench.py > gpurun_out/r02ff_bench_n1.json 2> gpurun_out/r02ff_bench_n1.err
+timeout 600 $RUN2 bench.py --gpus 2 > gpurun_out/r02ff_bench_n2.json 2> gpurun_out/r02ff_bench_n2.err
+timeout 600 $RUN4 bench.py --gpus 4 > gpurun_out/r02ff_bench_n4.json 2> gpurun_out/r02ff_bench_n4.err
+timeout 300 python bench.py --impl reference > gpurun_out/r02ff_ref_n1.json 2> gpurun_out/r02ff_ref_n1.err
+echo done

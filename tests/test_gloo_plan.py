@@ -3,18 +3,17 @@ counts its own row, the rows are all-gathered (the count exchange),
 and rafi_plan on every rank yields the oracle's receive plan and the same G
 and overflow decision."""
 import os
-import socket
+import tempfile
+import uuid
 
 import numpy as np
 import pytest
 
 
 def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
+    """A fresh file:// rendezvous for the gloo group (no TCP port to race for:
+    a port probed free and then bound by the workers can be taken in between)."""
+    return "file://" + os.path.join(tempfile.gettempdir(), "rafi_pg_%d_%s" % (os.getpid(), uuid.uuid4().hex))
 
 
 def _worker(rank, world, port, cap, n):
@@ -25,9 +24,7 @@ def _worker(rank, world, port, cap, n):
     import synth
     from paper_2605_30294_b200 import build, rafi
 
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", init_method=port, rank=rank, world_size=world)
     ds = synth.make_dests("skewed", 3, rank, 0, n, world)
     row = torch.from_numpy(np.bincount(ds, minlength=world).astype(np.int64))
     rows = [torch.zeros(world, dtype=torch.int64) for _ in range(world)]

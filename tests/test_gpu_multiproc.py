@@ -3,7 +3,8 @@ transports (PEER copy kernel over CUDA-IPC NVLink pointers; NCCL grouped
 send/recv).  Every rank checks its own outputs bit-exactly against the oracle
 run on all ranks' snapshots (P1)."""
 import os
-import socket
+import tempfile
+import uuid
 
 import numpy as np
 import pytest
@@ -26,11 +27,9 @@ def _need(world):
 
 
 def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
+    """A fresh file:// rendezvous for the gloo group (no TCP port to race for:
+    a port probed free and then bound by the workers can be taken in between)."""
+    return "file://" + os.path.join(tempfile.gettempdir(), "rafi_pg_%d_%s" % (os.getpid(), uuid.uuid4().hex))
 
 
 def _worker(rank, world, port, B, n, pattern, exchange, rounds, scatter=1, control=0, comm_mode="nccl"):
@@ -43,10 +42,8 @@ def _worker(rank, world, port, B, n, pattern, exchange, rounds, scatter=1, contr
     import synth
     from paper_2605_30294_b200 import rafi
 
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(rank)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", init_method=port, rank=rank, world_size=world)
     comm = None
     if comm_mode in ("nccl", "both"):
         obj = [rafi.nccl_unique_id() if rank == 0 else None]
@@ -146,10 +143,8 @@ def _worker_hybrid(rank, world, port, L, B, n, graph, scatter=1):
     import synth
     from paper_2605_30294_b200 import rafi
 
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(rank)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", init_method=port, rank=rank, world_size=world)
     obj = [rafi.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     comm = rafi.nccl_comm_init(world, rank, obj[0], rank)

@@ -19,7 +19,8 @@ so the two processes' kernels may time-slice freely.  Every round is checked
 bit-exactly against the oracle run on both processes' snapshots (P1).
 """
 import os
-import socket
+import tempfile
+import uuid
 
 import numpy as np
 import pytest
@@ -32,11 +33,9 @@ if not torch.cuda.is_available():
 
 
 def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
+    """A fresh file:// rendezvous for the gloo group (no TCP port to race for:
+    a port probed free and then bound by the workers can be taken in between)."""
+    return "file://" + os.path.join(tempfile.gettempdir(), "rafi_pg_%d_%s" % (os.getpid(), uuid.uuid4().hex))
 
 
 def _worker(rank, world, port, B, L, n, pattern, exchange, rounds, resize_round):
@@ -46,10 +45,8 @@ def _worker(rank, world, port, B, L, n, pattern, exchange, rounds, resize_round)
     import synth
     from paper_2605_30294_b200 import rafi
 
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", init_method=port, rank=rank, world_size=world)
     R = world * L
     cap = R * n  # any pattern fits (all_to_one sends everything to one rank)
     stream = torch.cuda.Stream()
@@ -111,10 +108,8 @@ def _worker_mismatch(rank, world, port):
 
     from paper_2605_30294_b200 import rafi
 
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", init_method=port, rank=rank, world_size=world)
     # the processes disagree on the capacity: creation fails on BOTH
     with pytest.raises(rafi.RafiError) as e:
         rafi.Context(32, 1000 + rank, bootstrap=(world, rank, rafi.torch_allgather()))
