@@ -202,3 +202,31 @@ def test_multigpu_hybrid_local_ranks(world, L, graph, scatter):
     import torch.multiprocessing as mp
     mp.spawn(_worker_hybrid, args=(world, _free_port(), L, 44, 20011, graph, scatter), nprocs=world,
              join=True)
+
+
+@pytest.mark.parametrize("scatter", [1, 2])  # THREADS (warp tiles), BULK
+def test_diag_redirect_to_peer_device(scatter):
+    """One process, two GPUs: rank 1's incoming queue of a 2-rank context on
+    cuda:0 is redirected to a buffer on cuda:1 (rafi_diag_redirect_incoming
+    enables peer access), so the scatter pushes rank 1's block over NVLink
+    -- the bytes that land on cuda:1 are exactly the oracle's incoming queue
+    of rank 1, and rank 0's own queue is untouched."""
+    from helpers import make_inputs, snapshot_world
+    from paper_2605_30294_b200 import rafi
+    B, L, n = 48, 2, 200003
+    inputs = make_inputs(L, n, B, "uniform", 77)
+    torch.cuda.set_device(0)
+    with rafi.Context(B, L * n, local_ranks=L, device=0) as ctx:
+        ctx.set_option(rafi.OPT_SCATTER, scatter)
+        buf = torch.zeros(L * n * B + 16, dtype=torch.uint8, device="cuda:1")
+        ctx.diag_redirect_incoming(1, buf)
+        for l, (it, ds) in enumerate(inputs):
+            ctx.emit_bulk(torch.from_numpy(it).cuda(0), torch.from_numpy(ds).cuda(0), n, local=l)
+        w, _ = snapshot_world(ctx, L, B)
+        assert ctx.forward() == w.forward()
+        m = ctx.num_incoming(1)
+        assert m == w.num_incoming(1)
+        torch.cuda.synchronize(1)
+        assert np.array_equal(buf[: m * B].cpu().numpy().reshape(m, B), w.incoming(1))
+        assert np.array_equal(ctx.read_incoming(0), w.incoming(0))
+        ctx.diag_redirect_incoming(1, None)
