@@ -511,13 +511,15 @@ static int enqueue_fused(Ctx* c, unsigned long long* G_dev, bool T) {
   const int R = c->R, L = c->L;
   c->fwd_launches = 0;
   if (T) RAFI_CK_CUDA(record_ev(c, 0));
-  RAFI_CK(launch_hist(c));
-  if (T) RAFI_CK_CUDA(record_ev(c, 1));
   // a3 (+ a5's plan when this process holds every rank: the scan's last block
   // plans; with peer control it first exchanges the counts through the
-  // mailboxes, so one kernel does scan + count exchange + plan)
+  // mailboxes, so one kernel does scan + count exchange + plan -- on small
+  // warp-tile forwards the histogram's last CTA does all of it)
   const bool peer = c->nprocs > 1 && c->ctl_peer;
-  RAFI_CK(launch_scan(c, (c->nprocs == 1 || peer) ? 2 : 0, G_dev, peer));
+  const int pm = (c->nprocs == 1 || peer) ? 2 : 0;
+  RAFI_CK(launch_hist(c, pm, G_dev, peer));
+  if (T) RAFI_CK_CUDA(record_ev(c, 1));
+  RAFI_CK(launch_scan(c, pm, G_dev, peer));
   if (T) RAFI_CK_CUDA(record_ev(c, 2));
   if (c->nprocs > 1 && !peer) {
     // a5: the whole R x R matrix on every rank; offsets + overflow on device
@@ -594,7 +596,7 @@ static int64_t forward_fused_host(Ctx* c) {
   const bool T = c->timing;
   c->fwd_launches = 0;
   if (T) RAFI_CK_CUDA(record_ev(c, 0));
-  RAFI_CK(launch_hist(c));
+  RAFI_CK(launch_hist(c, 0, nullptr, false));
   if (T) RAFI_CK_CUDA(record_ev(c, 1));
   RAFI_CK(launch_scan(c, 0, nullptr, false));
   if (T) RAFI_CK_CUDA(record_ev(c, 2));
@@ -736,7 +738,7 @@ static int64_t forward_staged(Ctx* c) {
   const bool T = c->timing;
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[0], c->stream));
   // a2-a4: bin every local rank's outgoing batch by destination
-  RAFI_CK(launch_hist(c));
+  RAFI_CK(launch_hist(c, 1));
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[1], c->stream));
   RAFI_CK(launch_scan(c, 1));  // + the send offsets, by the scan's last block
   if (T) RAFI_CK_CUDA(cudaEventRecord(c->ev[2], c->stream));

@@ -157,6 +157,92 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 
+// ---------------------------------------------------------------- a5 plan (device part)
+
+// Per-destination bases of local rank l (global g) from the count matrix
+// (PAPER:124-126), run by one whole block:
+//   staged (fused = false, row g only): dst_off[d] = send_off_g[d]
+//     = sum_{d'<d} C[g][d'] (where d's block starts in g's send batch);
+//   FUSED (all rows, after the all-gather): dst_off[d] = recv_off_d[g]
+//     = sum_{s<g} C[s][d] (where g's block starts in d's incoming queue),
+//     *num_in = sum_s C[s][g], and the collective overflow decision (Z3) and
+//     G = sum of all entries accumulated into *s_ovf / *s_G
+//     (block-shared).
+static __device__ void plan_block(const uint64_t* __restrict__ C, int g, int R, uint64_t cap, bool fused,
+                           uint64_t* __restrict__ dst_off, uint64_t* __restrict__ num_in, int* s_ovf,
+                           unsigned long long* s_G) {
+  for (int d = threadIdx.x; d < R; d += blockDim.x) {
+    if (fused) {
+      uint64_t recv_off = 0, col = 0;
+      for (int s = 0; s < R; ++s) {
+        const uint64_t c = C[(uint64_t)s * R + d];
+        if (s < g) recv_off += c;
+        col += c;
+      }
+      dst_off[d] = recv_off;
+      if (col > cap) *s_ovf = 1;
+      if (d == g) *num_in = col;
+      if (s_G) atomicAdd(s_G, (unsigned long long)col);
+    } else {
+      uint64_t send_off = 0;
+      for (int e = 0; e < d; ++e) send_off += C[(uint64_t)g * R + e];
+      dst_off[d] = send_off;
+    }
+  }
+}
+
+// Plan of every local rank by the calling block; writes *ovf and *G_out (FUSED).
+static __device__ void plan_all(const uint64_t* __restrict__ C, int grank0, int L, int R, uint64_t cap, bool fused,
+                         uint64_t* __restrict__ dst_off, uint64_t* __restrict__ num_in, int* __restrict__ ovf,
+                         unsigned long long* __restrict__ G_out) {
+  __shared__ int s_ovf;
+  __shared__ unsigned long long s_G;
+  if (threadIdx.x == 0) { s_ovf = 0; s_G = 0; }
+  __syncthreads();
+  for (int l = 0; l < L; ++l)
+    plan_block(C, grank0 + l, R, cap, fused, dst_off + (uint64_t)l * R, num_in + l, &s_ovf, l == 0 ? &s_G : nullptr);
+  __syncthreads();
+  if (fused && threadIdx.x == 0) {
+    *ovf = s_ovf;
+    if (G_out) *G_out = s_ovf ? ~0ull : s_G;
+  }
+}
+
+
+// Count exchange by one whole block: push this process's L count rows
+// (Cdev rows proc*L ..) into every process's mailbox, raise this process's
+// count flag there, wait for every process's flag, then copy the whole R x R
+// matrix into Cdev (where the plan and the host read it).  Returns false
+// (for every thread) if some wait timed out; Cdev is then incomplete.
+static __device__ bool ctl_counts_block(const PeerCtl& pc, uint64_t* Cdev, int L, int R) {
+  __shared__ unsigned long long se;
+  unsigned long long* mine = pc.mbox[pc.proc];
+  const int tid = threadIdx.x, P = pc.P;
+  if (tid == 0) { se = mine[0] + 1; mine[0] = se; }
+  __syncthreads();
+  const unsigned long long e = se;
+  const size_t C0 = 8 + 2 * (size_t)P, row0 = (size_t)pc.proc * L * R, n = (size_t)L * R;
+  for (size_t x = tid; x < (size_t)P * n; x += blockDim.x) {
+    const size_t p = x / n, i = x - p * n;
+    pc.mbox[p][C0 + row0 + i] = Cdev[row0 + i];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence_system();  // the rows before the flags, at every peer
+    for (int p = 0; p < P; ++p) st_relaxed_sys(&pc.mbox[p][8 + pc.proc], e);
+  }
+  bool ok = true;
+  for (int p = tid; p < P; p += blockDim.x) ok = spin_until(pc, &mine[8 + p], e) && ok;
+  if (!__syncthreads_and(ok)) return false;
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  for (size_t x = tid; x < (size_t)R * R; x += blockDim.x)
+    Cdev[x] = *reinterpret_cast<volatile unsigned long long*>(&mine[C0 + x]);
+  __syncthreads();
+  return true;
+}
+
+
+
 // Dynamic shared memory above 48 KiB is opted into per kernel AND per device
 // (every device has its own context): remember the largest grant per pair.
 inline cudaError_t ensure_smem(const void* fn, int bytes, int device) {
@@ -174,7 +260,10 @@ inline cudaError_t ensure_smem(const void* fn, int bytes, int device) {
 
 // The warp-tile histogram serves any 128/256-item tiling with R <= 8.
 inline bool hist_w_ok(uint32_t tile, int R) { return (tile == 128 || tile == 256) && R <= 8; }
-int launch_hist_w(Ctx* c, int nsm);
+// plan_mode / G_out / pc: k_scan's arguments, used when the histogram also
+// does the scan (small forwards, hist_w_fuses_scan).
+int launch_hist_w(Ctx* c, int nsm, int plan_mode, unsigned long long* G_out, PeerCtl pc);
+bool hist_w_fuses_scan(const Ctx* c);
 int launch_scatter_w(Ctx* c, bool fused, bool wrap, PeerCtl pc, int nsm);
 
 }  // namespace rafi_impl

@@ -186,7 +186,10 @@ uint32_t choose_tile_perm(uint64_t item_bytes, int R);
 bool perm_supported(uint64_t item_bytes);
 size_t perm_smem_bytes(uint32_t tile, uint64_t item_bytes, int R);
 int launch_emit_bulk(Ctx* c, int local, const uint8_t* items, const int32_t* dests, uint64_t n);
-int launch_hist(Ctx* c);
+// a2 + a3: histogram, then scan (+ plan, + peer count exchange).  On small
+// warp-tile forwards launch_hist also scans (and launch_scan is a no-op), so
+// both take the scan's arguments.
+int launch_hist(Ctx* c, int plan_mode, unsigned long long* G_out = nullptr, bool ctl = false);
 int launch_scan(Ctx* c, int plan_mode, unsigned long long* G_out = nullptr, bool ctl = false);
 int launch_scatter(Ctx* c, bool fused, bool wrap);
 int launch_plan(Ctx* c, bool fused, unsigned long long* G_out = nullptr);

@@ -70,13 +70,30 @@ __host__ __device__ constexpr uint32_t hist_w_smem(int L) {
   return kHWarps * (kHStages * HistBlk<kWT>::kBlk * 4 + 64) + 8 * (2 * L + 1);
 }
 
+// Small forwards (at most kFuseBlocks scan blocks per rank by capacity): the
+// histogram's last CTA also does k_scan's work -- the second scan level, the
+// count-matrix rows, the round's counters, and (PEER control) the count
+// exchange and the plan -- so a forward is two kernels instead of three.
+constexpr uint64_t kFuseBlocks = 64;
+
+struct ScanFuse {
+  int on;                       // 0: k_scan runs as its own launch
+  int grank0, plan_mode;        // as k_scan: plan_mode 0 none, 1 staged, 2 FUSED
+  uint64_t* Cmat;
+  unsigned* done;               // last-CTA counter
+  uint64_t* dst_off;
+  uint64_t* num_in;
+  int* ovf;
+  unsigned long long* G_out;
+};
+
 // Persistent: warp w of CTA x takes scan blocks gw, gw + stride, ... (flat
 // over the local ranks), each streamed into its private kHStages-deep ring by
 // one 8-KiB TMA bulk load.  Scan block b of local rank l = tiles 8b .. 8b+7.
 template <int kWT>
 __global__ void __launch_bounds__(kHWarps * 32, 1) k_hist_w(const RankDev* __restrict__ rk,
-                                                             const CtrlDev* __restrict__ ctrl, int L, int R,
-                                                             uint64_t cap) {
+                                                             CtrlDev* __restrict__ ctrl, int L, int R,
+                                                             uint64_t cap, ScanFuse fz, PeerCtl pc) {
   constexpr uint32_t kHBlk = HistBlk<kWT>::kBlk;
   extern __shared__ __align__(128) uint8_t smem[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -198,6 +215,43 @@ __global__ void __launch_bounds__(kHWarps * 32, 1) k_hist_w(const RankDev* __res
         if ((lane >> 2) == kHistTilesPerCta - 1) rk[l].H[(uint64_t)d * nblk + b] = (tot >> (16 * h)) & 0xffffu;
       }
     }
+  }
+  if (!fz.on || !last_block(fz.done)) return;
+  // k_scan's work, by the last CTA (every CTA's O/H writes are visible:
+  // last_block fences before counting itself in): per (rank, destination)
+  // the exclusive prefix of H over the <= kFuseBlocks scan blocks, in place,
+  // and the count-matrix row; then the round's counters
+  for (int x = threadIdx.x; x < L * R; x += blockDim.x) {
+    const int l = x / R, d = x - l * R;
+    const uint64_t tiles = (nl[l] + kWT - 1) / kWT;
+    const uint64_t nblk = (tiles + kHistTilesPerCta - 1) / kHistTilesPerCta;
+    uint32_t* H = rk[l].H + (uint64_t)d * nblk;
+    uint64_t acc = 0;
+    for (uint64_t b = 0; b < nblk; ++b) {
+      const uint32_t v = H[b];
+      H[b] = (uint32_t)acc;
+      acc += v;
+    }
+    fz.Cmat[(uint64_t)(fz.grank0 + l) * R + d] = acc;
+    if (d == 0) {
+      CtrlDev& c = ctrl[l];
+      c.n_out = nl[l];
+      c.dropped = c.ctr - nl[l];
+      c.invalid_last = c.invalid;
+    }
+  }
+  __syncthreads();
+  if (fz.plan_mode || pc.mbox) {
+    if (pc.mbox && !ctl_counts_block(pc, fz.Cmat, L, R)) {
+      // a peer never arrived: move nothing this round (the host reports RAFI_ERR_TIMEOUT)
+      if (threadIdx.x == 0) {
+        *fz.ovf = 2;
+        if (fz.G_out) *fz.G_out = ~0ull;
+      }
+      return;
+    }
+    if (fz.plan_mode)
+      plan_all(fz.Cmat, fz.grank0, L, R, cap, fz.plan_mode == 2, fz.dst_off, fz.num_in, fz.ovf, fz.G_out);
   }
 }
 
@@ -513,19 +567,34 @@ uint32_t warp_tile_for(uint64_t B, int R, int L) {
   return 0;
 }
 
+bool hist_w_fuses_scan(const Ctx* c) {
+  return (c->max_tiles + kHistTilesPerCta - 1) / kHistTilesPerCta <= kFuseBlocks;
+}
+
 template <int kWT>
-static int launch_hist_t(Ctx* c, int nsm) {
+static int launch_hist_t(Ctx* c, int nsm, int plan_mode, unsigned long long* G_out, PeerCtl pc) {
   const uint32_t sm = hist_w_smem<kWT>(c->L);
   RAFI_CK_CUDA(ensure_smem((const void*)k_hist_w<kWT>, (int)sm, c->device));
   const uint64_t blocks = (c->max_tiles + kHistTilesPerCta - 1) / kHistTilesPerCta * (uint64_t)c->L;
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)nsm, (blocks + kHWarps - 1) / kHWarps));
-  k_hist_w<kWT><<<grid, kHWarps * 32, sm, c->stream>>>(c->rank_dev, c->ctrl, c->L, c->R, c->cap);
+  ScanFuse fz;
+  fz.on = hist_w_fuses_scan(c) ? 1 : 0;
+  fz.grank0 = c->proc * c->L;
+  fz.plan_mode = plan_mode;
+  fz.Cmat = c->Cdev;
+  fz.done = c->done_dev;  // k_scan's last-block counter (k_scan is not launched then)
+  fz.dst_off = c->off_dev;
+  fz.num_in = c->plan_dev;
+  fz.ovf = c->ovf_dev;
+  fz.G_out = G_out;
+  k_hist_w<kWT><<<grid, kHWarps * 32, sm, c->stream>>>(c->rank_dev, c->ctrl, c->L, c->R, c->cap, fz, pc);
   RAFI_CK_CUDA(cudaGetLastError());
   return RAFI_OK;
 }
 
-int launch_hist_w(Ctx* c, int nsm) {
-  return c->tile == 128 ? launch_hist_t<128>(c, nsm) : launch_hist_t<256>(c, nsm);
+int launch_hist_w(Ctx* c, int nsm, int plan_mode, unsigned long long* G_out, PeerCtl pc) {
+  return c->tile == 128 ? launch_hist_t<128>(c, nsm, plan_mode, G_out, pc)
+                        : launch_hist_t<256>(c, nsm, plan_mode, G_out, pc);
 }
 
 template <typename U, int kWT>
