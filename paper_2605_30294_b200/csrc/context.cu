@@ -293,11 +293,14 @@ static int resolve_scatter(Ctx* c) {
   int x = c->scatter;
   if (x == RAFI_SCATTER_AUTO) {
     // BULK where the scatter pushes runs of 24 B and larger items to NVLink
-    // peers (measured faster there at N=2 and N=4 by 0-13%, DESIGN.md section
-    // 6); THREADS for local HBM (faster at every item size) and for 16-B items
-    // (N=2: 87 vs 66 G items/s; N=4: 130 vs 133)
+    // peers in large rounds (measured faster there at N=2 and N=4 by 0-13%,
+    // DESIGN.md section 6); THREADS for local HBM (faster at every item size),
+    // for 16-B items (N=2: 87 vs 66 G items/s; N=4: 130 vs 133), and for
+    // queues below 2^19 items, where the warp tiles' two-kernel forward wins
+    // on latency (N=2, 4096 items: 61 vs 66 us blocking, 41 vs 43 us graph)
     const bool remote_push = c->nprocs > 1 && c->exchange_eff == RAFI_EXCHANGE_FUSED;
-    x = remote_push && c->B >= 24 && perm_supported(c->B) && perm_smem_bytes(256, c->B, c->R) <= kMaxSmem
+    x = remote_push && c->B >= 24 && c->cap >= (1ull << 19) && perm_supported(c->B) &&
+                perm_smem_bytes(256, c->B, c->R) <= kMaxSmem
             ? RAFI_SCATTER_BULK
             : RAFI_SCATTER_THREADS;
   }
