@@ -138,8 +138,8 @@ typedef struct {
                                       that is not a multiple of 4 or a tile that does not fit */
 
 #define RAFI_SCATTER_AUTO 0        /* BULK when the scatter pushes runs of items of >= 24 B to NVLink peers
-                                      (FUSED over several processes) and BULK is supported, else THREADS
-                                      (measured winners) */
+                                      (FUSED over several processes), the queues hold >= 2^19 items and
+                                      BULK is supported, else THREADS (measured winners) */
 #define RAFI_SCATTER_THREADS 1     /* threads store every run with coalesced stores.  R <= 8 and
                                       item_bytes % 4 == 0: one warp per 128/256-item tile, 16/8/4-B item
                                       units.  Otherwise block tiles: 16/8/4/2/1-B item units, or, for 4-B
