@@ -54,3 +54,31 @@ def _worker(rank, world, port, cap, n):
 def test_gloo_world2_plan(cap):
     import torch.multiprocessing as mp
     mp.spawn(_worker, args=(2, _free_port(), cap, 1000), nprocs=2, join=True)
+
+
+def _worker_allgather(rank, world, port):
+    import ctypes
+
+    import torch.distributed as dist
+
+    from paper_2605_30294_b200 import rafi
+
+    dist.init_process_group("gloo", init_method=port, rank=rank, world_size=world)
+    fn = rafi.torch_allgather()
+    for nbytes in (0, 1, 13, 4096):
+        send = (ctypes.c_uint8 * max(nbytes, 1))(*[(rank * 31 + i) & 0xFF for i in range(max(nbytes, 1))])
+        recv = (ctypes.c_uint8 * max(world * nbytes, 1))()
+        assert fn(None, ctypes.addressof(send), ctypes.addressof(recv), nbytes) == 0
+        for p in range(world):
+            got = bytes(recv[p * nbytes:(p + 1) * nbytes])
+            assert got == bytes((p * 31 + i) & 0xFF for i in range(nbytes)), (p, nbytes)
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_bootstrap_allgather():
+    """rafi.torch_allgather -- the host all-gather behind rafi_create_boot and
+    HOST control (the paper's MPI host transport) -- on a gloo
+    world of 2: every process receives every process's bytes in rank order,
+    for empty, odd-sized and page-sized payloads."""
+    import torch.multiprocessing as mp
+    mp.spawn(_worker_allgather, args=(2, _free_port()), nprocs=2, join=True)
