@@ -55,19 +55,36 @@ constexpr uint32_t kWSmemMax = 227u * 1024u;
 
 // ---------------------------------------------------------------- a2 histogram
 
-constexpr int kHWarps = 8;      // warps per CTA (one CTA per SM)
-constexpr int kHStages = 3;     // TMA ring depth per warp
+// Warps per CTA (one CTA per SM) and TMA ring depth per warp, by tile size.
+// Measured at R = 8 (fraction of the copy peak, gpurun_out/r02pp_sweep.jsonl):
+// 256-item tiles 8 x 3: 0.72, 16 x 1: 0.75, 12 x 1: 0.77; 128-item tiles
+// 8 x 3: 0.51, 12 x 2: 0.66, 16 x 1 or 3: 0.74 -- warps in flight, not ring
+// depth, hide the load latency here.
+#ifndef RAFI_H_WARPS_256
+#define RAFI_H_WARPS_256 12
+#endif
+#ifndef RAFI_H_STAGES_256
+#define RAFI_H_STAGES_256 1
+#endif
+#ifndef RAFI_H_WARPS_128
+#define RAFI_H_WARPS_128 16
+#endif
+#ifndef RAFI_H_STAGES_128
+#define RAFI_H_STAGES_128 1
+#endif
 
 // dests per scan block: 8 tiles (2048 = 8 KiB at 256-item tiles, 1024 at 128)
 template <int kWT>
 struct HistBlk {
   static constexpr uint32_t kBlk = kWT * kHistTilesPerCta;
   static constexpr int kPerTile = kWT / 128;  // int4 per lane per tile
+  static constexpr int kStages = kWT == 256 ? RAFI_H_STAGES_256 : RAFI_H_STAGES_128;  // TMA ring depth per warp
+  static constexpr int kWarps = kWT == 256 ? RAFI_H_WARPS_256 : RAFI_H_WARPS_128;      // warps per CTA
 };
 
 template <int kWT>
 __host__ __device__ constexpr uint32_t hist_w_smem(int L) {
-  return kHWarps * (kHStages * HistBlk<kWT>::kBlk * 4 + 64) + 8 * (2 * L + 1);
+  return HistBlk<kWT>::kWarps * (HistBlk<kWT>::kStages * HistBlk<kWT>::kBlk * 4 + 64) + 8 * (2 * L + 1);
 }
 
 // Small forwards (at most kFuseBlocks scan blocks per rank by capacity): the
@@ -91,10 +108,12 @@ struct ScanFuse {
 // over the local ranks), each streamed into its private kHStages-deep ring by
 // one 8-KiB TMA bulk load.  Scan block b of local rank l = tiles 8b .. 8b+7.
 template <int kWT>
-__global__ void __launch_bounds__(kHWarps * 32, 1) k_hist_w(const RankDev* __restrict__ rk,
+__global__ void __launch_bounds__(HistBlk<kWT>::kWarps * 32, 1) k_hist_w(const RankDev* __restrict__ rk,
                                                              CtrlDev* __restrict__ ctrl, int L, int R,
                                                              uint64_t cap, ScanFuse fz, PeerCtl pc) {
   constexpr uint32_t kHBlk = HistBlk<kWT>::kBlk;
+  constexpr int kHStages = HistBlk<kWT>::kStages;
+  constexpr int kHWarps = HistBlk<kWT>::kWarps;
   extern __shared__ __align__(128) uint8_t smem[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* my = smem + (size_t)w * (kHStages * kHBlk * 4 + 64);
@@ -576,6 +595,7 @@ static int launch_hist_t(Ctx* c, int nsm, int plan_mode, unsigned long long* G_o
   const uint32_t sm = hist_w_smem<kWT>(c->L);
   RAFI_CK_CUDA(ensure_smem((const void*)k_hist_w<kWT>, (int)sm, c->device));
   const uint64_t blocks = (c->max_tiles + kHistTilesPerCta - 1) / kHistTilesPerCta * (uint64_t)c->L;
+  constexpr int kHWarps = HistBlk<kWT>::kWarps;
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)nsm, (blocks + kHWarps - 1) / kHWarps));
   ScanFuse fz;
   fz.on = hist_w_fuses_scan(c) ? 1 : 0;
