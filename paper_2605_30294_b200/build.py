@@ -108,7 +108,6 @@ def build_tools() -> list:
 VARIANTS = {  # scatter tuning experiments: name -> defines (build with --variants)
     "ilp2": ["RAFI_SCATTER_ILP=2"],
     "ilp8": ["RAFI_SCATTER_ILP=8"],
-    "w3": ["RAFI_W_STAGES=3"],
     "u4": ["RAFI_W_UNROLL=4"],
     "debug": ["RAFI_DEBUG_BOUNDS=1"],  # device-side bounds checks (scripts/sanitize_cases.py)
 }

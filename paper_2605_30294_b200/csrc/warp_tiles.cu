@@ -38,13 +38,9 @@
 namespace rafi_impl {
 
 // tuning (build-time; paper_2605_30294_b200/build.py variants)
-#ifndef RAFI_W_STAGES
-#define RAFI_W_STAGES 2
-#endif
 #ifndef RAFI_W_UNROLL
 #define RAFI_W_UNROLL 8
 #endif
-constexpr int kWStages = RAFI_W_STAGES;   // TMA ring depth per warp
 constexpr int kWMaxWarps = 16;
 constexpr int kWUnroll = RAFI_W_UNROLL;   // independent unit moves in flight per lane
 #ifndef RAFI_W_UNROLL_NARROW
@@ -277,7 +273,7 @@ __global__ void __launch_bounds__(HistBlk<kWT>::kWarps * 32, 1) k_hist_w(const R
 // ---------------------------------------------------------------- a4 scatter
 
 // Shared memory of k_scatter_w: `warps` private warp regions, then the CTA's
-// tile map.  Warp region: kWStages x (items, dests), src_of[256] (u16), the
+// tile map.  Warp region: stages_for(B) x (items, dests), src_of[256] (u16), the
 // chunk x destination table T[8][8] (u32), rs[R + 1] (u32), gb[R] (u64),
 // mbarriers.
 struct WarpLayout {
@@ -286,7 +282,14 @@ struct WarpLayout {
   uint32_t off_cta, total;
 };
 
+// TMA ring depth per warp: two stages for 16-byte-unit items up to 64 B;
+// one (so twice the warps fit) for narrower units and for large items --
+// there warps in flight beat ring depth (at R = 8: 44 B 0.75 -> 0.83,
+// 128 B 0.90 -> 0.94, but 48 B 0.95 -> 0.89; gpurun_out/r02rr_sweep.jsonl).
+static int stages_for(uint64_t B) { return (B % 16 == 0 && B <= 64) ? 2 : 1; }
+
 static WarpLayout warp_layout(uint32_t kWT, uint64_t B, int R, int L, int warps) {
+  const int kWStages = stages_for(B);
   auto al = [](uint64_t x, uint64_t a) { return (uint32_t)((x + a - 1) / a * a); };
   WarpLayout s;
   s.stage_items = al((uint64_t)kWT * B, 16);
@@ -321,7 +324,7 @@ __device__ __forceinline__ void st_global(uint32_t* p, const uint32_t& v) {
   asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <typename U, int kWT>
+template <typename U, int kWT, int kWStages>
 __global__ void __launch_bounds__(kWMaxWarps * 32, 1)
 k_scatter_w(const RankDev* __restrict__ rk, const CtrlDev* __restrict__ ctrl, uint8_t* const* __restrict__ dst_table,
             const uint64_t* __restrict__ dst_off, const int* __restrict__ ovf, int L, int R, uint64_t cap, int cur,
@@ -574,15 +577,16 @@ bool warp_tiles_ok(uint32_t tile, uint64_t B, int R, int L) {
   return (tile == 128 || tile == 256) && R <= 8 && B % 4 == 0 && warps_that_fit(tile, B, R, L) >= 2;
 }
 
-// 256-item tiles while they leave >= 6 warps per SM (items <= 64 B), else
-// 128 (twice the warps; 96 B: 0.90 vs 0.82 of HBM, 128 B: 0.88 vs 0.72 --
-// at <= 64 B the 256-item tiles win, 0.93-0.95 vs 0.84-0.89, and their
-// histogram streams 8-KiB blocks: 0.71 vs 0.50, gpurun_out/r02n_sweep.jsonl);
-// 0 = the warp-tile path does not apply.
+// 256-item tiles while they leave >= 6 warps per SM (with stages_for(): up to
+// 128-B items), else 128 while >= 4 warps fit (up to 256 B).  Measured with
+// two stages everywhere (gpurun_out/r02n_sweep.jsonl): at <= 64 B the
+// 256-item tiles win, 0.93-0.95 vs 0.84-0.89, and their histogram streams
+// 8-KiB blocks; with one stage, 128-B items at 256 items per tile reach 0.94
+// (r02ss).  0 = the warp-tile path does not apply.
 uint32_t warp_tile_for(uint64_t B, int R, int L) {
   if (!(R <= 8 && B % 4 == 0)) return 0;
   if (warps_that_fit(256, B, R, L) >= 6) return 256;
-  if (warps_that_fit(128, B, R, L) >= 2) return 128;
+  if (warps_that_fit(128, B, R, L) >= 4) return 128;  // else (items > 256 B) block tiles
   return 0;
 }
 
@@ -617,11 +621,11 @@ int launch_hist_w(Ctx* c, int nsm, int plan_mode, unsigned long long* G_out, Pee
                         : launch_hist_t<256>(c, nsm, plan_mode, G_out, pc);
 }
 
-template <typename U, int kWT>
+template <typename U, int kWT, int kS>
 static int launch_w(Ctx* c, bool fused, bool wrap, PeerCtl pc, int nsm) {
   const int warps = warps_that_fit(kWT, c->B, c->R, c->L);
   const WarpLayout lay = warp_layout(kWT, c->B, c->R, c->L, warps);
-  auto k = k_scatter_w<U, kWT>;
+  auto k = k_scatter_w<U, kWT, kS>;
   RAFI_CK_CUDA(ensure_smem((const void*)k, (int)lay.total, c->device));
   const uint32_t UPI = (uint32_t)(c->B / sizeof(U));
   const uint64_t tiles_all = c->max_tiles * (uint64_t)c->L;
@@ -639,13 +643,16 @@ static int launch_w(Ctx* c, bool fused, bool wrap, PeerCtl pc, int nsm) {
 // from the words of the one or two items it covers -- was measured and
 // dropped: 44 B at R = 8, 0.53 vs 0.76 of HBM with plain 4-byte units.)
 int launch_scatter_w(Ctx* c, bool fused, bool wrap, PeerCtl pc, int nsm) {
+  const bool two = stages_for(c->B) == 2;  // only for 16-byte units
   if (c->tile == 128)
-    return c->B % 16 == 0  ? launch_w<uint4, 128>(c, fused, wrap, pc, nsm)
-           : c->B % 8 == 0 ? launch_w<uint2, 128>(c, fused, wrap, pc, nsm)
-                           : launch_w<uint32_t, 128>(c, fused, wrap, pc, nsm);
-  return c->B % 16 == 0  ? launch_w<uint4, 256>(c, fused, wrap, pc, nsm)
-         : c->B % 8 == 0 ? launch_w<uint2, 256>(c, fused, wrap, pc, nsm)
-                         : launch_w<uint32_t, 256>(c, fused, wrap, pc, nsm);
+    return c->B % 16 == 0  ? (two ? launch_w<uint4, 128, 2>(c, fused, wrap, pc, nsm)
+                                  : launch_w<uint4, 128, 1>(c, fused, wrap, pc, nsm))
+           : c->B % 8 == 0 ? launch_w<uint2, 128, 1>(c, fused, wrap, pc, nsm)
+                           : launch_w<uint32_t, 128, 1>(c, fused, wrap, pc, nsm);
+  return c->B % 16 == 0  ? (two ? launch_w<uint4, 256, 2>(c, fused, wrap, pc, nsm)
+                                : launch_w<uint4, 256, 1>(c, fused, wrap, pc, nsm))
+         : c->B % 8 == 0 ? launch_w<uint2, 256, 1>(c, fused, wrap, pc, nsm)
+                         : launch_w<uint32_t, 256, 1>(c, fused, wrap, pc, nsm);
 }
 
 }  // namespace rafi_impl

@@ -501,7 +501,7 @@ def test_warp_tiles_many_rounds_empty_ranks_and_resize(R):
     k_scatter_w) over many forwards on one context: sizes that change every
     round (empty ranks, partial scan blocks and tiles), a resize between
     rounds (new H/O arrays), every round P1-exact against the oracle."""
-    B = 48 if R != 3 else 96   # 256- and 128-item warp tiles
+    B = 48 if R != 3 else 256   # 256- and 128-item warp tiles
     sizes = [[5000, 0, 70001], [0, 0, 0], [2048, 2047, 1], [300000, 4096, 0], [1, 0, 123457]]
     with _ctx(B, 300000, R) as ctx:
         assert ctx.get_option(rafi.OPT_TILE) == (256 if B == 48 else 128)
@@ -514,12 +514,14 @@ def test_warp_tiles_many_rounds_empty_ranks_and_resize(R):
             p1_forward(ctx, R, B)
 
 
-@pytest.mark.parametrize("B,L,tile", [(16, 8, 256), (44, 8, 256), (48, 8, 256), (64, 8, 256), (96, 8, 128),
-                                      (128, 8, 128), (48, 1, 256), (48, 9, None), (42, 4, None), (520, 2, None)])
+@pytest.mark.parametrize("B,L,tile", [(16, 8, 256), (44, 8, 256), (48, 8, 256), (64, 8, 256), (96, 8, 256),
+                                      (128, 8, 256), (256, 8, 128), (48, 1, 256), (48, 9, None), (42, 4, None),
+                                      (520, 2, None)])
 def test_automatic_tile_choice(B, L, tile):
     """The automatic binning tile: warp tiles of 256
-    items while >= 6 warp regions fit (items <= 64 B), 128 above; block tiles
-    (256 * 2^k) for R > 8 or item sizes that are not a multiple of 4 B."""
+    items while >= 6 warp regions fit (with one TMA stage per warp from 96 B
+    up: up to 128-B items), 128 above; block tiles (256 * 2^k) for R > 8 or
+    item sizes that are not a multiple of 4 B."""
     with _ctx(B, 50000, L) as ctx:
         assert ctx.get_option(rafi.OPT_SCATTER) == rafi.SCATTER_THREADS
         t = ctx.get_option(rafi.OPT_TILE)
