@@ -282,11 +282,12 @@ struct WarpLayout {
   uint32_t off_cta, total;
 };
 
-// TMA ring depth per warp: two stages for 16-byte-unit items up to 64 B;
-// one (so twice the warps fit) for narrower units and for large items --
+// TMA ring depth per warp: two stages for 16-byte-unit items up to 96 B;
+// one (so twice the warps fit) for narrower units and for larger items --
 // there warps in flight beat ring depth (at R = 8: 44 B 0.75 -> 0.83,
-// 128 B 0.90 -> 0.94, but 48 B 0.95 -> 0.89; gpurun_out/r02rr_sweep.jsonl).
-static int stages_for(uint64_t B) { return (B % 16 == 0 && B <= 64) ? 2 : 1; }
+// 128 B 0.90 -> 0.94, but 48 B 0.95 -> 0.89 and 96 B 0.94 -> 0.92;
+// gpurun_out/r02rr_sweep.jsonl, r02ss_sweep.jsonl).
+static int stages_for(uint64_t B) { return (B % 16 == 0 && B <= 96) ? 2 : 1; }
 
 static WarpLayout warp_layout(uint32_t kWT, uint64_t B, int R, int L, int warps) {
   const int kWStages = stages_for(B);

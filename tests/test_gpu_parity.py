@@ -514,14 +514,14 @@ def test_warp_tiles_many_rounds_empty_ranks_and_resize(R):
             p1_forward(ctx, R, B)
 
 
-@pytest.mark.parametrize("B,L,tile", [(16, 8, 256), (44, 8, 256), (48, 8, 256), (64, 8, 256), (96, 8, 256),
+@pytest.mark.parametrize("B,L,tile", [(16, 8, 256), (44, 8, 256), (48, 8, 256), (64, 8, 256), (96, 8, 128),
                                       (128, 8, 256), (256, 8, 128), (48, 1, 256), (48, 9, None), (42, 4, None),
                                       (520, 2, None)])
 def test_automatic_tile_choice(B, L, tile):
     """The automatic binning tile: warp tiles of 256
-    items while >= 6 warp regions fit (with one TMA stage per warp from 96 B
-    up: up to 128-B items), 128 above; block tiles (256 * 2^k) for R > 8 or
-    item sizes that are not a multiple of 4 B."""
+    items while >= 6 warp regions fit (two TMA stages per warp up to 96 B,
+    one above: 16-64 B and 128 B), 128 otherwise; block tiles (256 * 2^k) for
+    R > 8, items over 256 B or item sizes that are not a multiple of 4 B."""
     with _ctx(B, 50000, L) as ctx:
         assert ctx.get_option(rafi.OPT_SCATTER) == rafi.SCATTER_THREADS
         t = ctx.get_option(rafi.OPT_TILE)
